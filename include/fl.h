@@ -1,0 +1,215 @@
+/*
+ * fl.h — C-ABI of the B200-native FedAvg-round engine (Pollen, arXiv 2306.17453).
+ *
+ * One simulated FedAvg round (§2.1): the server sends θ_g to
+ * every cohort client, each client runs E epochs of minibatch SGD on its own
+ * ragged dataset, and the server forms the sample-count-weighted mean
+ * (Eq. 1-2).  Around it: Pollen's push-based placement of the whole
+ * cohort onto workers in one step (§4.1, §5), here one
+ * worker = one GPU = one process (rank).
+ *
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; readings Ax =
+ * DESIGN.md §"Readings of the paper".
+ *
+ * Conventions (all entry points):
+ *  - Every function returns fl_status; no exception or abort crosses the ABI.
+ *  - Host pointers are borrowed for the duration of the call unless stated.
+ *  - Device pointers must be on cfg.device; borrowed, never freed by the library.
+ *  - Outputs are caller-allocated.
+ *  - Validation errors return FL_ERR_INVALID and leave the context unchanged.
+ *  - A CUDA/NCCL failure latches the context into a FAILED state; every later
+ *    call on it returns FL_ERR_STATE.  fl_last_error() describes the cause.
+ *  - Determinism: the same inputs give bit-identical plans and segment
+ *    offsets on every rank and every run; aggregation is deterministic for a
+ *    fixed world size (fixed client order, fp64 accumulation).
+ *  - There is no CPU fallback: entry points that compute need a CUDA device
+ *    (sm_100a) and return FL_ERR_CUDA without one.  Only fl_place_plan,
+ *    fl_pack_plan, fl_n_params and fl_abi_version are host-only.
+ */
+#ifndef FL_B200_H
+#define FL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FL_ABI_VERSION 1u
+
+typedef enum {
+  FL_OK = 0,
+  FL_ERR_INVALID = 1,     /* bad argument; ctx unchanged */
+  FL_ERR_STATE = 2,       /* call out of order, or ctx FAILED */
+  FL_ERR_OOM = 3,         /* device allocation failed */
+  FL_ERR_CUDA = 4,        /* CUDA runtime/launch error (or no device) */
+  FL_ERR_NCCL = 5,        /* NCCL missing or failed */
+  FL_ERR_EMPTY = 6,       /* total sample count is 0 */
+  FL_ERR_UNSUPPORTED = 7  /* model/option not built in this version */
+} fl_status;
+
+typedef enum {
+  FL_MODEL_LOGREG = 0,     /* 784 -> 10 softmax regression (BASELINE configs[0]) */
+  FL_MODEL_CNN_CIFAR = 1,  /* McMahan CNN, 3x32x32, 'same' padding (reading A10) */
+  FL_MODEL_CNN_SPEECH = 2, /* conv+MLP on 1x40x98 (reading A10) */
+  FL_MODEL_CHAR_LSTM = 3   /* LEAF char-LSTM, embed 8, 2x256, seq 80 */
+} fl_model;
+
+/* Placement policies, §5 L358-388.  Clients are ordered by batch
+ * count m = ceil(n/B) descending, ties by client id ascending (reading A15);
+ * BU/LB append each client to the worker with the lowest load, ties to the
+ * lowest worker id.  BU load = Σ m (L370); LB load = Σ Eq. 3
+ * prediction a·m + b·ln(c·m) + d, clamped to >= 1e-12 (L380-388). */
+typedef enum { FL_PLACE_BU = 0, FL_PLACE_LB = 1, FL_PLACE_RR = 2, FL_PLACE_SRR = 3 } fl_policy;
+
+typedef struct fl_ctx fl_ctx; /* opaque; owns device buffers, stream, events, NCCL comm */
+
+typedef struct {
+  uint32_t abi_version;     /* must be FL_ABI_VERSION */
+  int32_t model;            /* fl_model */
+  int32_t batch_size;       /* B >= 1 */
+  int32_t local_epochs;     /* E >= 1 */
+  float lr;                 /* η >= 0: plain SGD, no momentum / decay (reading A8) */
+  int32_t shuffle;          /* 0: stored order; 1: SplitMix64 Fisher-Yates per (seed, round, id, epoch) (A5) */
+  uint64_t seed;
+  int64_t min_samples;      /* clients with n < min_samples are rejected (P:447 exclusion, reading A6); >= 1 */
+  int32_t rank, world_size; /* one process per GPU; 0 <= rank < world_size */
+  int32_t device;           /* CUDA ordinal of this rank */
+  const uint8_t* nccl_unique_id; /* 128 bytes from fl_nccl_unique_id() on rank 0; NULL iff world_size == 1 */
+  int32_t math;             /* 0: tensor cores (TF32, tcgen05) where built; 1: FP32 SIMT everywhere */
+  void* stream;             /* optional borrowed cudaStream_t; NULL: the ctx creates its own */
+} fl_config;
+
+/* The client population, client-id order.  Sample rows of client k
+ * are rows [Σ_{j<k} n_j, Σ_{j<=k} n_j) of x / y.
+ *   logreg/CNN/speech: x = float32[rows][feature_dim] (CNN: C,H,W order), y = int32 class
+ *   LSTM:              x = uint8[rows][80] characters, y = int32 next character
+ * on_device = 1: x, y are device pointers on cfg.device, borrowed for the ctx lifetime.
+ * on_device = 0: x, y are host pointers, borrowed for the ctx lifetime; each
+ *   round copies this rank's cohort rows host->device (the end-to-end path). */
+typedef struct {
+  int64_t n_clients;
+  const int64_t* n_samples; /* [n_clients], host, copied at init */
+  int32_t feature_dim;      /* 784, 3072, 3920 or 80 */
+  const void* x;
+  const int32_t* y;
+  int32_t on_device;
+} fl_population;
+
+/* Device-time statistics of the last round on this rank (CUDA events on the ctx stream). */
+typedef struct {
+  double round_ms;      /* fl_round entry (plan on host) to θ_new resident on this GPU */
+  double place_ms;      /* host placement + packing (wall) */
+  double stage_ms;      /* cohort gather / host->device staging */
+  double train_ms;      /* local SGD of this rank's clients (device) */
+  double agg_ms;        /* fused per-GPU accumulation + (NCCL reduce) + finalize */
+  double allreduce_ms;  /* NCCL part of agg_ms (0 when world_size == 1) */
+  double client_updates_per_s; /* clients_total / round_ms (this rank's clock) */
+  int64_t clients_total, clients_local;
+  int64_t samples_total, samples_local;
+  int64_t steps_local;  /* Σ E·m over this rank's clients */
+  int64_t waves;        /* max E·m over this rank's clients (critical path in SGD steps) */
+  int64_t h2d_bytes;    /* host->device bytes copied this round */
+  int64_t kernels;      /* kernel launches this round */
+} fl_round_stats;
+
+uint32_t fl_abi_version(void);
+
+/* Canonical parameter count P of a model (torch state_dict order, §8c.2 of SURVEY):
+ * logreg 7,850; CNN 2,156,490; speech 3,993,507; LSTM 819,920.  0 if unknown. */
+int64_t fl_n_params(int32_t model);
+
+/* ---- host-only planning (no device needed) -------------------------------- */
+/* Placement (§5): cohort_ids[n_cohort] distinct ids < n_clients; n_samples[n_clients].
+ * Writes out_ids[n_cohort] grouped by worker in assignment order (largest first for
+ * SRR/BU/LB) and out_off[world_size+1] CSR offsets.  lb_coef = (a,b,c,d) for LB,
+ * ignored otherwise.  FL_ERR_INVALID on unknown/duplicate id, n_cohort > n_clients,
+ * world_size < 1, batch_size < 1, n_samples < 1 of a cohort member, LB without coef. */
+fl_status fl_place_plan(int32_t policy, const int64_t* cohort_ids, int64_t n_cohort,
+                        const int64_t* n_samples, int64_t n_clients, int32_t batch_size,
+                        int32_t world_size, const double* lb_coef,
+                        int64_t* out_ids, int64_t* out_off);
+
+/* Ragged packer for one worker list ids[n]: seg_off[n+1] prefix sums of
+ * n_samples in list order; steps[n] = E·ceil(n_k/B). */
+fl_status fl_pack_plan(const int64_t* ids, int64_t n, const int64_t* n_samples, int64_t n_clients,
+                       int32_t batch_size, int32_t local_epochs, int64_t* seg_off, int64_t* steps);
+
+/* ---- context ---------------------------------------------------------------- */
+/* Writes 128 bytes of a fresh NCCL unique id (call on rank 0, broadcast to others). */
+fl_status fl_nccl_unique_id(uint8_t* out128);
+
+/* global_params: host float32[n_params] in canonical layout; n_params must equal
+ * fl_n_params(cfg->model).  Allocates device state for the population and the
+ * largest cohort share this rank can receive (n_clients). */
+fl_status fl_round_init(const fl_config* cfg, const fl_population* pop,
+                        const float* global_params, int64_t n_params, fl_ctx** out);
+
+/* Push-based placement of a round's cohort.  Stores the plan in
+ * the ctx; out_ids / out_off may be NULL. */
+fl_status fl_place(fl_ctx* ctx, const int64_t* cohort_ids, int64_t n_cohort, int32_t policy,
+                   const double* lb_coef, int64_t* out_ids, int64_t* out_off);
+
+/* Local SGD of this rank's share of the last plan (stream-ordered, asynchronous).
+ * round_index keys the shuffle (A5).  FL_ERR_STATE if no plan. */
+fl_status fl_train_clients(fl_ctx* ctx, int32_t round_index);
+
+/* Fused per-GPU weighted accumulation S_g = Σ n_k(θ_k − θ_g) (fp64), NCCL allreduce
+ * of [S_g ‖ N_g] when world_size > 1, θ_new = fp32(θ_g + S/N) (Eq. 1-2 in delta form,
+ * reading A2).  θ_new becomes the ctx's θ_g.  out_params: nullable host float32[P]
+ * (canonical layout, synchronous copy); out_total_samples: nullable. */
+fl_status fl_aggregate(fl_ctx* ctx, float* out_params, int64_t* out_total_samples);
+
+/* fl_place + fl_train_clients + fl_aggregate, timed; stats nullable.  Asynchronous
+ * with respect to the host except for the stats event reads (it synchronises the
+ * ctx stream when stats != NULL). */
+fl_status fl_round(fl_ctx* ctx, const int64_t* cohort_ids, int64_t n_cohort, int32_t policy,
+                   const double* lb_coef, int32_t round_index, fl_round_stats* stats);
+
+/* ---- parity / test entry points ---------------------------------------------- */
+/* Weighted FedAvg of K arbitrary fp32 vectors of length P (device pointers):
+ * out = fp32(θ_g + Σ n_k(θ_k − θ_g) / Σ n_k), fp64 accumulation in index order k.
+ * theta_k: device float32[K][P]; n: host int64[K] (>= 1); theta_g, out: device float32[P]. */
+fl_status fl_fedavg_vectors(fl_ctx* ctx, const float* theta_k, const int64_t* n, int64_t K,
+                            int64_t P, const float* theta_g, float* out);
+
+/* This rank's local plan: ids[n_local] (execution order = plan order), seg_off[n_local+1],
+ * steps[n_local]; any pointer may be NULL; *n_local always written. */
+fl_status fl_get_local_plan(fl_ctx* ctx, int64_t* ids, int64_t* seg_off, int64_t* steps,
+                            int64_t* n_local);
+
+/* θ_k of a locally trained client after fl_train_clients (host float32[P], canonical). */
+fl_status fl_get_client_params(fl_ctx* ctx, int64_t client_id, float* out);
+
+/* Current θ_g (host float32[P], canonical) / replace it. */
+fl_status fl_get_global_params(fl_ctx* ctx, float* out);
+fl_status fl_set_global_params(fl_ctx* ctx, const float* params);
+
+/* Stats of the last fl_round. */
+fl_status fl_get_stats(fl_ctx* ctx, fl_round_stats* out);
+
+/* Per-kernel-class device time of the last round, for roofline reports.  Off by default:
+ * fl_set_profiling(ctx, 1) brackets every launch with CUDA events on the ctx stream (adds
+ * a small gap between launches; do not time throughput with it on).  kind indexes the
+ * classes 0 .. n-1 (names: pack, conv1_fwd, ..., fedavg_accum); FL_ERR_INVALID past the
+ * end.  flops / bytes are the ALGORITHMIC work of those launches. */
+typedef struct {
+  char name[32];
+  double ms;        /* Σ of launch durations */
+  int64_t launches;
+  double flops;     /* Σ algorithmic FLOPs */
+  double bytes;     /* Σ algorithmic HBM bytes */
+} fl_kernel_stats;
+fl_status fl_set_profiling(fl_ctx* ctx, int32_t on);
+fl_status fl_get_kernel_stats(fl_ctx* ctx, int32_t kind, fl_kernel_stats* out);
+
+/* The cudaStream_t the ctx launches on (for the caller's event timing). */
+void* fl_get_stream(fl_ctx* ctx);
+
+const char* fl_last_error(const fl_ctx* ctx); /* ctx-owned string; "" if none; NULL ctx ok */
+void fl_round_destroy(fl_ctx* ctx);           /* NULL ok */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FL_B200_H */

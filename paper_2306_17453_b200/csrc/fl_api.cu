@@ -1,0 +1,808 @@
+// fl_api.cu — the C-ABI (include/fl.h): context, staging, wave scheduling, aggregation.
+//
+// Round = place (host, §5) -> pack/stage (host tables + K3 gather) -> local SGD of every
+// local client as waves of grouped kernels (a4-a7) -> fused fp64 accumulation (K1) ->
+// NCCL allreduce of [S ‖ N] across ranks (a9) -> finalize (K2).  PAPER.md §4.1-4.4,
+// Eq. 1-2; SURVEY.md §3.3.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only; the library is dlopen'ed when world_size > 1
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <chrono>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/fl.h"
+#include "fl_host.h"
+#include "fl_internal.h"
+
+namespace flb {
+
+const char* const kKindName[K_NKINDS] = {
+    "pack", "conv1_fwd", "pool1", "conv2_fwd", "pool2", "fc1_fwd", "head_fc2_ce", "fc1_dx", "unpool2",
+    "fc1_dw_sgd", "conv2_dx", "unpool1", "conv2_dw", "conv2_dw_reduce_sgd", "conv1_dw", "conv1_dw_reduce_sgd",
+    "logreg_client", "fedavg_accum"};
+
+// ---------------------------------------------------------------- layouts
+static int64_t up32(int64_t x) { return (x + 31) / 32 * 32; }
+
+bool make_layout(int model, Layout* L) {
+  L->model = model;
+  L->canon_of.clear();
+  if (model == FL_MODEL_LOGREG) {
+    L->P = 7850;
+    L->P_pad = up32(7850);
+    L->D_in = 784;
+    L->D_pack = 784;
+    L->canon_of.assign((size_t)L->P_pad, -1);
+    for (int64_t i = 0; i < 7850; ++i) L->canon_of[(size_t)i] = i;
+    return true;
+  }
+  if (model != FL_MODEL_CNN_CIFAR && model != FL_MODEL_CNN_SPEECH) return false;
+  CnnDims& d = L->d;
+  if (model == FL_MODEL_CNN_CIFAR) { d.cin = 3; d.H0 = 32; d.W0 = 32; d.HID = 512; d.NCLS = 10; }
+  else { d.cin = 1; d.H0 = 40; d.W0 = 98; d.HID = 256; d.NCLS = 35; }
+  d.cpad = 4; d.C1 = 32; d.C2 = 64;
+  d.H1 = d.H0 / 2; d.W1 = d.W0 / 2; d.H2 = d.H1 / 2; d.W2 = d.W1 / 2;
+  d.F = d.C2 * d.H2 * d.W2;
+  L->D_in = d.cin * d.H0 * d.W0;
+  L->D_pack = d.cpad * d.H0 * d.W0;
+  // canonical (torch) offsets
+  const int64_t c_c1w = 0, c_c1b = c_c1w + (int64_t)d.C1 * d.cin * 25, c_c2w = c_c1b + d.C1,
+                c_c2b = c_c2w + (int64_t)d.C2 * d.C1 * 25, c_f1w = c_c2b + d.C2, c_f1b = c_f1w + (int64_t)d.HID * d.F,
+                c_f2w = c_f1b + d.HID, c_f2b = c_f2w + (int64_t)d.NCLS * d.HID, c_end = c_f2b + d.NCLS;
+  L->P = c_end;
+  int64_t o = 0;
+  L->o_c1w = o; o = up32(o + (int64_t)d.C1 * 25 * d.cpad);
+  L->o_c1b = o; o = up32(o + d.C1);
+  L->o_c2w = o; o = up32(o + (int64_t)d.C2 * 25 * d.C1);
+  L->o_c2b = o; o = up32(o + d.C2);
+  L->o_f1w = o; o = up32(o + (int64_t)d.HID * d.F);
+  L->o_f1b = o; o = up32(o + d.HID);
+  L->o_f2w = o; o = up32(o + (int64_t)d.NCLS * d.HID);
+  L->o_f2b = o; o = up32(o + d.NCLS);
+  L->P_pad = o;
+  std::vector<int64_t>& m = L->canon_of;
+  m.assign((size_t)L->P_pad, -1);
+  for (int oc = 0; oc < d.C1; ++oc)
+    for (int t = 0; t < 25; ++t)
+      for (int c = 0; c < d.cin; ++c) m[(size_t)(L->o_c1w + ((int64_t)oc * 25 + t) * d.cpad + c)] = c_c1w + ((int64_t)oc * d.cin + c) * 25 + t;
+  for (int oc = 0; oc < d.C1; ++oc) m[(size_t)(L->o_c1b + oc)] = c_c1b + oc;
+  for (int oc = 0; oc < d.C2; ++oc)
+    for (int t = 0; t < 25; ++t)
+      for (int c = 0; c < d.C1; ++c) m[(size_t)(L->o_c2w + ((int64_t)oc * 25 + t) * d.C1 + c)] = c_c2w + ((int64_t)oc * d.C1 + c) * 25 + t;
+  for (int oc = 0; oc < d.C2; ++oc) m[(size_t)(L->o_c2b + oc)] = c_c2b + oc;
+  // fc1 columns: internal (h,w,c) order of the NHWC pooled map, canonical (c,h,w)
+  for (int n = 0; n < d.HID; ++n)
+    for (int h = 0; h < d.H2; ++h)
+      for (int w = 0; w < d.W2; ++w)
+        for (int c = 0; c < d.C2; ++c)
+          m[(size_t)(L->o_f1w + (int64_t)n * d.F + ((int64_t)h * d.W2 + w) * d.C2 + c)] =
+              c_f1w + (int64_t)n * d.F + ((int64_t)c * d.H2 + h) * d.W2 + w;
+  for (int n = 0; n < d.HID; ++n) m[(size_t)(L->o_f1b + n)] = c_f1b + n;
+  for (int64_t i = 0; i < (int64_t)d.NCLS * d.HID; ++i) m[(size_t)(L->o_f2w + i)] = c_f2w + i;
+  for (int q = 0; q < d.NCLS; ++q) m[(size_t)(L->o_f2b + q)] = c_f2b + q;
+  return true;
+}
+
+}  // namespace flb
+
+using namespace flb;
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+namespace {
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+  bool load() {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
+    return getUniqueId && commInitRank && allReduce && commDestroy;
+  }
+};
+Nccl g_nccl;
+
+template <class T>
+cudaError_t grow_dev(T*& p, int64_t& cap, int64_t need) {
+  if (need <= cap && p) return cudaSuccess;
+  if (p) cudaFree(p);
+  p = nullptr;
+  int64_t n = std::max<int64_t>(need, 1);
+  cudaError_t e = cudaMalloc((void**)&p, sizeof(T) * (size_t)n);
+  cap = e == cudaSuccess ? n : 0;
+  return e;
+}
+}  // namespace
+
+struct fl_ctx {
+  fl_config cfg{};
+  Layout L;
+  int64_t n_pop = 0;
+  std::vector<int64_t> n_samples, pop_off;
+  const void* x = nullptr;
+  const int32_t* y = nullptr;
+  bool pop_dev = false, host_registered = false;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+
+  float* d_theta = nullptr;  // θ_g, internal layout [P_pad]
+  int64_t* d_canon_of = nullptr;
+  float* d_canon = nullptr;  // scratch [P]
+  float* d_slots = nullptr;
+  int64_t slots_cap = 0;
+  double* d_S = nullptr;  // [P_pad + 1] (world > 1)
+
+  // plan
+  bool have_plan = false, trained = false, failed = false;
+  std::vector<int64_t> plan_ids, plan_off, local_ids;  // local_ids in plan order
+  std::vector<int64_t> exec;                           // exec position -> index into local_ids
+  std::vector<int64_t> steps_exec, n_exec, pseg;
+  int64_t N_total = 0, N_local = 0, K_total = 0;
+
+  // staging
+  float* d_xpack = nullptr;
+  int64_t xpack_cap = 0;
+  int32_t* d_ypack = nullptr;
+  int64_t ypack_cap = 0;
+  float* d_stage = nullptr;
+  int64_t stage_cap = 0;
+  int32_t* d_ystage = nullptr;
+  int64_t ystage_cap = 0;
+  int64_t* d_src_row = nullptr;
+  int64_t src_cap = 0;
+  int64_t* d_n = nullptr;
+  int64_t n_cap = 0;
+  int32_t* d_steps = nullptr;
+  int64_t steps_cap = 0;
+  int64_t* d_slot_off = nullptr;
+  int64_t slot_off_cap = 0;
+  int64_t sidx_cap = 0, bs_cap = 0;
+  WaveSched ws;
+  CnnBufs cb;
+  int64_t cb_slots_cap = 0, cb_part_cap = 0;
+
+  // pinned host staging of the per-round tables
+  char* h_tab = nullptr;
+  size_t h_tab_cap = 0;
+  double* h_N = nullptr;
+
+  cudaEvent_t ev_entry = nullptr, ev_start = nullptr, ev_staged = nullptr, ev_trained = nullptr,
+              ev_agg0 = nullptr, ev_acc1 = nullptr, ev_ar0 = nullptr, ev_ar1 = nullptr, ev_end = nullptr,
+              ev_tab = nullptr;
+  bool tab_pending = false;
+  double place_ms = 0.0;
+  int64_t kernels = 0, h2d = 0, train_launches = 0;
+  fl_round_stats stats{};
+  KProf prof;
+  std::string err;
+};
+
+// ---------------------------------------------------------------- error helpers
+static fl_status set_err(fl_ctx* c, fl_status s, const char* fmt, ...) {
+  if (!c) return s;
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  c->err = buf;
+  if (s == FL_ERR_CUDA || s == FL_ERR_NCCL || s == FL_ERR_OOM) c->failed = true;
+  return s;
+}
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      return set_err(c, e_ == cudaErrorMemoryAllocation ? FL_ERR_OOM : FL_ERR_CUDA, "%s: %s (%s:%d)", \
+                     #call, cudaGetErrorString(e_), __FILE__, __LINE__);                          \
+  } while (0)
+
+#define CKL()                                                                                     \
+  do {                                                                                            \
+    cudaError_t e_ = cudaGetLastError();                                                          \
+    if (e_ != cudaSuccess)                                                                        \
+      return set_err(c, FL_ERR_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+static bool model_supported(int m) {
+  return m == FL_MODEL_LOGREG || m == FL_MODEL_CNN_CIFAR || m == FL_MODEL_CNN_SPEECH;
+}
+
+extern "C" {
+
+uint32_t fl_abi_version(void) { return FL_ABI_VERSION; }
+
+int64_t fl_n_params(int32_t model) {
+  switch (model) {
+    case FL_MODEL_LOGREG: return 7850;
+    case FL_MODEL_CNN_CIFAR: return 2156490;
+    case FL_MODEL_CNN_SPEECH: return 3993507;
+    case FL_MODEL_CHAR_LSTM: return 819920;
+  }
+  return 0;
+}
+
+fl_status fl_place_plan(int32_t policy, const int64_t* cohort_ids, int64_t n_cohort, const int64_t* n_samples,
+                        int64_t n_clients, int32_t batch_size, int32_t world_size, const double* lb_coef,
+                        int64_t* out_ids, int64_t* out_off) {
+  if (!cohort_ids && n_cohort > 0) return FL_ERR_INVALID;
+  if (!n_samples || !out_off || (!out_ids && n_cohort > 0)) return FL_ERR_INVALID;
+  return (fl_status)place(policy, cohort_ids, n_cohort, n_samples, n_clients, batch_size, world_size, lb_coef,
+                          out_ids, out_off);
+}
+
+fl_status fl_pack_plan(const int64_t* ids, int64_t n, const int64_t* n_samples, int64_t n_clients, int32_t batch_size,
+                       int32_t local_epochs, int64_t* seg_off, int64_t* steps) {
+  if ((!ids && n > 0) || !n_samples) return FL_ERR_INVALID;
+  return (fl_status)pack(ids, n, n_samples, n_clients, batch_size, local_epochs, seg_off, steps);
+}
+
+fl_status fl_nccl_unique_id(uint8_t* out128) {
+  if (!out128) return FL_ERR_INVALID;
+  if (!g_nccl.load()) return FL_ERR_NCCL;
+  ncclUniqueId id;
+  if (g_nccl.getUniqueId(&id) != ncclSuccess) return FL_ERR_NCCL;
+  memcpy(out128, id.internal, 128);
+  return FL_OK;
+}
+
+const char* fl_last_error(const fl_ctx* c) { return c ? c->err.c_str() : ""; }
+
+void* fl_get_stream(fl_ctx* c) { return c ? (void*)c->st : nullptr; }
+
+void fl_round_destroy(fl_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->cfg.device);
+  if (c->st) cudaStreamSynchronize(c->st);
+  if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+  void* ptrs[] = {c->d_theta, c->d_canon_of, c->d_canon, c->d_slots, c->d_S, c->d_xpack, c->d_ypack, c->d_stage,
+                  c->d_ystage, c->d_src_row, c->d_n, c->d_steps, c->d_slot_off, c->ws.d_sidx, c->ws.d_bs,
+                  c->cb.a1, c->cb.p1, c->cb.a2, c->cb.p2, c->cb.h, c->cb.dh, c->cb.am1, c->cb.am2, c->cb.dp2,
+                  c->cb.dY2, c->cb.dp1, c->cb.dY1, c->cb.part1, c->cb.part2};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->h_tab) cudaFreeHost(c->h_tab);
+  if (c->h_N) cudaFreeHost(c->h_N);
+  cudaEvent_t evs[] = {c->ev_entry, c->ev_start, c->ev_staged, c->ev_trained, c->ev_agg0,
+                       c->ev_acc1, c->ev_ar0, c->ev_ar1, c->ev_end, c->ev_tab};
+  for (cudaEvent_t e : evs)
+    if (e) cudaEventDestroy(e);
+  if (c->host_registered) cudaHostUnregister((void*)c->x);
+  if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const float* global_params, int64_t n_params,
+                        fl_ctx** out) {
+  if (!cfg || !pop || !global_params || !out) return FL_ERR_INVALID;
+  *out = nullptr;
+  if (cfg->abi_version != FL_ABI_VERSION) return FL_ERR_INVALID;
+  if (cfg->batch_size < 1 || cfg->local_epochs < 1 || !(cfg->lr >= 0.f) || cfg->min_samples < 1) return FL_ERR_INVALID;
+  if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) return FL_ERR_INVALID;
+  if (cfg->world_size > 1 && !cfg->nccl_unique_id) return FL_ERR_INVALID;
+  if (fl_n_params(cfg->model) == 0) return FL_ERR_INVALID;
+  if (n_params != fl_n_params(cfg->model)) return FL_ERR_INVALID;
+  if (!model_supported(cfg->model)) return FL_ERR_UNSUPPORTED;
+  if (pop->n_clients < 1 || !pop->n_samples || !pop->x || !pop->y) return FL_ERR_INVALID;
+  fl_ctx* c = new fl_ctx();
+  c->cfg = *cfg;
+  make_layout(cfg->model, &c->L);
+  if (pop->feature_dim != c->L.D_in) {
+    delete c;
+    return FL_ERR_INVALID;
+  }
+  c->n_pop = pop->n_clients;
+  c->n_samples.assign(pop->n_samples, pop->n_samples + pop->n_clients);
+  c->pop_off.assign((size_t)c->n_pop + 1, 0);
+  for (int64_t k = 0; k < c->n_pop; ++k) {
+    if (c->n_samples[(size_t)k] < 0) {
+      delete c;
+      return FL_ERR_INVALID;
+    }
+    c->pop_off[(size_t)k + 1] = c->pop_off[(size_t)k] + c->n_samples[(size_t)k];
+  }
+  c->x = pop->x;
+  c->y = pop->y;
+  c->pop_dev = pop->on_device != 0;
+  *out = c;  // from here on errors are reported through the ctx
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(c, FL_ERR_CUDA, "no CUDA device: this library has no CPU path");
+  CK(cudaSetDevice(cfg->device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, cfg->device));
+  if (prop.major != 10) return set_err(c, FL_ERR_CUDA, "device %s is sm_%d%d; this build targets sm_100a", prop.name,
+                                       prop.major, prop.minor);
+  if (cfg->stream) c->st = (cudaStream_t)cfg->stream;
+  else {
+    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  cudaEvent_t* evs[] = {&c->ev_entry, &c->ev_start, &c->ev_staged, &c->ev_trained, &c->ev_agg0,
+                        &c->ev_acc1, &c->ev_ar0, &c->ev_ar1, &c->ev_end, &c->ev_tab};
+  for (cudaEvent_t* e : evs) CK(cudaEventCreate(e));
+  if (!c->pop_dev) {
+    // borrowed host population: pin it so per-round staging copies run at full PCIe rate
+    size_t xb = (size_t)c->pop_off.back() * (size_t)c->L.D_in * sizeof(float);
+    if (cudaHostRegister((void*)c->x, xb, cudaHostRegisterReadOnly) == cudaSuccess) c->host_registered = true;
+    else cudaGetLastError();
+  }
+  const int64_t P = c->L.P, Pp = c->L.P_pad;
+  CK(cudaMalloc(&c->d_theta, sizeof(float) * Pp));
+  CK(cudaMalloc(&c->d_canon_of, sizeof(int64_t) * Pp));
+  CK(cudaMalloc(&c->d_canon, sizeof(float) * P));
+  CK(cudaMalloc(&c->d_S, sizeof(double) * (Pp + 1)));
+  CK(cudaMallocHost(&c->h_N, sizeof(double)));
+  CK(cudaMemcpyAsync(c->d_canon_of, c->L.canon_of.data(), sizeof(int64_t) * Pp, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->d_canon, global_params, sizeof(float) * P, cudaMemcpyHostToDevice, c->st));
+  canon_to_internal(c->d_canon, c->d_canon_of, Pp, c->d_theta, c->st);
+  CKL();
+  CK(cudaStreamSynchronize(c->st));
+  if (cfg->world_size > 1) {
+    if (!g_nccl.load()) return set_err(c, FL_ERR_NCCL, "cannot dlopen libnccl.so.2");
+    ncclUniqueId id;
+    memcpy(id.internal, cfg->nccl_unique_id, 128);
+    ncclResult_t r = g_nccl.commInitRank(&c->comm, cfg->world_size, id, cfg->rank);
+    if (r != ncclSuccess)
+      return set_err(c, FL_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.errStr ? g_nccl.errStr(r) : "?");
+  }
+  return FL_OK;
+}
+
+fl_status fl_place(fl_ctx* c, const int64_t* cohort_ids, int64_t n_cohort, int32_t policy, const double* lb_coef,
+                   int64_t* out_ids, int64_t* out_off) {
+  if (!c) return FL_ERR_INVALID;
+  if (c->failed) return FL_ERR_STATE;
+  auto t0 = std::chrono::steady_clock::now();
+  if (n_cohort < 0 || (n_cohort > 0 && !cohort_ids)) return set_err(c, FL_ERR_INVALID, "bad cohort");
+  for (int64_t i = 0; i < n_cohort; ++i) {
+    int64_t id = cohort_ids[i];
+    if (id >= 0 && id < c->n_pop && c->n_samples[(size_t)id] < c->cfg.min_samples)
+      return set_err(c, FL_ERR_INVALID, "client %lld has %lld < min_samples samples", (long long)id,
+                     (long long)c->n_samples[(size_t)id]);
+  }
+  std::vector<int64_t> ids((size_t)n_cohort), off((size_t)c->cfg.world_size + 1);
+  int rc = place(policy, cohort_ids, n_cohort, c->n_samples.data(), c->n_pop, c->cfg.batch_size, c->cfg.world_size,
+                 lb_coef, ids.data(), off.data());
+  if (rc != FL_OK) return set_err(c, (fl_status)rc, "invalid cohort / policy (unknown or duplicate id?)");
+  c->plan_ids.swap(ids);
+  c->plan_off.swap(off);
+  const int r = c->cfg.rank;
+  c->local_ids.assign(c->plan_ids.begin() + c->plan_off[(size_t)r], c->plan_ids.begin() + c->plan_off[(size_t)r + 1]);
+  c->K_total = n_cohort;
+  c->N_total = 0;
+  for (int64_t i = 0; i < n_cohort; ++i) c->N_total += c->n_samples[(size_t)cohort_ids[i]];
+  c->have_plan = true;
+  c->trained = false;
+  if (out_ids) std::copy(c->plan_ids.begin(), c->plan_ids.end(), out_ids);
+  if (out_off) std::copy(c->plan_off.begin(), c->plan_off.end(), out_off);
+  c->place_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return FL_OK;
+}
+
+// Per-round host tables (pinned) -> device, then staging and the SGD waves.
+fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
+  if (!c) return FL_ERR_INVALID;
+  if (c->failed || !c->have_plan) return set_err(c, FL_ERR_STATE, c->failed ? "ctx failed" : "no plan: call fl_place first");
+  CK(cudaSetDevice(c->cfg.device));
+  auto t0 = std::chrono::steady_clock::now();
+  const Layout& L = c->L;
+  const int64_t B = c->cfg.batch_size, E = c->cfg.local_epochs, K = (int64_t)c->local_ids.size();
+  // execution order: steps descending (= batches descending), plan order on ties
+  c->exec.resize((size_t)K);
+  std::iota(c->exec.begin(), c->exec.end(), 0);
+  auto nb = [&](int64_t i) { return (c->n_samples[(size_t)c->local_ids[(size_t)i]] + B - 1) / B; };
+  std::stable_sort(c->exec.begin(), c->exec.end(), [&](int64_t a, int64_t b) { return nb(a) > nb(b); });
+  c->steps_exec.resize((size_t)K);
+  c->n_exec.resize((size_t)K);
+  c->pseg.assign((size_t)K + 1, 0);
+  c->N_local = 0;
+  for (int64_t e = 0; e < K; ++e) {
+    int64_t id = c->local_ids[(size_t)c->exec[(size_t)e]];
+    c->n_exec[(size_t)e] = c->n_samples[(size_t)id];
+    c->steps_exec[(size_t)e] = E * nb(c->exec[(size_t)e]);
+    c->pseg[(size_t)e + 1] = c->pseg[(size_t)e] + c->n_exec[(size_t)e];
+    c->N_local += c->n_exec[(size_t)e];
+  }
+  const int64_t R = c->pseg[(size_t)K];
+  WaveSched& ws = c->ws;
+  ws.n_waves = K ? c->steps_exec[0] : 0;
+  ws.A.assign((size_t)ws.n_waves, 0);
+  ws.slot_off.assign((size_t)ws.n_waves + 1, 0);
+  ws.bs_off.assign((size_t)ws.n_waves + 1, 0);
+  for (int64_t t = 0; t < ws.n_waves; ++t) {
+    int32_t A = 0;
+    while (A < K && c->steps_exec[(size_t)A] > t) ++A;  // prefix property of the exec order
+    ws.A[(size_t)t] = A;
+    ws.slot_off[(size_t)t + 1] = ws.slot_off[(size_t)t] + (int64_t)A * B;
+    ws.bs_off[(size_t)t + 1] = ws.bs_off[(size_t)t] + A;
+  }
+  const int64_t n_sidx = ws.slot_off[(size_t)ws.n_waves], n_bs = ws.bs_off[(size_t)ws.n_waves];
+  // pinned table layout: src_row[R] i64 | n[K] i64 | slot_off[W+1] i64 | sidx i32 | bs i32 | steps[K] i32
+  size_t need = sizeof(int64_t) * (size_t)(R + K + ws.n_waves + 1) + sizeof(int32_t) * (size_t)(n_sidx + n_bs + K) + 64;
+  if (c->tab_pending) {
+    CK(cudaEventSynchronize(c->ev_tab));
+    c->tab_pending = false;
+  }
+  if (need > c->h_tab_cap) {
+    if (c->h_tab) cudaFreeHost(c->h_tab);
+    c->h_tab = nullptr;
+    CK(cudaMallocHost(&c->h_tab, need * 2));
+    c->h_tab_cap = need * 2;
+  }
+  int64_t* h_src = (int64_t*)c->h_tab;
+  int64_t* h_n = h_src + R;
+  int64_t* h_soff = h_n + K;
+  int32_t* h_sidx = (int32_t*)(h_soff + ws.n_waves + 1);
+  int32_t* h_bs = h_sidx + n_sidx;
+  int32_t* h_steps = h_bs + n_bs;
+  for (int64_t e = 0; e < K; ++e) {
+    int64_t id = c->local_ids[(size_t)c->exec[(size_t)e]];
+    for (int64_t i = 0; i < c->n_exec[(size_t)e]; ++i) h_src[c->pseg[(size_t)e] + i] = c->pop_off[(size_t)id] + i;
+    h_n[e] = c->n_exec[(size_t)e];
+    h_steps[e] = (int32_t)c->steps_exec[(size_t)e];
+  }
+  for (int64_t t = 0; t <= ws.n_waves; ++t) h_soff[t] = ws.slot_off[(size_t)t];
+  // batches: epoch ep of client e uses permutation π_{e,ep} (A5) sliced into m_e batches
+  std::vector<int32_t> perm;
+  for (int64_t e = 0; e < K; ++e) {
+    const int64_t n = c->n_exec[(size_t)e], m = (n + B - 1) / B;
+    const int64_t id = c->local_ids[(size_t)c->exec[(size_t)e]];
+    perm.resize((size_t)n);
+    for (int64_t ep = 0; ep < E; ++ep) {
+      if (c->cfg.shuffle) shuffle_perm(c->cfg.seed, (uint64_t)round_index, (uint64_t)id, (uint64_t)ep, n, perm.data());
+      else std::iota(perm.begin(), perm.end(), 0);
+      for (int64_t j = 0; j < m; ++j) {
+        const int64_t t = ep * m + j;
+        int32_t* srow = h_sidx + ws.slot_off[(size_t)t] + e * B;
+        int32_t bsz = 0;
+        for (int64_t r = 0; r < B; ++r) {
+          const int64_t i = j * B + r;
+          if (i < n) {
+            srow[r] = (int32_t)(c->pseg[(size_t)e] + perm[(size_t)i]);
+            ++bsz;
+          } else {
+            srow[r] = -1;
+          }
+        }
+        h_bs[ws.bs_off[(size_t)t] + e] = bsz;
+      }
+    }
+  }
+  // device capacity (grow-only; allocation happens on the first round of a given size)
+  CK(grow_dev(c->d_slots, c->slots_cap, std::max<int64_t>(K, 1) * L.P_pad));
+  CK(grow_dev(c->d_xpack, c->xpack_cap, std::max<int64_t>(R, 1) * L.D_pack));
+  CK(grow_dev(c->d_ypack, c->ypack_cap, R));
+  CK(grow_dev(c->d_src_row, c->src_cap, R));
+  CK(grow_dev(c->d_n, c->n_cap, K));
+  CK(grow_dev(c->d_steps, c->steps_cap, K));
+  CK(grow_dev(c->d_slot_off, c->slot_off_cap, ws.n_waves + 1));
+  CK(grow_dev(ws.d_sidx, c->sidx_cap, n_sidx));
+  CK(grow_dev(ws.d_bs, c->bs_cap, n_bs));
+  if (!c->pop_dev) {
+    CK(grow_dev(c->d_stage, c->stage_cap, std::max<int64_t>(R, 1) * L.D_in));
+    CK(grow_dev(c->d_ystage, c->ystage_cap, R));
+  }
+  const bool cnn = (L.model == FL_MODEL_CNN_CIFAR || L.model == FL_MODEL_CNN_SPEECH);
+  if (cnn && K > 0) {
+    CnnBufs& b = c->cb;
+    const CnnDims& d = L.d;
+    b.nch = (int)std::min<int64_t>(8, B);
+    const int64_t S = (int64_t)K * B;  // wave 0 has every local client active
+    if (S > c->cb_slots_cap) {
+      void* old[] = {b.a1, b.p1, b.a2, b.p2, b.h, b.dh, b.am1, b.am2, b.dp2, b.dY2, b.dp1, b.dY1};
+      for (void* p : old)
+        if (p) cudaFree(p);
+      const int64_t hw0 = (int64_t)d.H0 * d.W0, hw1 = (int64_t)d.H1 * d.W1, hw2 = (int64_t)d.H2 * d.W2;
+      CK(cudaMalloc(&b.a1, sizeof(float) * S * hw0 * d.C1));
+      CK(cudaMalloc(&b.dY1, sizeof(float) * S * hw0 * d.C1));
+      CK(cudaMalloc(&b.p1, sizeof(float) * S * hw1 * d.C1));
+      CK(cudaMalloc(&b.am1, S * hw1 * d.C1));
+      CK(cudaMalloc(&b.dp1, sizeof(float) * S * hw1 * d.C1));
+      CK(cudaMalloc(&b.a2, sizeof(float) * S * hw1 * d.C2));
+      CK(cudaMalloc(&b.dY2, sizeof(float) * S * hw1 * d.C2));
+      CK(cudaMalloc(&b.p2, sizeof(float) * S * hw2 * d.C2));
+      CK(cudaMalloc(&b.am2, S * hw2 * d.C2));
+      CK(cudaMalloc(&b.dp2, sizeof(float) * S * hw2 * d.C2));
+      CK(cudaMalloc(&b.h, sizeof(float) * S * d.HID));
+      CK(cudaMalloc(&b.dh, sizeof(float) * S * d.HID));
+      c->cb_slots_cap = S;
+    }
+    const int64_t P2 = (int64_t)K * b.nch;
+    if (P2 > c->cb_part_cap) {
+      if (b.part1) cudaFree(b.part1);
+      if (b.part2) cudaFree(b.part2);
+      CK(cudaMalloc(&b.part2, sizeof(float) * P2 * d.C2 * (25 * d.C1 + 1)));
+      CK(cudaMalloc(&b.part1, sizeof(float) * P2 * d.C1 * (25 * d.cpad + 1)));
+      c->cb_part_cap = P2;
+    }
+  }
+  c->place_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+
+  // ---- device work, stream-ordered
+  cudaStream_t st = c->st;
+  int64_t launches = 0, h2d = 0;
+  c->prof.reset();
+  CK(cudaEventRecord(c->ev_start, st));
+  CK(cudaMemcpyAsync(c->d_src_row, h_src, sizeof(int64_t) * R, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_n, h_n, sizeof(int64_t) * K, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_slot_off, h_soff, sizeof(int64_t) * (ws.n_waves + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ws.d_sidx, h_sidx, sizeof(int32_t) * n_sidx, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ws.d_bs, h_bs, sizeof(int32_t) * n_bs, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_steps, h_steps, sizeof(int32_t) * K, cudaMemcpyHostToDevice, st));
+  CK(cudaEventRecord(c->ev_tab, st));
+  c->tab_pending = true;
+  h2d += (int64_t)(sizeof(int64_t) * (R + K + ws.n_waves + 1) + sizeof(int32_t) * (n_sidx + n_bs + K));
+  // stage the cohort's samples: device population -> gather; host population -> H2D copies
+  const float* xsrc = (const float*)c->x;
+  const int32_t* ysrc = c->y;
+  const int64_t* srow = c->d_src_row;
+  if (!c->pop_dev && R > 0) {
+    for (int64_t e = 0; e < K; ++e) {
+      int64_t id = c->local_ids[(size_t)c->exec[(size_t)e]];
+      int64_t r0 = c->pop_off[(size_t)id], n = c->n_exec[(size_t)e];
+      CK(cudaMemcpyAsync(c->d_stage + c->pseg[(size_t)e] * L.D_in, (const float*)c->x + r0 * L.D_in,
+                         sizeof(float) * n * L.D_in, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(c->d_ystage + c->pseg[(size_t)e], c->y + r0, sizeof(int32_t) * n, cudaMemcpyHostToDevice,
+                         st));
+    }
+    h2d += R * (int64_t)(L.D_in * sizeof(float) + sizeof(int32_t));
+    xsrc = c->d_stage;
+    ysrc = c->d_ystage;
+    srow = nullptr;
+  }
+  c->prof.begin(st);
+  if (cnn) launches += pack_cnn(L, xsrc, srow, R, c->d_xpack, st);
+  else launches += gather_rows_f32(xsrc, srow, R, L.D_pack, c->d_xpack, st);
+  launches += gather_i32(ysrc, srow, R, c->d_ypack, st);
+  c->prof.end(K_PACK, 0, (double)R * (4.0 * (L.D_in + L.D_pack) + 8.0), st);
+  CKL();
+  CK(cudaEventRecord(c->ev_staged, st));
+  // ---- local SGD
+  int64_t tl = 0;
+  if (K > 0) {
+    if (cnn) {
+      for (int64_t t = 0; t < ws.n_waves; ++t) {
+        int64_t sum_bs = 0;
+        for (int32_t a = 0; a < ws.A[(size_t)t]; ++a) sum_bs += h_bs[ws.bs_off[(size_t)t] + a];
+        WaveArgs wa{ws.A[(size_t)t], (int)B, t == 0, ws.d_sidx + ws.slot_off[(size_t)t], ws.d_bs + ws.bs_off[(size_t)t],
+                    c->cfg.lr, sum_bs, &c->prof};
+        tl += cnn_wave_simt(L, wa, c->d_xpack, c->d_ypack, c->d_theta, c->d_slots, c->cb, st);
+      }
+    } else {
+      c->prof.begin(st);
+      tl += logreg_train(L, ws, (int)K, (int)B, c->cfg.lr, c->d_xpack, c->d_ypack, c->d_theta, c->d_slots,
+                         c->d_steps, c->d_slot_off, st);
+      double S = 0;
+      for (int64_t e = 0; e < K; ++e) S += (double)c->n_exec[(size_t)e] * E;
+      c->prof.end(K_LOGREG, 3.0 * 2.0 * S * 7840, 4.0 * S * 785 + 8.0 * K * L.P_pad, st);
+    }
+    CKL();
+  }
+  CK(cudaEventRecord(c->ev_trained, st));
+  c->kernels = launches + tl;
+  c->train_launches = tl;
+  c->h2d = h2d;
+  c->trained = true;
+  return FL_OK;
+}
+
+fl_status fl_aggregate(fl_ctx* c, float* out_params, int64_t* out_total_samples) {
+  if (!c) return FL_ERR_INVALID;
+  if (c->failed || !c->trained) return set_err(c, FL_ERR_STATE, c->failed ? "ctx failed" : "train before aggregate");
+  if (c->N_total <= 0) return set_err(c, FL_ERR_EMPTY, "total sample count is 0");
+  CK(cudaSetDevice(c->cfg.device));
+  const int64_t Pp = c->L.P_pad, K = (int64_t)c->exec.size();
+  cudaStream_t st = c->st;
+  CK(cudaEventRecord(c->ev_agg0, st));
+  int64_t n = 0;
+  c->prof.begin(st);
+  const double agg_bytes = 4.0 * (double)Pp * (double)(K + 1) + (c->cfg.world_size == 1 ? 4.0 : 8.0) * (double)Pp;
+  if (c->cfg.world_size == 1) {
+    n += fedavg_accum_final(c->d_slots, Pp, c->d_n, (int)K, Pp, c->d_theta, (double)c->N_total, c->d_theta, st);
+    CKL();
+    c->prof.end(K_FEDAVG, 3.0 * (double)Pp * K, agg_bytes, st);
+    CK(cudaEventRecord(c->ev_acc1, st));
+    CK(cudaEventRecord(c->ev_ar0, st));
+    CK(cudaEventRecord(c->ev_ar1, st));
+  } else {
+    n += fedavg_accum_partial(c->d_slots, Pp, c->d_n, (int)K, Pp, c->d_theta, c->d_S, st);
+    CKL();
+    c->prof.end(K_FEDAVG, 3.0 * (double)Pp * K, agg_bytes, st);
+    CK(cudaEventRecord(c->ev_acc1, st));
+    *c->h_N = (double)c->N_local;
+    CK(cudaMemcpyAsync(c->d_S + Pp, c->h_N, sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(c->ev_ar0, st));
+    ncclResult_t r = g_nccl.allReduce(c->d_S, c->d_S, (size_t)(Pp + 1), ncclFloat64, ncclSum, c->comm, st);
+    if (r != ncclSuccess) return set_err(c, FL_ERR_NCCL, "ncclAllReduce: %s", g_nccl.errStr ? g_nccl.errStr(r) : "?");
+    CK(cudaEventRecord(c->ev_ar1, st));
+    n += fedavg_finalize(c->d_S, Pp, c->d_theta, c->d_S + Pp, c->d_theta, st);
+    CKL();
+  }
+  CK(cudaEventRecord(c->ev_end, st));
+  c->kernels += n;
+  c->trained = false;
+  c->have_plan = false;
+  if (out_total_samples) *out_total_samples = c->N_total;
+  if (out_params) {
+    internal_to_canon(c->d_theta, c->d_canon_of, Pp, c->d_canon, st);
+    CKL();
+    CK(cudaMemcpyAsync(out_params, c->d_canon, sizeof(float) * c->L.P, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return FL_OK;
+}
+
+static double ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    cudaGetLastError();
+    return 0.0;
+  }
+  return ms;
+}
+
+static void fill_stats(fl_ctx* c, fl_round_stats* s) {
+  memset(s, 0, sizeof *s);
+  s->round_ms = ev_ms(c->ev_entry, c->ev_end);
+  s->place_ms = c->place_ms;
+  s->stage_ms = ev_ms(c->ev_start, c->ev_staged);
+  s->train_ms = ev_ms(c->ev_staged, c->ev_trained);
+  s->agg_ms = ev_ms(c->ev_agg0, c->ev_end);
+  s->allreduce_ms = ev_ms(c->ev_ar0, c->ev_ar1);
+  s->clients_total = c->K_total;
+  s->clients_local = (int64_t)c->exec.size();
+  s->samples_total = c->N_total;
+  s->samples_local = c->N_local;
+  for (int64_t v : c->steps_exec) s->steps_local += v;
+  s->waves = c->ws.n_waves;
+  s->h2d_bytes = c->h2d;
+  s->kernels = c->kernels;
+  s->client_updates_per_s = s->round_ms > 0 ? (double)c->K_total / (s->round_ms * 1e-3) : 0.0;
+}
+
+fl_status fl_round(fl_ctx* c, const int64_t* cohort_ids, int64_t n_cohort, int32_t policy, const double* lb_coef,
+                   int32_t round_index, fl_round_stats* stats) {
+  if (!c) return FL_ERR_INVALID;
+  if (c->failed) return set_err(c, FL_ERR_STATE, "ctx failed");
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaEventRecord(c->ev_entry, c->st));
+  fl_status s = fl_place(c, cohort_ids, n_cohort, policy, lb_coef, nullptr, nullptr);
+  if (s != FL_OK) return s;
+  s = fl_train_clients(c, round_index);
+  if (s != FL_OK) return s;
+  s = fl_aggregate(c, nullptr, nullptr);
+  if (s != FL_OK) return s;
+  if (stats) {
+    CK(cudaEventSynchronize(c->ev_end));
+    fill_stats(c, &c->stats);
+    *stats = c->stats;
+  }
+  return FL_OK;
+}
+
+fl_status fl_get_stats(fl_ctx* c, fl_round_stats* out) {
+  if (!c || !out) return FL_ERR_INVALID;
+  CK(cudaEventSynchronize(c->ev_end));
+  fill_stats(c, &c->stats);
+  *out = c->stats;
+  return FL_OK;
+}
+
+fl_status fl_set_profiling(fl_ctx* c, int32_t on) {
+  if (!c) return FL_ERR_INVALID;
+  c->prof.on = on != 0;
+  return FL_OK;
+}
+
+fl_status fl_get_kernel_stats(fl_ctx* c, int32_t kind, fl_kernel_stats* out) {
+  if (!c || !out || kind < 0 || kind >= K_NKINDS) return FL_ERR_INVALID;
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaStreamSynchronize(c->st));
+  memset(out, 0, sizeof *out);
+  snprintf(out->name, sizeof out->name, "%s", kKindName[kind]);
+  for (const KRec& r : c->prof.recs) {
+    if (r.kind != kind) continue;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    out->ms += ms;
+    out->launches += 1;
+    out->flops += r.flops;
+    out->bytes += r.bytes;
+  }
+  return FL_OK;
+}
+
+fl_status fl_fedavg_vectors(fl_ctx* c, const float* theta_k, const int64_t* n, int64_t K, int64_t P,
+                            const float* theta_g, float* out) {
+  if (!c || !theta_k || !n || !theta_g || !out || K < 1 || P < 1) return FL_ERR_INVALID;
+  if (c->failed) return FL_ERR_STATE;
+  int64_t N = 0;
+  for (int64_t k = 0; k < K; ++k) {
+    if (n[k] < 1) return set_err(c, FL_ERR_INVALID, "weight < 1");
+    N += n[k];
+  }
+  CK(cudaSetDevice(c->cfg.device));
+  CK(grow_dev(c->d_n, c->n_cap, K));
+  CK(cudaMemcpyAsync(c->d_n, n, sizeof(int64_t) * K, cudaMemcpyHostToDevice, c->st));
+  CK(cudaEventRecord(c->ev_agg0, c->st));
+  fedavg_accum_final(theta_k, P, c->d_n, (int)K, P, theta_g, (double)N, out, c->st);
+  CKL();
+  CK(cudaEventRecord(c->ev_acc1, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return FL_OK;
+}
+
+fl_status fl_get_local_plan(fl_ctx* c, int64_t* ids, int64_t* seg_off, int64_t* steps, int64_t* n_local) {
+  if (!c || !n_local) return FL_ERR_INVALID;
+  const int64_t K = (int64_t)c->local_ids.size();
+  *n_local = K;
+  if (ids) std::copy(c->local_ids.begin(), c->local_ids.end(), ids);
+  if (seg_off || steps)
+    return (fl_status)pack(c->local_ids.data(), K, c->n_samples.data(), c->n_pop, c->cfg.batch_size,
+                           c->cfg.local_epochs, seg_off, steps);
+  return FL_OK;
+}
+
+fl_status fl_get_client_params(fl_ctx* c, int64_t client_id, float* out) {
+  if (!c || !out) return FL_ERR_INVALID;
+  if (c->failed) return FL_ERR_STATE;
+  int64_t e = -1;
+  for (size_t i = 0; i < c->exec.size(); ++i)
+    if (c->local_ids[(size_t)c->exec[i]] == client_id) e = (int64_t)i;
+  if (e < 0 || !c->d_slots) return set_err(c, FL_ERR_INVALID, "client %lld not trained on this rank", (long long)client_id);
+  CK(cudaSetDevice(c->cfg.device));
+  internal_to_canon(c->d_slots + e * c->L.P_pad, c->d_canon_of, c->L.P_pad, c->d_canon, c->st);
+  CKL();
+  CK(cudaMemcpyAsync(out, c->d_canon, sizeof(float) * c->L.P, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return FL_OK;
+}
+
+fl_status fl_get_global_params(fl_ctx* c, float* out) {
+  if (!c || !out) return FL_ERR_INVALID;
+  if (c->failed) return FL_ERR_STATE;
+  CK(cudaSetDevice(c->cfg.device));
+  internal_to_canon(c->d_theta, c->d_canon_of, c->L.P_pad, c->d_canon, c->st);
+  CKL();
+  CK(cudaMemcpyAsync(out, c->d_canon, sizeof(float) * c->L.P, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return FL_OK;
+}
+
+fl_status fl_set_global_params(fl_ctx* c, const float* params) {
+  if (!c || !params) return FL_ERR_INVALID;
+  if (c->failed) return FL_ERR_STATE;
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaMemcpyAsync(c->d_canon, params, sizeof(float) * c->L.P, cudaMemcpyHostToDevice, c->st));
+  canon_to_internal(c->d_canon, c->d_canon_of, c->L.P_pad, c->d_theta, c->st);
+  CKL();
+  CK(cudaStreamSynchronize(c->st));
+  return FL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,141 @@
+// fl_internal.h — internal declarations shared by the library's translation units.
+// Nothing here is part of the ABI (see include/fl.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace flb {
+
+// ---------------------------------------------------------------- model geometry
+// CNN family (McMahan CNN on CIFAR / speech, reading A10): conv5x5 'same' + ReLU +
+// maxpool2 -> conv5x5 'same' + ReLU + maxpool2 -> fc + ReLU -> fc.
+struct CnnDims {
+  int cin, cpad;       // input channels, padded to 4 for 16-byte NHWC pixels
+  int H0, W0;          // input
+  int C1, C2;          // conv channels (32, 64)
+  int H1, W1, H2, W2;  // after pool1 / pool2 (floor)
+  int F;               // C2*H2*W2 (fc1 fan-in)
+  int HID, NCLS;
+};
+
+// Internal (device) parameter layout: NHWC-friendly, every tensor 128-byte aligned.
+//   c1w [C1][5][5][cpad]  c1b [C1]  c2w [C2][5][5][C1]  c2b [C2]
+//   f1w [HID][H2][W2][C2] f1b [HID] f2w [NCLS][HID]     f2b [NCLS]
+// logreg: w [10][784] b [10].   LSTM: canonical order (see lstm kernels).
+struct Layout {
+  int model = -1;
+  int64_t P = 0;      // canonical parameter count
+  int64_t P_pad = 0;  // internal per-slot stride (floats, multiple of 32)
+  int D_in = 0;       // population feature dim
+  int D_pack = 0;     // packed per-sample floats (NHWC4 for CNN)
+  CnnDims d{};
+  int64_t o_c1w = 0, o_c1b = 0, o_c2w = 0, o_c2b = 0, o_f1w = 0, o_f1b = 0, o_f2w = 0, o_f2b = 0;
+  std::vector<int64_t> canon_of;  // [P_pad]: canonical index of each internal slot, -1 = padding
+};
+
+bool make_layout(int model, Layout* L);
+
+// ---------------------------------------------------------------- per-wave schedule
+// Wave t = SGD step t of every local client with more than t steps.  Local clients
+// are executed in order of steps descending, so wave t's active clients are the
+// prefix [0, A_t).  Slot (a, r) = a*B + r holds row r of client a's current batch.
+struct WaveSched {
+  int64_t n_waves = 0;
+  std::vector<int32_t> A;          // active clients per wave
+  std::vector<int64_t> slot_off;   // offset of the wave's [A_t*B] sample table
+  std::vector<int64_t> bs_off;     // offset of the wave's [A_t] batch-size table
+  int32_t* d_sidx = nullptr;       // device: packed sample row or -1
+  int32_t* d_bs = nullptr;         // device: |b| of each active client
+};
+
+// ---------------------------------------------------------------- CNN buffers
+struct CnnBufs {
+  int64_t slots = 0;  // capacity in (client, row) slots
+  int64_t clients = 0;
+  int nch = 0;        // split-K chunks of the dW GEMMs
+  float *a1 = nullptr, *p1 = nullptr, *a2 = nullptr, *p2 = nullptr, *h = nullptr, *dh = nullptr;
+  uint8_t *am1 = nullptr, *am2 = nullptr;
+  float *dp2 = nullptr, *dY2 = nullptr, *dp1 = nullptr, *dY1 = nullptr;
+  float *part2 = nullptr, *part1 = nullptr;  // split-K partials of conv dW (+ bias column)
+};
+
+// ---------------------------------------------------------------- per-kernel timing
+// Optional instrumentation: every launch bracketed by CUDA events on the launch stream,
+// tagged with its kernel class and the algorithmic FLOPs / bytes of that launch.
+enum KKind {
+  K_PACK = 0, K_CONV1_FWD, K_POOL1, K_CONV2_FWD, K_POOL2, K_FC1_FWD, K_HEAD, K_FC1_DX, K_UNPOOL2, K_FC1_DW,
+  K_CONV2_DX, K_UNPOOL1, K_CONV2_DW, K_CONV2_DWR, K_CONV1_DW, K_CONV1_DWR, K_LOGREG, K_FEDAVG, K_NKINDS
+};
+extern const char* const kKindName[K_NKINDS];
+struct KRec {
+  int kind;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
+struct KProf {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<KRec> recs;
+  cudaEvent_t cur = nullptr;
+  cudaEvent_t next_event() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void begin(cudaStream_t st) {
+    if (!on) return;
+    cur = next_event();
+    cudaEventRecord(cur, st);
+  }
+  void end(int kind, double flops, double bytes, cudaStream_t st) {
+    if (!on) return;
+    cudaEvent_t e = next_event();
+    cudaEventRecord(e, st);
+    recs.push_back({kind, cur, e, flops, bytes});
+  }
+  void reset() { used = 0; recs.clear(); }
+  ~KProf() { for (cudaEvent_t e : pool) cudaEventDestroy(e); }
+};
+
+struct WaveArgs {
+  int A;             // active clients
+  int B;             // batch size
+  bool first;        // wave 0: weights are read from theta_g
+  const int32_t* sidx;
+  const int32_t* bs;
+  float lr;
+  int64_t sum_bs;    // Σ |b| over the wave's clients (algorithmic work accounting)
+  KProf* prof;
+};
+
+// Kernel launchers (k_*.cu). All asynchronous on `st`. Return the number of launches.
+int cnn_wave_simt(const Layout& L, const WaveArgs& w, const float* xpack, const int32_t* ypack,
+                  const float* theta_g, float* slots, CnnBufs& b, cudaStream_t st);
+int logreg_train(const Layout& L, const WaveSched& ws, int n_local, int B, float lr, const float* xpack,
+                 const int32_t* ypack, const float* theta_g, float* slots, const int32_t* steps_dev,
+                 const int64_t* wave_slot_off_dev, cudaStream_t st);
+int pack_cnn(const Layout& L, const float* x_src, const int64_t* src_row, int64_t rows, float* xpack,
+             cudaStream_t st);
+int gather_rows_f32(const float* src, const int64_t* src_row, int64_t rows, int64_t dim, float* dst,
+                    cudaStream_t st);
+int gather_i32(const int32_t* src, const int64_t* src_row, int64_t rows, int32_t* dst, cudaStream_t st);
+int canon_to_internal(const float* canon, const int64_t* canon_of, int64_t P_pad, float* internal,
+                      cudaStream_t st);
+int internal_to_canon(const float* internal, const int64_t* canon_of, int64_t P_pad, float* canon,
+                      cudaStream_t st);
+// FedAvg (K1/K2): slots[k*stride + p], k in [0,K); weights n[k] (device int64).
+int fedavg_accum_final(const float* slots, int64_t stride, const int64_t* n, int K, int64_t P,
+                       const float* theta_g, double N, float* out, cudaStream_t st);
+int fedavg_accum_partial(const float* slots, int64_t stride, const int64_t* n, int K, int64_t P,
+                         const float* theta_g, double* S, cudaStream_t st);
+int fedavg_finalize(const double* S, int64_t P, const float* theta_g, const double* Ndev, float* out,
+                    cudaStream_t st);
+
+}  // namespace flb

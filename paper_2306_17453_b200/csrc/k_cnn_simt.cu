@@ -1,0 +1,437 @@
+// k_cnn_simt.cu — one SGD wave of the CNN family on FP32 CUDA cores ("math = 1" path,
+// and the reference the tensor-core kernels are checked against).
+//
+// A wave is SGD step t of every active local client (PAPER.md P:176,
+// P:362-363).  Every layer is a grouped GEMM over the active clients (grid.z = client, or
+// client x split-K chunk), expressed as an "op" with element accessors and an epilogue,
+// run by one tiled SIMT GEMM template.  Activations are slot-major NHWC: slot (a, r) =
+// a*B + r.  Weights of client a are read from θ_g on the first wave (slot init fused, a3)
+// and from the client's slot afterwards; SGD (a7) is fused into the dW epilogues.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fl_internal.h"
+
+namespace flb {
+namespace {
+
+constexpr int TM = 64, TN = 64, TK = 16, NT = 256;
+
+// C[m][n] = Σ_k A(z,m,k)·Bv(z,n,k) for problem z; op.store() consumes C.
+template <class Op>
+__global__ void __launch_bounds__(NT) k_gemm(const Op op) {
+  const int z = blockIdx.z;
+  int M, N, kb, ke;
+  if (!op.setup(z, M, N, kb, ke)) return;
+  const int m0 = blockIdx.x * TM, n0 = blockIdx.y * TN;
+  if (m0 >= M || n0 >= N) return;
+  __shared__ float As[TK][TM + 4];
+  __shared__ float Bs[TK][TN + 4];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  for (int k0 = kb; k0 < ke; k0 += TK) {
+#pragma unroll
+    for (int i = 0; i < (TM * TK) / NT; ++i) {
+      const int e = tid + i * NT;
+      int mm, kk;
+      if (Op::kAK) { mm = e / TK; kk = e % TK; } else { mm = e % TM; kk = e / TM; }
+      const int m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < M && k < ke) ? op.A(z, m, k) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < (TN * TK) / NT; ++i) {
+      const int e = tid + i * NT;
+      int nn, kk;
+      if (Op::kBK) { nn = e / TK; kk = e % TK; } else { nn = e % TN; kk = e / TN; }
+      const int n = n0 + nn, k = k0 + kk;
+      Bs[kk][nn] = (n < N && k < ke) ? op.Bv(z, n, k) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+      if (m < M && n < N) op.store(z, m, n, acc[i][j]);
+    }
+}
+
+struct WSrc {  // weights of client z: θ_g on the first wave, the client's slot afterwards
+  const float* base;
+  int64_t stride;
+  __device__ const float* at(int z, int64_t off) const { return base + (int64_t)z * stride + off; }
+};
+
+// conv 5x5 'same' (pad 2) as implicit GEMM. rows (r,h,w), cols o, K = (kh,kw,c).
+// Y = conv(X) + bias (pre-activation).  X rows come from the packed input via sidx (conv1)
+// or from the slot-major activations (conv2).
+struct ConvFwd {
+  static constexpr bool kAK = true, kBK = true;
+  const float* X;
+  const int32_t* sidx;
+  const int32_t* bs;
+  int B, H, W, C, O;
+  WSrc w;
+  int64_t o_w, o_b;
+  float* Y;
+  __device__ bool setup(int z, int& M, int& N, int& kb, int& ke) const {
+    M = bs[z] * H * W; N = O; kb = 0; ke = 25 * C;
+    return M > 0;
+  }
+  __device__ float A(int z, int m, int k) const {
+    const int HW = H * W, r = m / HW, pix = m - r * HW, h = pix / W, x = pix - h * W;
+    const int tap = k / C, c = k - tap * C, kh = tap / 5, kw = tap - kh * 5;
+    const int ih = h + kh - 2, iw = x + kw - 2;
+    if (ih < 0 || ih >= H || iw < 0 || iw >= W) return 0.f;
+    const int64_t row = sidx ? (int64_t)sidx[z * B + r] : (int64_t)z * B + r;
+    return X[((row * H + ih) * W + iw) * C + c];
+  }
+  __device__ float Bv(int z, int n, int k) const { return *w.at(z, o_w + (int64_t)n * 25 * C + k); }
+  __device__ void store(int z, int m, int n, float v) const {
+    Y[((int64_t)z * B * H * W + m) * O + n] = v + *w.at(z, o_b + n);
+  }
+};
+
+// dX of a 5x5 'same' conv (transposed conv): rows (r,y,x), cols c, K = (kh,kw,o).
+struct ConvDx {
+  static constexpr bool kAK = true, kBK = false;
+  const float* dY;
+  const int32_t* bs;
+  int B, H, W, C, O;
+  WSrc w;
+  int64_t o_w;
+  float* dX;
+  __device__ bool setup(int z, int& M, int& N, int& kb, int& ke) const {
+    M = bs[z] * H * W; N = C; kb = 0; ke = 25 * O;
+    return M > 0;
+  }
+  __device__ float A(int z, int m, int k) const {
+    const int HW = H * W, r = m / HW, pix = m - r * HW, y = pix / W, x = pix - y * W;
+    const int tap = k / O, o = k - tap * O, kh = tap / 5, kw = tap - kh * 5;
+    const int iy = y - kh + 2, ix = x - kw + 2;
+    if (iy < 0 || iy >= H || ix < 0 || ix >= W) return 0.f;
+    return dY[((((int64_t)z * B + r) * H + iy) * W + ix) * O + o];
+  }
+  __device__ float Bv(int z, int n, int k) const {
+    const int tap = k / O, o = k - tap * O;
+    return *w.at(z, o_w + ((int64_t)o * 25 + tap) * C + n);
+  }
+  __device__ void store(int z, int m, int n, float v) const { dX[((int64_t)z * B * H * W + m) * C + n] = v; }
+};
+
+// dW partial of a 5x5 conv over a chunk of rows: rows o, cols (kh,kw,c) plus a bias
+// column (B = 1), K = pixels of the chunk's samples.
+struct ConvDw {
+  static constexpr bool kAK = false, kBK = false;
+  const float* dY;
+  const float* X;
+  const int32_t* sidx;
+  const int32_t* bs;
+  int B, H, W, C, O, nch, rpc;
+  float* part;
+  __device__ bool setup(int z, int& M, int& N, int& kb, int& ke) const {
+    const int a = z / nch, ch = z - a * nch, r0 = ch * rpc;
+    int r1 = r0 + rpc;
+    if (r1 > bs[a]) r1 = bs[a];
+    M = O; N = 25 * C + 1; kb = 0; ke = (r1 - r0) * H * W;
+    return r1 > r0;
+  }
+  __device__ float A(int z, int m, int k) const {
+    const int a = z / nch, ch = z - a * nch, HW = H * W;
+    const int r = ch * rpc + k / HW, pix = k % HW;
+    return dY[(((int64_t)a * B + r) * HW + pix) * O + m];
+  }
+  __device__ float Bv(int z, int n, int k) const {
+    if (n == 25 * C) return 1.f;
+    const int a = z / nch, ch = z - a * nch, HW = H * W;
+    const int r = ch * rpc + k / HW, pix = k % HW, h = pix / W, x = pix - h * W;
+    const int tap = n / C, c = n - tap * C, kh = tap / 5, kw = tap - kh * 5;
+    const int ih = h + kh - 2, iw = x + kw - 2;
+    if (ih < 0 || ih >= H || iw < 0 || iw >= W) return 0.f;
+    const int64_t row = sidx ? (int64_t)sidx[a * B + r] : (int64_t)a * B + r;
+    return X[((row * H + ih) * W + iw) * C + c];
+  }
+  __device__ void store(int z, int m, int n, float v) const {
+    const int N = 25 * C + 1;
+    part[(int64_t)z * O * N + (int64_t)m * N + n] = v;
+  }
+};
+
+// fc1 forward: h = ReLU(p2·W1ᵀ + b1). rows r, cols n, K = F.
+struct FcFwd {
+  static constexpr bool kAK = true, kBK = true;
+  const float* X;
+  const int32_t* bs;
+  int B, F, HID;
+  WSrc w;
+  int64_t o_w, o_b;
+  float* h;
+  __device__ bool setup(int z, int& M, int& N, int& kb, int& ke) const {
+    M = bs[z]; N = HID; kb = 0; ke = F;
+    return M > 0;
+  }
+  __device__ float A(int z, int m, int k) const { return X[((int64_t)z * B + m) * F + k]; }
+  __device__ float Bv(int z, int n, int k) const { return *w.at(z, o_w + (int64_t)n * F + k); }
+  __device__ void store(int z, int m, int n, float v) const {
+    v += *w.at(z, o_b + n);
+    h[((int64_t)z * B + m) * HID + n] = v > 0.f ? v : 0.f;
+  }
+};
+
+// fc1 dX: dp2 = dh·W1. rows r, cols k (F), K = HID.
+struct FcDx {
+  static constexpr bool kAK = true, kBK = false;
+  const float* dh;
+  const int32_t* bs;
+  int B, F, HID;
+  WSrc w;
+  int64_t o_w;
+  float* dX;
+  __device__ bool setup(int z, int& M, int& N, int& kb, int& ke) const {
+    M = bs[z]; N = F; kb = 0; ke = HID;
+    return M > 0;
+  }
+  __device__ float A(int z, int m, int k) const { return dh[((int64_t)z * B + m) * HID + k]; }
+  __device__ float Bv(int z, int n, int k) const { return *w.at(z, o_w + (int64_t)k * F + n); }
+  __device__ void store(int z, int m, int n, float v) const { dX[((int64_t)z * B + m) * F + n] = v; }
+};
+
+// fc1 dW with fused SGD: W1 <- W1 − η·dhᵀ·p2 (+ bias column). rows n, cols k, K = r.
+struct FcDwSgd {
+  static constexpr bool kAK = false, kBK = false;
+  const float* dh;
+  const float* X;
+  const int32_t* bs;
+  int B, F, HID;
+  WSrc w;
+  float* dst;
+  int64_t P_pad, o_w, o_b;
+  float lr;
+  __device__ bool setup(int z, int& M, int& N, int& kb, int& ke) const {
+    M = HID; N = F + 1; kb = 0; ke = bs[z];
+    return ke > 0;
+  }
+  __device__ float A(int z, int m, int k) const { return dh[((int64_t)z * B + k) * HID + m]; }
+  __device__ float Bv(int z, int n, int k) const { return n < F ? X[((int64_t)z * B + k) * F + n] : 1.f; }
+  __device__ void store(int z, int m, int n, float v) const {
+    const int64_t off = n < F ? o_w + (int64_t)m * F + n : o_b + m;
+    dst[(int64_t)z * P_pad + off] = *w.at(z, off) - lr * v;
+  }
+};
+
+// ReLU + 2x2 max-pool (floor), first maximum in row-major window order (reading A13).
+__global__ void k_pool(const float* __restrict__ a, int H, int W, int C, int B, const int32_t* __restrict__ bs,
+                       float* __restrict__ p, uint8_t* __restrict__ am) {
+  const int s = blockIdx.y, z = s / B, r = s - z * B;
+  if (r >= bs[z]) return;
+  const int Hp = H / 2, Wp = W / 2, tot = Hp * Wp * C;
+  const float* base = a + (int64_t)s * H * W * C;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {
+    const int c = e % C, pw = (e / C) % Wp, ph = e / (C * Wp);
+    const float* q = base + ((2 * ph) * W + 2 * pw) * C + c;
+    float bv = q[0];
+    int best = 0;
+    float v = q[C];
+    if (v > bv) { bv = v; best = 1; }
+    v = q[W * C];
+    if (v > bv) { bv = v; best = 2; }
+    v = q[W * C + C];
+    if (v > bv) { bv = v; best = 3; }
+    p[(int64_t)s * tot + e] = bv > 0.f ? bv : 0.f;
+    am[(int64_t)s * tot + e] = (uint8_t)best;
+  }
+}
+
+// Backward of pool + ReLU: route dp to the window's argmax if the pooled value > 0.
+__global__ void k_unpool(const float* __restrict__ dp, const float* __restrict__ p, const uint8_t* __restrict__ am,
+                         int H, int W, int C, int B, const int32_t* __restrict__ bs, float* __restrict__ dY) {
+  const int s = blockIdx.y, z = s / B, r = s - z * B;
+  if (r >= bs[z]) return;
+  const int Hp = H / 2, Wp = W / 2, ptot = Hp * Wp * C, tot = H * W * C;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {
+    const int c = e % C, x = (e / C) % W, y = e / (C * W);
+    const int ph = y >> 1, pw = x >> 1;
+    float g = 0.f;
+    if (ph < Hp && pw < Wp) {
+      const int64_t pe = (int64_t)s * ptot + (ph * Wp + pw) * C + c;
+      if (am[pe] == ((y & 1) * 2 + (x & 1)) && p[pe] > 0.f) g = dp[pe];
+    }
+    dY[(int64_t)s * tot + e] = g;
+  }
+}
+
+// Σ of the split-K partials, then fused SGD on the conv weights and bias.
+__global__ void k_dw_reduce_sgd(const float* __restrict__ part, int nch, int rpc, const int32_t* __restrict__ bs,
+                                int O, int N, WSrc w, int64_t o_w, int64_t o_b, float* dst, int64_t P_pad, float lr) {
+  const int a = blockIdx.y;
+  const int nvalid = (bs[a] + rpc - 1) / rpc;
+  const int tot = O * N;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {
+    float g = 0.f;
+    for (int ch = 0; ch < nvalid; ++ch) g += part[((int64_t)a * nch + ch) * tot + e];
+    const int m = e / N, n = e - m * N;
+    const int64_t off = n < N - 1 ? o_w + (int64_t)m * (N - 1) + n : o_b + m;
+    dst[(int64_t)a * P_pad + off] = *w.at(a, off) - lr * g;
+  }
+}
+
+// Classifier head of one client per block: logits = h·W2ᵀ + b2, softmax-CE (mean over
+// |b|, reading A9), dz = (p − onehot)/|b|, dh = (dz·W2) ⊙ [h > 0], then SGD on W2, b2.
+__global__ void __launch_bounds__(256) k_head(const float* __restrict__ h, const int32_t* __restrict__ ypack,
+                                              const int32_t* __restrict__ sidx, const int32_t* __restrict__ bs,
+                                              int B, int HID, int NCLS, WSrc w, int64_t o_w, int64_t o_b,
+                                              float* dst, int64_t P_pad, float lr, float* __restrict__ dh) {
+  extern __shared__ float sm[];
+  const int z = blockIdx.x, b = bs[z];
+  if (b == 0) return;
+  float* Ws = sm;                    // [NCLS][HID]
+  float* bias = Ws + NCLS * HID;     // [NCLS]
+  float* dz = bias + NCLS;           // [B][NCLS]
+  const float* W = w.at(z, o_w);
+  for (int e = threadIdx.x; e < NCLS * HID; e += blockDim.x) Ws[e] = W[e];
+  for (int e = threadIdx.x; e < NCLS; e += blockDim.x) bias[e] = *w.at(z, o_b + e);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int idx = warp; idx < b * NCLS; idx += nw) {
+    const int r = idx / NCLS, q = idx - r * NCLS;
+    const float* hr = h + ((int64_t)z * B + r) * HID;
+    float s = 0.f;
+    for (int n = lane; n < HID; n += 32) s = fmaf(Ws[q * HID + n], hr[n], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) dz[r * NCLS + q] = s + bias[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < b) {
+    const int r = threadIdx.x;
+    float* zr = dz + r * NCLS;
+    const int y = ypack[sidx[z * B + r]];
+    float mx = zr[0];
+    for (int q = 1; q < NCLS; ++q) mx = fmaxf(mx, zr[q]);
+    float s = 0.f;
+    for (int q = 0; q < NCLS; ++q) s += expf(zr[q] - mx);
+    const float inv = 1.f / (float)b;
+    for (int q = 0; q < NCLS; ++q) zr[q] = (expf(zr[q] - mx) / s - (q == y ? 1.f : 0.f)) * inv;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < b * HID; e += blockDim.x) {
+    const int r = e / HID, n = e - r * HID;
+    const int64_t hi = ((int64_t)z * B + r) * HID + n;
+    float s = 0.f;
+    for (int q = 0; q < NCLS; ++q) s = fmaf(Ws[q * HID + n], dz[r * NCLS + q], s);
+    dh[hi] = h[hi] > 0.f ? s : 0.f;
+  }
+  float* Wd = dst + (int64_t)z * P_pad;
+  for (int e = threadIdx.x; e < NCLS * HID; e += blockDim.x) {
+    const int q = e / HID, n = e - q * HID;
+    float g = 0.f;
+    for (int r = 0; r < b; ++r) g = fmaf(dz[r * NCLS + q], h[((int64_t)z * B + r) * HID + n], g);
+    Wd[o_w + e] = Ws[e] - lr * g;
+  }
+  if (threadIdx.x < NCLS) {
+    const int q = threadIdx.x;
+    float g = 0.f;
+    for (int r = 0; r < b; ++r) g += dz[r * NCLS + q];
+    Wd[o_b + q] = bias[q] - lr * g;
+  }
+}
+
+template <class Op>
+void launch(const Op& op, int Mmax, int Nmax, int Z, cudaStream_t st) {
+  dim3 grid((Mmax + TM - 1) / TM, (Nmax + TN - 1) / TN, Z);
+  k_gemm<Op><<<grid, NT, 0, st>>>(op);
+}
+
+}  // namespace
+
+int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const int32_t* ypack,
+                  const float* theta_g, float* slots, CnnBufs& b, cudaStream_t st) {
+  const CnnDims& d = L.d;
+  const int A = wa.A, B = wa.B;
+  const WSrc w{wa.first ? theta_g : slots, wa.first ? 0 : L.P_pad};
+  KProf& pf = *wa.prof;
+  const double S = (double)wa.sum_bs, hw0 = (double)d.H0 * d.W0, hw1 = (double)d.H1 * d.W1;
+  // algorithmic FLOPs of each GEMM (conv1 K = 25*cin, not the padded 25*cpad)
+  const double f_c1 = 2.0 * S * hw0 * d.C1 * 25 * d.cin, f_c2 = 2.0 * S * hw1 * d.C2 * 25 * d.C1,
+               f_f1 = 2.0 * S * d.HID * d.F, f_f2 = 2.0 * S * d.NCLS * d.HID;
+  const double wbytes = 4.0 * (double)A * (double)d.HID * d.F;  // one pass over the fc1 weights
+  int n = 0;
+  // ---- forward
+  pf.begin(st);
+  launch(ConvFwd{xpack, wa.sidx, wa.bs, B, d.H0, d.W0, d.cpad, d.C1, w, L.o_c1w, L.o_c1b, b.a1},
+         B * d.H0 * d.W0, d.C1, A, st), ++n;
+  pf.end(K_CONV1_FWD, f_c1, 4.0 * S * hw0 * (d.cin + d.C1), st);
+  pf.begin(st);
+  k_pool<<<dim3(8, A * B), 256, 0, st>>>(b.a1, d.H0, d.W0, d.C1, B, wa.bs, b.p1, b.am1), ++n;
+  pf.end(K_POOL1, 0, S * hw0 * d.C1 * (4.0 + 5.0 / 4.0), st);
+  pf.begin(st);
+  launch(ConvFwd{b.p1, nullptr, wa.bs, B, d.H1, d.W1, d.C1, d.C2, w, L.o_c2w, L.o_c2b, b.a2},
+         B * d.H1 * d.W1, d.C2, A, st), ++n;
+  pf.end(K_CONV2_FWD, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
+  pf.begin(st);
+  k_pool<<<dim3(4, A * B), 256, 0, st>>>(b.a2, d.H1, d.W1, d.C2, B, wa.bs, b.p2, b.am2), ++n;
+  pf.end(K_POOL2, 0, S * hw1 * d.C2 * (4.0 + 5.0 / 4.0), st);
+  pf.begin(st);
+  launch(FcFwd{b.p2, wa.bs, B, d.F, d.HID, w, L.o_f1w, L.o_f1b, b.h}, B, d.HID, A, st), ++n;
+  pf.end(K_FC1_FWD, f_f1, wbytes + 4.0 * S * (d.F + d.HID), st);
+  size_t hsm = sizeof(float) * (size_t)(d.NCLS * d.HID + d.NCLS + B * d.NCLS);
+  pf.begin(st);
+  k_head<<<A, 256, hsm, st>>>(b.h, ypack, wa.sidx, wa.bs, B, d.HID, d.NCLS, w, L.o_f2w, L.o_f2b, slots, L.P_pad,
+                              wa.lr, b.dh), ++n;
+  pf.end(K_HEAD, 3.0 * f_f2, 8.0 * A * d.NCLS * d.HID + 8.0 * S * d.HID, st);
+  // ---- backward (each layer's dX reads W before its dW epilogue overwrites it)
+  pf.begin(st);
+  launch(FcDx{b.dh, wa.bs, B, d.F, d.HID, w, L.o_f1w, b.dp2}, B, d.F, A, st), ++n;
+  pf.end(K_FC1_DX, f_f1, wbytes + 4.0 * S * (d.F + d.HID), st);
+  pf.begin(st);
+  k_unpool<<<dim3(4, A * B), 256, 0, st>>>(b.dp2, b.p2, b.am2, d.H1, d.W1, d.C2, B, wa.bs, b.dY2), ++n;
+  pf.end(K_UNPOOL2, 0, S * hw1 * d.C2 * (4.0 + 9.0 / 4.0), st);
+  pf.begin(st);
+  launch(FcDwSgd{b.dh, b.p2, wa.bs, B, d.F, d.HID, w, slots, L.P_pad, L.o_f1w, L.o_f1b, wa.lr}, d.HID, d.F + 1, A,
+         st), ++n;
+  pf.end(K_FC1_DW, f_f1, 2.0 * wbytes + 4.0 * S * (d.F + d.HID), st);
+  pf.begin(st);
+  launch(ConvDx{b.dY2, wa.bs, B, d.H1, d.W1, d.C1, d.C2, w, L.o_c2w, b.dp1}, B * d.H1 * d.W1, d.C1, A, st), ++n;
+  pf.end(K_CONV2_DX, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
+  pf.begin(st);
+  k_unpool<<<dim3(8, A * B), 256, 0, st>>>(b.dp1, b.p1, b.am1, d.H0, d.W0, d.C1, B, wa.bs, b.dY1), ++n;
+  pf.end(K_UNPOOL1, 0, S * hw0 * d.C1 * (4.0 + 9.0 / 4.0), st);
+  const int rpc = (B + b.nch - 1) / b.nch;
+  pf.begin(st);
+  launch(ConvDw{b.dY2, b.p1, nullptr, wa.bs, B, d.H1, d.W1, d.C1, d.C2, b.nch, rpc, b.part2}, d.C2,
+         25 * d.C1 + 1, A * b.nch, st), ++n;
+  pf.end(K_CONV2_DW, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
+  pf.begin(st);
+  k_dw_reduce_sgd<<<dim3(16, A), 256, 0, st>>>(b.part2, b.nch, rpc, wa.bs, d.C2, 25 * d.C1 + 1, w, L.o_c2w,
+                                               L.o_c2b, slots, L.P_pad, wa.lr), ++n;
+  pf.end(K_CONV2_DWR, 0, 8.0 * A * d.C2 * 25 * d.C1, st);
+  pf.begin(st);
+  launch(ConvDw{b.dY1, xpack, wa.sidx, wa.bs, B, d.H0, d.W0, d.cpad, d.C1, b.nch, rpc, b.part1}, d.C1,
+         25 * d.cpad + 1, A * b.nch, st), ++n;
+  pf.end(K_CONV1_DW, f_c1, 4.0 * S * hw0 * (d.cin + d.C1), st);
+  pf.begin(st);
+  k_dw_reduce_sgd<<<dim3(4, A), 256, 0, st>>>(b.part1, b.nch, rpc, wa.bs, d.C1, 25 * d.cpad + 1, w, L.o_c1w,
+                                              L.o_c1b, slots, L.P_pad, wa.lr), ++n;
+  pf.end(K_CONV1_DWR, 0, 8.0 * A * d.C1 * 25 * d.cin, st);
+  return n;
+}
+
+}  // namespace flb

@@ -1,0 +1,230 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU fp64 oracle.
+
+Bars (BASELINE.json north_star): placement / segment offsets bit-exact;
+aggregation alone within 1e-6 relative (reading A20: |g − o| ≤ 1e-6·s_p with
+s_p = Σ_k (n_k/N)|θ_k,p|); parameters within 1e-3 max-abs after a full round.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2306_17453_b200 as fl  # noqa: E402
+
+TOL_ROUND = 1e-3
+TOL_AGG = 1e-6
+
+
+def make_ctx(wl, sizes, x, y, theta, on_device=True, **kw):
+    cfg = fl.Config(model=wl.model, batch_size=wl.B, local_epochs=wl.E, lr=wl.lr, shuffle=wl.shuffle, seed=wl.seed,
+                    **kw)
+    if on_device:
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.from_numpy(y.astype(np.int32)).cuda()
+        return fl.fl_round_init(cfg, sizes, xd, yd, theta), (xd, yd)
+    return fl.fl_round_init(cfg, sizes, x, y, theta, on_device=False), None
+
+
+def agg_err(gpu, theta_k, n):
+    """max_p |g − o| / s_p with o the oracle's fp64 mean of the same fp32 inputs."""
+    o, _ = oracle.fedavg(theta_k.astype(np.float64), n)
+    w = np.asarray(n, np.float64) / np.sum(n)
+    s = np.abs(theta_k.astype(np.float64)).T @ w
+    return np.max(np.abs(gpu.astype(np.float64) - o) / np.maximum(s, 1e-30))
+
+
+# ------------------------------------------------------------------ aggregation alone
+@pytest.mark.parametrize("K,P", [(1, 4096), (7, 1003), (137, 65536), (1000, 2048)])
+def test_fedavg_vectors_parity(K, P):
+    rng = np.random.default_rng(K * 31 + P)
+    wl = synth.preset("C1")
+    sizes = synth.client_sizes(wl)
+    _, x, y = synth.population(wl, sizes)
+    ctx, keep = make_ctx(wl, sizes, x, y, synth.init_params("logreg"))
+    tk = (rng.standard_normal((K, P)) * rng.uniform(0.01, 10, size=(K, 1))).astype(np.float32)
+    tg = rng.standard_normal(P).astype(np.float32)
+    n = rng.integers(1, 2001, size=K)
+    out = torch.empty(P, device="cuda")
+    ctx.fl_fedavg_vectors(torch.from_numpy(tk).cuda(), n, torch.from_numpy(tg).cuda(), out)
+    assert agg_err(out.cpu().numpy(), tk, n) <= TOL_AGG
+    # constant vectors: the weighted mean is exact (integer weights, fp64 accumulation)
+    v = rng.standard_normal(P).astype(np.float32)
+    ctx.fl_fedavg_vectors(torch.from_numpy(np.tile(v, (K, 1))).cuda(), n, torch.from_numpy(tg).cuda(), out)
+    assert np.array_equal(out.cpu().numpy(), v)
+    # identical clients => the single client's vector
+    ctx.fl_fedavg_vectors(torch.from_numpy(np.tile(tk[:1], (K, 1))).cuda(), n, torch.from_numpy(tg).cuda(), out)
+    assert np.array_equal(out.cpu().numpy(), tk[0])
+
+
+# ------------------------------------------------------------------ placement through the ctx
+def test_ctx_plan_matches_oracle():
+    """fl_place through a context = the oracle's plan; local segments = oracle packer."""
+    wl = synth.preset("C2")
+    sizes = synth.client_sizes(wl)
+    xs = np.zeros((int(sizes.sum()), 3072), np.float32)
+    ys = np.zeros(int(sizes.sum()), np.int32)
+    ctx, keep = make_ctx(wl, sizes, xs, ys, synth.init_params("cnn"), on_device=False)
+    for pol in ["bu", "rr", "srr", "lb"]:
+        coef = [0.01, 0.3, 1.0, 0.05]
+        ids, off = ctx.fl_place(np.arange(100)[::-1], pol, coef)
+        oids, ooff = oracle.place(pol, np.arange(100)[::-1], sizes, wl.B, 1, lb=coef)
+        assert np.array_equal(ids, oids) and np.array_equal(off, ooff)
+        lids, seg, steps = ctx.fl_get_local_plan()
+        oseg, osteps = oracle.pack(oids, sizes, wl.B, wl.E)
+        assert np.array_equal(lids, oids)
+        assert np.array_equal(seg, oseg) and np.array_equal(steps, osteps)
+
+
+# ------------------------------------------------------------------ full rounds vs oracle
+def run_round(wl, sizes, cohort, on_device=True, threads=0, math=0):
+    _, x, y = synth.population(wl, sizes)
+    theta = synth.init_params(wl.model)
+    ctx, keep = make_ctx(wl, sizes, x, y, theta, on_device=on_device, math=math)
+    ctx.fl_place(cohort, "bu")
+    ctx.fl_train_clients(0)
+    tk_gpu = {int(c): ctx.fl_get_client_params(c) for c in cohort}
+    out, N = ctx.fl_aggregate()
+    ref, Nref, tk = oracle.fedavg_round(wl.model, theta, x, y, sizes, cohort, wl.B, wl.E, wl.lr, wl.shuffle,
+                                        wl.seed, 0, threads)
+    return out, N, ref, Nref, tk, tk_gpu, theta
+
+
+def test_logreg_round_C1():
+    wl = synth.preset("C1")
+    sizes = synth.client_sizes(wl)
+    cohort = synth.cohort(wl)
+    out, N, ref, Nref, tk, tk_gpu, _ = run_round(wl, sizes, cohort)
+    assert N == Nref == sizes[cohort].sum()
+    for i, c in enumerate(cohort):
+        assert np.max(np.abs(tk_gpu[int(c)] - tk[i])) <= TOL_ROUND
+    err = np.max(np.abs(out - ref))
+    assert err <= TOL_ROUND, err
+
+
+def test_logreg_shuffled_multi_epoch_host_population():
+    wl = synth.preset("C1", E=3, shuffle=1, n_pop=12, n_cohort=9)
+    sizes = synth.client_sizes(wl)
+    cohort = synth.cohort(wl)
+    out, N, ref, *_ = run_round(wl, sizes, cohort, on_device=False)
+    assert np.max(np.abs(out - ref)) <= TOL_ROUND
+
+
+# CNN: ragged sizes covering n < B, n = B, n = B+1, several batches with a tail
+RAGGED = np.array([1, 7, 32, 33, 70, 45], dtype=np.int64)
+
+
+@pytest.mark.parametrize("E,shuffle,on_device", [(1, 0, True), (2, 1, True), (2, 1, False)])
+def test_cnn_round_ragged(E, shuffle, on_device):
+    wl = synth.preset("C2", n_pop=len(RAGGED), n_cohort=len(RAGGED), E=E, shuffle=shuffle)
+    cohort = np.array([4, 0, 2, 5, 1, 3])
+    out, N, ref, Nref, tk, tk_gpu, theta = run_round(wl, RAGGED, cohort, on_device=on_device)
+    assert N == Nref == RAGGED.sum()
+    for i, c in enumerate(cohort):
+        e = np.max(np.abs(tk_gpu[int(c)] - tk[i]))
+        assert e <= TOL_ROUND, (c, e)
+    err = np.max(np.abs(out - ref))
+    assert err <= TOL_ROUND, err
+    assert np.max(np.abs(out - theta)) > 1e-4  # the round moved the model
+
+
+def test_speech_round_small():
+    sizes = np.array([3, 20, 26], dtype=np.int64)
+    wl = synth.preset("C4", n_pop=3, n_cohort=3)
+    out, N, ref, Nref, tk, tk_gpu, _ = run_round(wl, sizes, np.arange(3))
+    for i in range(3):
+        assert np.max(np.abs(tk_gpu[i] - tk[i])) <= TOL_ROUND
+    assert np.max(np.abs(out - ref)) <= TOL_ROUND
+
+
+def test_cnn_lr_zero_is_identity():
+    wl = synth.preset("C2", n_pop=4, n_cohort=4, lr=0.0)
+    sizes = np.array([5, 40, 3, 64], dtype=np.int64)
+    _, x, y = synth.population(wl, sizes)
+    theta = synth.init_params("cnn")
+    ctx, keep = make_ctx(wl, sizes, x, y, theta)
+    ctx.fl_round(np.arange(4))
+    assert np.array_equal(ctx.fl_get_global_params(), theta)
+
+
+def test_cnn_identical_clients_equal_single():
+    wl = synth.preset("C2", n_pop=5, n_cohort=5)
+    x1, y1 = synth.client_data(wl, 0, 37)
+    sizes = np.full(5, 37, dtype=np.int64)
+    x, y = np.concatenate([x1] * 5), np.concatenate([y1] * 5)
+    theta = synth.init_params("cnn")
+    ctx, keep = make_ctx(wl, sizes, x, y, theta)
+    ctx.fl_place(np.arange(5))
+    ctx.fl_train_clients(0)
+    t0 = ctx.fl_get_client_params(0)
+    out, _ = ctx.fl_aggregate()
+    assert np.array_equal(out, t0)
+    single = oracle.local_sgd("cnn", theta, x1, y1, wl.B, wl.E, wl.lr)
+    assert np.max(np.abs(out - single)) <= TOL_ROUND
+
+
+def test_multi_round_state_carries_over():
+    wl = synth.preset("C1")
+    sizes = synth.client_sizes(wl)
+    _, x, y = synth.population(wl, sizes)
+    theta = synth.init_params("logreg")
+    ctx, keep = make_ctx(wl, sizes, x, y, theta)
+    th = theta.astype(np.float64)
+    for r in range(3):
+        ctx.fl_round(np.arange(10), round_index=r)
+        th, _, _ = oracle.fedavg_round("logreg", th.astype(np.float32), x, y, sizes, np.arange(10), wl.B, wl.E, wl.lr)
+    assert np.max(np.abs(ctx.fl_get_global_params() - th)) <= TOL_ROUND
+
+
+def test_errors_through_ctx():
+    wl = synth.preset("C1")
+    sizes = synth.client_sizes(wl)
+    _, x, y = synth.population(wl, sizes)
+    ctx, keep = make_ctx(wl, sizes, x, y, synth.init_params("logreg"))
+    with pytest.raises(fl.FLError) as e:
+        ctx.fl_train_clients(0)
+    assert e.value.status == fl.FL_ERR_STATE
+    with pytest.raises(fl.FLError) as e:
+        ctx.fl_place([0, 0])
+    assert e.value.status == fl.FL_ERR_INVALID
+    with pytest.raises(fl.FLError) as e:
+        ctx.fl_place([0, 99])
+    assert e.value.status == fl.FL_ERR_INVALID
+    ctx.fl_place([])
+    ctx.fl_train_clients(0)
+    with pytest.raises(fl.FLError) as e:
+        ctx.fl_aggregate()
+    assert e.value.status == fl.FL_ERR_EMPTY
+
+
+# ------------------------------------------------------------------ the bench configuration (C2, full size)
+def test_C2_full_size_sampled():
+    """BASELINE configs[1] in bench.py's launch configuration: every client trained
+    by the GPU; θ_k checked against the oracle on a sample of clients (the smallest,
+    a few random), aggregation checked at full size on sampled coordinates."""
+    wl = synth.preset("C2")
+    sizes = synth.client_sizes(wl)
+    cohort = synth.cohort(wl)
+    _, x, y = synth.population(wl, sizes)
+    theta = synth.init_params("cnn")
+    ctx, keep = make_ctx(wl, sizes, x, y, theta)
+    ctx.fl_place(cohort)
+    ctx.fl_train_clients(0)
+    tk_gpu = np.stack([ctx.fl_get_client_params(c) for c in cohort])
+    out, N = ctx.fl_aggregate()
+    assert N == sizes.sum()
+    rng = np.random.default_rng(0)
+    order = np.argsort(sizes)
+    sample = list(order[:3]) + list(rng.choice(order[3:60], size=3, replace=False))
+    pop_off = np.concatenate([[0], np.cumsum(sizes)])
+    tk_ref, _ = oracle.train_clients("cnn", theta, x, y, pop_off, np.array(sample), wl.B, wl.E, wl.lr)
+    for i, c in enumerate(sample):
+        assert np.max(np.abs(tk_gpu[c] - tk_ref[i])) <= TOL_ROUND
+    coords = rng.choice(len(theta), size=20000, replace=False)
+    assert agg_err(out[coords], tk_gpu[:, coords], sizes[cohort]) <= TOL_AGG
