@@ -264,6 +264,9 @@ class Ctx:
     def fl_fedavg_vectors(self, theta_k, n, theta_g, out):
         """theta_k [K,P], theta_g [P], out [P]: torch CUDA float32 tensors; n host ints."""
         n = _i64(n)
+        for t in (theta_k, theta_g, out):
+            if str(getattr(t, "dtype", "")) != "torch.float32" or not t.is_cuda or not t.is_contiguous():
+                raise FLError(FL_ERR_INVALID, "fl_fedavg_vectors: float32 contiguous CUDA tensors required")
         K, P = theta_k.shape
         self._check(lib().fl_fedavg_vectors(self._h, _ptr(theta_k), _ptr(n), K, P, _ptr(theta_g), _ptr(out)),
                     "fl_fedavg_vectors")

@@ -51,7 +51,7 @@ def test_fedavg_vectors_parity(K, P):
     tk = (rng.standard_normal((K, P)) * rng.uniform(0.01, 10, size=(K, 1))).astype(np.float32)
     tg = rng.standard_normal(P).astype(np.float32)
     n = rng.integers(1, 2001, size=K)
-    out = torch.empty(P, device="cuda")
+    out = torch.empty(P, device="cuda", dtype=torch.float32)
     ctx.fl_fedavg_vectors(torch.from_numpy(tk).cuda(), n, torch.from_numpy(tg).cuda(), out)
     assert agg_err(out.cpu().numpy(), tk, n) <= TOL_AGG
     # constant vectors: the weighted mean is exact (integer weights, fp64 accumulation)

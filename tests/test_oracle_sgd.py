@@ -15,7 +15,6 @@ import torch.nn.functional as F
 import oracle
 import synth
 
-torch.set_default_dtype(torch.float64)
 
 
 def split(model, theta):
@@ -46,7 +45,7 @@ def torch_loss(model, p, x, y):
     else:
         e = F.embedding(torch.as_tensor(x, dtype=torch.long), p["emb"])
         # torch's fused LSTM op on our parameter tensors (gate order i,f,g,o)
-        out = torch._VF.lstm(e, (torch.zeros(2, e.shape[0], 256), torch.zeros(2, e.shape[0], 256)),
+        out = torch._VF.lstm(e, (torch.zeros(2, e.shape[0], 256, dtype=torch.float64), torch.zeros(2, e.shape[0], 256, dtype=torch.float64)),
                              [p["w_ih_l0"], p["w_hh_l0"], p["b_ih_l0"], p["b_hh_l0"],
                               p["w_ih_l1"], p["w_hh_l1"], p["b_ih_l1"], p["b_hh_l1"]],
                              True, 2, 0.0, False, False, True)[0]
