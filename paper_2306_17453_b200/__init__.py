@@ -30,7 +30,7 @@ ABI_VERSION = 1
 EXPORTS = ["fl_abi_version", "fl_n_params", "fl_place_plan", "fl_pack_plan", "fl_nccl_unique_id", "fl_round_init",
            "fl_place", "fl_train_clients", "fl_aggregate", "fl_round", "fl_fedavg_vectors", "fl_get_local_plan",
            "fl_get_client_params", "fl_get_global_params", "fl_set_global_params", "fl_get_stats",
-           "fl_set_profiling", "fl_get_kernel_stats", "fl_get_stream", "fl_last_error", "fl_round_destroy"]
+           "fl_set_profiling", "fl_get_kernel_stats", "fl_get_stream", "fl_last_error", "fl_round_destroy", "fl_debug_read"]
 
 
 class FLError(RuntimeError):
@@ -102,6 +102,7 @@ def lib():
             "fl_get_stream": (vp, [vp]),
             "fl_last_error": (C.c_char_p, [vp]),
             "fl_round_destroy": (None, [vp]),
+            "fl_debug_read": (C.c_int, [vp, C.c_char_p, vp, i64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -293,6 +294,12 @@ class Ctx:
     def fl_set_global_params(self, theta):
         theta = np.ascontiguousarray(theta, np.float32)
         self._check(lib().fl_set_global_params(self._h, _ptr(theta)), "fl_set_global_params")
+
+    def fl_debug_read(self, name, shape, dtype=np.float32):
+        """Test-only: copy an activation buffer of the last wave (include/fl_debug.h)."""
+        out = np.empty(shape, dtype)
+        self._check(lib().fl_debug_read(self._h, name.encode(), _ptr(out), out.nbytes), "fl_debug_read")
+        return out
 
     def fl_get_stats(self):
         st = fl_round_stats()

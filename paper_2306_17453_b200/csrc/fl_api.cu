@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/fl.h"
+#include "../../include/fl_debug.h"
 #include "fl_host.h"
 #include "fl_internal.h"
 
@@ -531,6 +532,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       CK(cudaMalloc(&b.h, sizeof(float) * S * d.HID));
       CK(cudaMalloc(&b.dh, sizeof(float) * S * d.HID));
       c->cb_slots_cap = S;
+      b.slots = S;
     }
     const int64_t P2 = (int64_t)K * b.nch;
     if (P2 > c->cb_part_cap) {
@@ -590,8 +592,10 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
         int64_t sum_bs = 0;
         for (int32_t a = 0; a < ws.A[(size_t)t]; ++a) sum_bs += h_bs[ws.bs_off[(size_t)t] + a];
         WaveArgs wa{ws.A[(size_t)t], (int)B, t == 0, ws.d_sidx + ws.slot_off[(size_t)t], ws.d_bs + ws.bs_off[(size_t)t],
-                    c->cfg.lr, sum_bs, &c->prof};
-        tl += cnn_wave_simt(L, wa, c->d_xpack, c->d_ypack, c->d_theta, c->d_slots, c->cb, st);
+                    c->cfg.lr, sum_bs, &c->prof, c->cfg.math == 0, c->slots_cap / L.P_pad};
+        int nl = cnn_wave_simt(L, wa, c->d_xpack, c->d_ypack, c->d_theta, c->d_slots, c->cb, st);
+        if (nl < 0) return set_err(c, FL_ERR_CUDA, "tensor-core kernel launch / tensor map failed (wave %lld)", (long long)t);
+        tl += nl;
       }
     } else {
       c->prof.begin(st);
@@ -805,4 +809,27 @@ fl_status fl_set_global_params(fl_ctx* c, const float* params) {
   return FL_OK;
 }
 
+fl_status fl_debug_read(fl_ctx* c, const char* name, void* host, int64_t bytes) {
+  if (!c || !name || !host || bytes < 0) return FL_ERR_INVALID;
+  if (c->L.model != FL_MODEL_CNN_CIFAR && c->L.model != FL_MODEL_CNN_SPEECH) return FL_ERR_INVALID;
+  const CnnBufs& b = c->cb;
+  const CnnDims& d = c->L.d;
+  const int64_t S = b.slots, hw0 = (int64_t)d.H0 * d.W0, hw1 = (int64_t)d.H1 * d.W1, hw2 = (int64_t)d.H2 * d.W2;
+  struct { const char* n; const void* p; int64_t bytes; } tab[] = {
+      {"p1", b.p1, 4 * S * hw1 * d.C1}, {"am1", b.am1, S * hw1 * d.C1}, {"p2", b.p2, 4 * S * hw2 * d.C2},
+      {"am2", b.am2, S * hw2 * d.C2},   {"h", b.h, 4 * S * d.HID},      {"dh", b.dh, 4 * S * d.HID},
+      {"dp2", b.dp2, 4 * S * d.F},      {"dY2", b.dY2, 4 * S * hw1 * d.C2}, {"dp1", b.dp1, 4 * S * hw1 * d.C1},
+      {"dY1", b.dY1, 4 * S * hw0 * d.C1}};
+  for (auto& t : tab) {
+    if (strcmp(t.n, name) != 0) continue;
+    if (!t.p) return set_err(c, FL_ERR_STATE, "buffer %s not allocated yet", name);
+    CK(cudaSetDevice(c->cfg.device));
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaMemcpy(host, t.p, (size_t)std::min<int64_t>(bytes, t.bytes), cudaMemcpyDeviceToHost));
+    return FL_OK;
+  }
+  return set_err(c, FL_ERR_INVALID, "unknown buffer %s", name);
+}
+
 }  // extern "C"
+

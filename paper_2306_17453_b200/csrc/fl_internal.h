@@ -113,11 +113,19 @@ struct WaveArgs {
   float lr;
   int64_t sum_bs;    // Σ |b| over the wave's clients (algorithmic work accounting)
   KProf* prof;
+  bool use_tc;       // tensor-core (tcgen05) kernels where built for this geometry
+  int64_t wclients;  // client slots allocated (weights tensor-map extent)
 };
 
 // Kernel launchers (k_*.cu). All asynchronous on `st`. Return the number of launches.
 int cnn_wave_simt(const Layout& L, const WaveArgs& w, const float* xpack, const int32_t* ypack,
                   const float* theta_g, float* slots, CnnBufs& b, cudaStream_t st);
+// tcgen05 kernels (k_conv_tc.cu)
+bool conv_tc_supported(const Layout& L);
+int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p1,
+                 int64_t slots, float* p2, uint8_t* am2, cudaStream_t st);
+int conv2_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dY2,
+                int64_t slots, float* dp1, cudaStream_t st);
 int logreg_train(const Layout& L, const WaveSched& ws, int n_local, int B, float lr, const float* xpack,
                  const int32_t* ypack, const float* theta_g, float* slots, const int32_t* steps_dev,
                  const int64_t* wave_slot_off_dev, cudaStream_t st);

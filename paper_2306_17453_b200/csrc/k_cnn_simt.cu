@@ -382,13 +382,22 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   pf.begin(st);
   k_pool<<<dim3(8, A * B), 256, 0, st>>>(b.a1, d.H0, d.W0, d.C1, B, wa.bs, b.p1, b.am1), ++n;
   pf.end(K_POOL1, 0, S * hw0 * d.C1 * (4.0 + 5.0 / 4.0), st);
-  pf.begin(st);
-  launch(ConvFwd{b.p1, nullptr, wa.bs, B, d.H1, d.W1, d.C1, d.C2, w, L.o_c2w, L.o_c2b, b.a2},
-         B * d.H1 * d.W1, d.C2, A, st), ++n;
-  pf.end(K_CONV2_FWD, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
-  pf.begin(st);
-  k_pool<<<dim3(4, A * B), 256, 0, st>>>(b.a2, d.H1, d.W1, d.C2, B, wa.bs, b.p2, b.am2), ++n;
-  pf.end(K_POOL2, 0, S * hw1 * d.C2 * (4.0 + 5.0 / 4.0), st);
+  const bool tc = wa.use_tc && conv_tc_supported(L);
+  const int64_t wcl = wa.first ? 1 : wa.wclients;
+  if (tc) {  // tcgen05 implicit GEMM with fused bias + ReLU + pool epilogue
+    pf.begin(st);
+    if (conv2_fwd_tc(L, wa, w.base, wcl, b.p1, b.slots, b.p2, b.am2, st) < 0) return -1;
+    ++n;
+    pf.end(K_CONV2_FWD, f_c2, 4.0 * S * hw1 * d.C1 + 5.0 * S * hw1 * d.C2 / 4.0, st);
+  } else {
+    pf.begin(st);
+    launch(ConvFwd{b.p1, nullptr, wa.bs, B, d.H1, d.W1, d.C1, d.C2, w, L.o_c2w, L.o_c2b, b.a2},
+           B * d.H1 * d.W1, d.C2, A, st), ++n;
+    pf.end(K_CONV2_FWD, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
+    pf.begin(st);
+    k_pool<<<dim3(4, A * B), 256, 0, st>>>(b.a2, d.H1, d.W1, d.C2, B, wa.bs, b.p2, b.am2), ++n;
+    pf.end(K_POOL2, 0, S * hw1 * d.C2 * (4.0 + 5.0 / 4.0), st);
+  }
   pf.begin(st);
   launch(FcFwd{b.p2, wa.bs, B, d.F, d.HID, w, L.o_f1w, L.o_f1b, b.h}, B, d.HID, A, st), ++n;
   pf.end(K_FC1_FWD, f_f1, wbytes + 4.0 * S * (d.F + d.HID), st);
@@ -409,7 +418,12 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
          st), ++n;
   pf.end(K_FC1_DW, f_f1, 2.0 * wbytes + 4.0 * S * (d.F + d.HID), st);
   pf.begin(st);
-  launch(ConvDx{b.dY2, wa.bs, B, d.H1, d.W1, d.C1, d.C2, w, L.o_c2w, b.dp1}, B * d.H1 * d.W1, d.C1, A, st), ++n;
+  if (tc) {
+    if (conv2_dx_tc(L, wa, w.base, wcl, b.dY2, b.slots, b.dp1, st) < 0) return -1;
+    ++n;
+  } else {
+    launch(ConvDx{b.dY2, wa.bs, B, d.H1, d.W1, d.C1, d.C2, w, L.o_c2w, b.dp1}, B * d.H1 * d.W1, d.C1, A, st), ++n;
+  }
   pf.end(K_CONV2_DX, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
   pf.begin(st);
   k_unpool<<<dim3(8, A * B), 256, 0, st>>>(b.dp1, b.p1, b.am1, d.H0, d.W0, d.C1, B, wa.bs, b.dY1), ++n;

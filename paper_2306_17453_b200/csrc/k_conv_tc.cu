@@ -1,0 +1,282 @@
+// k_conv_tc.cu — 5x5 'same' convolutions of the CIFAR CNN's second layer on the 5th-gen
+// tensor cores (tcgen05.mma kind::tf32, fp32 accumulators in TMEM, operands staged by TMA).
+//
+// Implicit GEMM without an im2col buffer.  One CTA computes one sample's 16x16 output
+// plane (M = 256 pixels = two M=128 accumulators) for all output channels N.  For each
+// horizontal tap kw (and 32-channel input chunk q) TMA loads ONE shifted copy of the input
+// plane, copy[h'][x][c] = X[h'-2][x+kw-2][32q+c] for h' in [0,20), x in [0,16), with the
+// zero padding produced by TMA's out-of-bounds fill.  A pixel is a 128-byte SW128 row, so
+// the A operand of tap (kh, kw) for M-half mh is that copy shifted by (8·mh + kh)·16 rows:
+// a descriptor offset, no data movement.  Each input byte is fetched 5 times instead of 25.
+//
+//   conv2 forward: X = p1 (C = 32), B = W2[o][tap][c] K-major, N = 64; epilogue fuses
+//                  bias + ReLU + 2x2 max-pool + argmax (reading A13) -> p2, am2.
+//   conv2 dX:      X = dY2 (C = 64, 2 chunks), B[n=c][k=o] = W2[o][flip tap][c] MN-major,
+//                  N = 32; epilogue stores dp1 (pre-unpool).
+//
+// Warp roles (192 threads): warp 0 TMA producer + TMEM owner, warp 1 MMA issuer, warps
+// 2-5 epilogue (TMEM lane quarter = warp % 4).  PAPER.md P:176 (client SGD) — this is
+// the dominant dense contraction of a client step.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "fl_internal.h"
+#include "tc_common.cuh"
+
+namespace flb {
+
+// ------------------------------------------------------------------ host: tensor maps
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+// swz: 0 none, 1 128B (16-B granules, K-major operands), 2 128B with 32-B atoms (32-bit
+// MN-major operands: matches the SWIZZLE_128B_BASE32B descriptor layout, Swizzle<2,5,2>).
+bool tmap_encode(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_b,
+                 const uint32_t* box, int swz) {
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return false;
+    g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base),
+                        (const cuuint64_t*)dims, (const cuuint64_t*)strides_b, (const cuuint32_t*)box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swz == 1 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : (swz == 2 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_NONE),
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    fprintf(stderr, "cuTensorMapEncodeTiled failed (%d)\n", (int)r);
+    return false;
+  }
+  return true;
+}
+
+namespace {
+
+constexpr int HH = 16, WW = 16;          // conv2 plane (CIFAR)
+constexpr int ROWS = (HH + 4) * WW;      // 320 pixels per shifted copy
+constexpr int A_BYTES = ROWS * 128;      // 40960
+constexpr int NSTAGE = 2;
+
+template <int N, int NB>  // N output channels; NB = rows of one tap's B tile (N, or 32 for MN-major)
+struct ConvSmem {
+  static constexpr int B_TAP = NB * 128;
+  static constexpr int B_BYTES = 5 * B_TAP;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = NSTAGE * STAGE;
+  static constexpr int TOTAL = BAR_OFF + 128 + 1024;  // barriers + tmem slot + alignment slack
+};
+
+struct ConvTcArgs {
+  const int32_t* bs;
+  int B;
+  int wmul;               // 0: every client reads θ_g (first wave), 1: client slot
+  const float* bias;      // bias of client 0; client a at bias + a*bias_stride
+  int64_t bias_stride;
+  float* out;             // fwd: p2 [S][8][8][N]; dx: dp1 [S][16][16][N]
+  uint8_t* am;            // fwd: argmax [S][8][8][N]
+};
+
+// N: output channels; CH: 32-channel chunks of the input; BMN: B operand MN-major;
+// FLIP: transposed conv (dX); POOL: fused bias + ReLU + max-pool epilogue.
+template <int N, int CH, int BMN, int FLIP, int POOL>
+__global__ void __launch_bounds__(192, 1)
+    k_conv5_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, ConvTcArgs p) {
+  constexpr int NB = BMN ? 32 : N;
+  using S = ConvSmem<N, NB>;
+  constexpr uint32_t TMEM_COLS = (2 * N <= 32) ? 32 : (2 * N <= 64 ? 64 : (2 * N <= 128 ? 128 : 256));
+  constexpr uint32_t IDESC = tc::idesc_tf32(128, N, 0, BMN);
+  constexpr int NKB = 5 * CH;
+
+  const int r = blockIdx.x, a = blockIdx.y;
+  if (r >= p.bs[a]) return;
+  const int s = a * p.B + r;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+  uint64_t* empty = full + NSTAGE;
+  uint64_t* tfull = empty + NSTAGE;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::prefetch_tmap(&mapX);
+      tc::prefetch_tmap(&mapW);
+      for (int i = 0; i < NSTAGE; ++i) {
+        tc::mbar_init(full + i, 1);
+        tc::mbar_init(empty + i, 1);
+      }
+      tc::mbar_init(tfull, 1);
+      tc::fence_mbar_init();
+    }
+    __syncwarp();
+    tc::tmem_alloc<TMEM_COLS>(tslot);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (tc::elect_one()) {
+      for (int kb = 0; kb < NKB; ++kb) {
+        const int st = kb % NSTAGE, ph = (kb / NSTAGE) & 1;
+        const int kw = kb / CH, q = kb % CH;
+        tc::mbar_wait(empty + st, ph ^ 1);
+        uint8_t* sa = smem + st * S::STAGE;
+        uint8_t* sb = sa + A_BYTES;
+        tc::mbar_expect_tx(full + st, S::STAGE);
+        tc::tma_load_4d(sa, &mapX, full + st, 32 * q, kw - 2, -2, s);
+        for (int kh = 0; kh < 5; ++kh) {
+          const int tap = FLIP ? (4 - kh) * 5 + (4 - kw) : kh * 5 + kw;
+          tc::tma_load_4d(sb + kh * S::B_TAP, &mapW, full + st, 0, tap, BMN ? 32 * q : 0, a * p.wmul);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread)
+    if (tc::elect_one()) {
+      for (int kb = 0; kb < NKB; ++kb) {
+        const int st = kb % NSTAGE, ph = (kb / NSTAGE) & 1;
+        tc::mbar_wait(full + st, ph);
+        tc::tc_fence_after();
+        const uint32_t sa = tc::smem_u32(smem + st * S::STAGE);
+        const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+        for (int kh = 0; kh < 5; ++kh)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t bd = BMN ? tc::sdesc(sb + kh * S::B_TAP + k * 1024, NB * 128, 512, tc::kSW128_32B)
+                                    : tc::sdesc(sb + kh * S::B_TAP + k * 32, 0, 1024, tc::kSW128);
+#pragma unroll
+            for (int mh = 0; mh < 2; ++mh) {
+              const uint64_t ad = tc::sdesc(sa + (mh * 8 + kh) * WW * 128 + k * 32, 0, 1024, tc::kSW128);
+              tc::mma_tf32(tbase + mh * N, ad, bd, IDESC, (kb | kh | k) != 0);
+            }
+          }
+        tc::mma_commit(empty + st);  // stage free once these MMAs have read it
+      }
+      tc::mma_commit(tfull);         // accumulators complete
+    }
+  } else {
+    // ---------------- epilogue: TMEM -> registers -> global
+    const int qd = warp & 3;                 // TMEM lane quarter of this warp
+    tc::mbar_wait(tfull, 0);
+    tc::tc_fence_after();
+    const int i = qd * 32 + lane;            // accumulator row = pixel within the M-half
+    const float* bias = p.bias + (int64_t)a * p.bias_stride * p.wmul;
+#pragma unroll
+    for (int mh = 0; mh < 2; ++mh) {
+      const int h = mh * 8 + (i >> 4), w = i & 15;
+#pragma unroll
+      for (int n0 = 0; n0 < N; n0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + mh * N + n0, v);
+        if (POOL) {
+          // window (2i..2i+1, 2j..2j+1) = lanes l, l^1, l^16, l^17 of this warp
+          float pv[16];
+          uint8_t pa[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float x00 = v[j] + bias[n0 + j];
+            const float x01 = __shfl_xor_sync(0xffffffffu, x00, 1);
+            const float x10 = __shfl_xor_sync(0xffffffffu, x00, 16);
+            const float x11 = __shfl_xor_sync(0xffffffffu, x00, 17);
+            float bv = x00;
+            int bi = 0;
+            if (x01 > bv) { bv = x01; bi = 1; }
+            if (x10 > bv) { bv = x10; bi = 2; }
+            if (x11 > bv) { bv = x11; bi = 3; }
+            pv[j] = bv > 0.f ? bv : 0.f;
+            pa[j] = (uint8_t)bi;
+          }
+          if ((lane & 17) == 0) {
+            const int64_t o = (((int64_t)s * 8 + (h >> 1)) * 8 + (w >> 1)) * N + n0;
+            float4* dst = reinterpret_cast<float4*>(p.out + o);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = make_float4(pv[4 * j], pv[4 * j + 1], pv[4 * j + 2], pv[4 * j + 3]);
+            uint32_t packed[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              packed[j] = pa[4 * j] | (pa[4 * j + 1] << 8) | (pa[4 * j + 2] << 16) | ((uint32_t)pa[4 * j + 3] << 24);
+            *reinterpret_cast<uint4*>(p.am + o) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+          }
+        } else {
+          const int64_t o = (((int64_t)s * HH + h) * WW + w) * N + n0;
+          float4* dst = reinterpret_cast<float4*>(p.out + o);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<TMEM_COLS>(tbase);
+}
+
+template <int N, int CH, int BMN, int FLIP, int POOL>
+cudaError_t launch_conv5(const CUtensorMap& mx, const CUtensorMap& mw, const ConvTcArgs& p, int A, cudaStream_t st) {
+  constexpr int NB = BMN ? 32 : N;
+  const int smem = ConvSmem<N, NB>::TOTAL;
+  auto kfn = k_conv5_tc<N, CH, BMN, FLIP, POOL>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  kfn<<<dim3(p.B, A), 192, smem, st>>>(mx, mw, p);
+  return cudaGetLastError();
+}
+
+// conv2 weights c2w[o][tap][c] of every client slot (or θ_g) as a 4-D tensor
+// (c, tap, o, client) with a box of {32 c, 1 tap, nb o-rows, 1 client}.
+bool make_w2_map(CUtensorMap* m, const Layout& L, const float* base, int64_t nclients, int nb, int swz) {
+  const CnnDims& d = L.d;
+  uint64_t dims[4] = {(uint64_t)d.C1, 25, (uint64_t)d.C2, (uint64_t)nclients};
+  uint64_t str[3] = {(uint64_t)d.C1 * 4, (uint64_t)25 * d.C1 * 4, (uint64_t)L.P_pad * 4};
+  uint32_t box[4] = {32, 1, (uint32_t)nb, 1};
+  return tmap_encode(m, base + L.o_c2w, 4, dims, str, box, swz);
+}
+
+// NHWC activations [S][16][16][C] with a box of one 20-row x 16-pixel x 32-channel copy.
+bool make_plane_map(CUtensorMap* m, const float* base, int C, int64_t slots) {
+  uint64_t dims[4] = {(uint64_t)C, WW, HH, (uint64_t)slots};
+  uint64_t str[3] = {(uint64_t)C * 4, (uint64_t)C * 4 * WW, (uint64_t)C * 4 * WW * HH};
+  uint32_t box[4] = {32, WW, HH + 4, 1};
+  return tmap_encode(m, base, 4, dims, str, box, 1);
+}
+
+}  // namespace
+
+bool conv_tc_supported(const Layout& L) {
+  return L.model == 1 && L.d.H1 == HH && L.d.W1 == WW && L.d.C1 == 32 && L.d.C2 == 64;
+}
+
+// conv2 forward + bias + ReLU + pool on tensor cores: p1 -> p2, am2.
+int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p1,
+                 int64_t slots, float* p2, uint8_t* am2, cudaStream_t st) {
+  CUtensorMap mx, mw;
+  if (!make_plane_map(&mx, p1, 32, slots) || !make_w2_map(&mw, L, wbase, wclients, 64, 1)) return -1;
+  ConvTcArgs p{wa.bs, wa.B, wa.first ? 0 : 1, wbase + L.o_c2b, L.P_pad, p2, am2};
+  return launch_conv5<64, 1, 0, 0, 1>(mx, mw, p, wa.A, st) == cudaSuccess ? 1 : -1;
+}
+
+// conv2 dX (transposed conv) on tensor cores: dY2 -> dp1.
+int conv2_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dY2,
+                int64_t slots, float* dp1, cudaStream_t st) {
+  CUtensorMap mx, mw;
+  if (!make_plane_map(&mx, dY2, 64, slots) || !make_w2_map(&mw, L, wbase, wclients, 32, 2)) return -1;
+  ConvTcArgs p{wa.bs, wa.B, wa.first ? 0 : 1, nullptr, 0, dp1, nullptr};
+  return launch_conv5<32, 2, 1, 1, 0>(mx, mw, p, wa.A, st) == cudaSuccess ? 1 : -1;
+}
+
+}  // namespace flb

@@ -1,0 +1,97 @@
+"""Layer-level checks of the tensor-core (tcgen05, TF32) kernels.
+
+After one SGD wave of a client from θ_g, each tensor-core layer's output is compared
+with a plain torch CPU fp64 reference of the same op applied to THAT kernel's own
+inputs (read back with fl_debug_read), so upstream differences cannot mask or fake
+an error.  TF32 operands keep 10 mantissa bits: outputs match to ~1e-3 relative in
+norm; pooling argmax may flip only where two window values are that close.
+"""
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import torch.nn.functional as F  # noqa: E402
+
+import paper_2306_17453_b200 as fl  # noqa: E402
+
+B = 32
+TOL = 4e-3  # relative Frobenius error allowed for TF32 tensor-core outputs
+
+
+def params(theta):
+    out, o = {}, 0
+    for n, s in synth.param_shapes("cnn"):
+        k = int(np.prod(s))
+        out[n] = torch.tensor(theta[o:o + k].reshape(s), dtype=torch.float64)
+        o += k
+    return out
+
+
+def one_wave(sizes, math=0):
+    wl = synth.preset("C2", n_pop=len(sizes), n_cohort=len(sizes))
+    _, x, y = synth.population(wl, sizes)
+    theta = synth.init_params("cnn")
+    cfg = fl.Config(model="cnn", batch_size=B, lr=wl.lr, math=math)
+    ctx = fl.fl_round_init(cfg, sizes, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), theta)
+    ctx.fl_place(np.arange(len(sizes)))
+    ctx.fl_train_clients(0)  # single-step clients: the buffers hold wave 0
+    return ctx, theta
+
+
+def nchw(a):  # [S][H][W][C] -> torch [S][C][H][W] fp64
+    return torch.from_numpy(np.ascontiguousarray(a)).double().permute(0, 3, 1, 2)
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-30))
+
+
+SIZES = [np.array([32]), np.array([32, 5, 17])]
+
+
+@pytest.mark.parametrize("sizes", SIZES)
+def test_conv2_forward_pool_tc(sizes):
+    ctx, theta = one_wave(sizes)
+    S = len(sizes) * B
+    p1 = ctx.fl_debug_read("p1", (S, 16, 16, 32))
+    p2 = ctx.fl_debug_read("p2", (S, 8, 8, 64))
+    am2 = ctx.fl_debug_read("am2", (S, 8, 8, 64), np.uint8)
+    P = params(theta)
+    valid = np.concatenate([np.arange(a * B, a * B + int(n)) for a, n in enumerate(sizes)])
+    a2 = F.conv2d(nchw(p1[valid]), P["conv2.w"], P["conv2.b"], padding=2)
+    ref, idx = F.max_pool2d(F.relu(a2), 2, return_indices=True)
+    ref = ref.permute(0, 2, 3, 1).numpy()
+    assert rel(p2[valid], ref) < TOL
+    # argmax: torch's flat index over the 16x16 plane -> window position (di*2 + dj)
+    idx = idx.permute(0, 2, 3, 1).numpy()
+    di, dj = (idx // 16) % 2, (idx % 16) % 2
+    pos = di * 2 + dj
+    positive = ref > 1e-3 * np.abs(ref).max()  # windows with a ReLU-active maximum
+    assert np.mean(am2[valid][positive] == pos[positive]) > 0.995
+
+
+@pytest.mark.parametrize("sizes", SIZES)
+def test_conv2_dx_tc(sizes):
+    ctx, theta = one_wave(sizes)
+    S = len(sizes) * B
+    dY2 = ctx.fl_debug_read("dY2", (S, 16, 16, 64))
+    dp1 = ctx.fl_debug_read("dp1", (S, 16, 16, 32))
+    P = params(theta)
+    valid = np.concatenate([np.arange(a * B, a * B + int(n)) for a, n in enumerate(sizes)])
+    ref = F.conv_transpose2d(nchw(dY2[valid]), P["conv2.w"], padding=2).permute(0, 2, 3, 1).numpy()
+    assert rel(dp1[valid], ref) < TOL
+
+
+def test_tc_path_close_to_fp32_path():
+    """Whole wave: tensor-core path vs FP32 SIMT path on the same client (drift only)."""
+    ctx0, _ = one_wave(np.array([32]), 0)
+    ctx1, _ = one_wave(np.array([32]), 1)
+    for k, shp in [("p2", (32, 8, 8, 64)), ("h", (32, 512))]:
+        assert rel(ctx0.fl_debug_read(k, shp), ctx1.fl_debug_read(k, shp)) < TOL
