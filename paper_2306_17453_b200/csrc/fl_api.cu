@@ -538,7 +538,10 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
     if (P2 > c->cb_part_cap) {
       if (b.part1) cudaFree(b.part1);
       if (b.part2) cudaFree(b.part2);
-      CK(cudaMalloc(&b.part2, sizeof(float) * P2 * d.C2 * (25 * d.C1 + 1)));
+      const int64_t tcz = conv2_dw_tc_part_z(K);
+      CK(cudaMalloc(&b.part2, sizeof(float) * std::max<int64_t>(P2 * d.C2 * (25 * d.C1 + 1),
+                                                                tcz * conv2_dw_tc_z_floats())));
+      b.part2_tc_cap = tcz;
       CK(cudaMalloc(&b.part1, sizeof(float) * P2 * d.C1 * (25 * d.cpad + 1)));
       c->cb_part_cap = P2;
     }

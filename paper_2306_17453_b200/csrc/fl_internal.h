@@ -60,6 +60,7 @@ struct CnnBufs {
   uint8_t *am1 = nullptr, *am2 = nullptr;
   float *dp2 = nullptr, *dY2 = nullptr, *dp1 = nullptr, *dY1 = nullptr;
   float *part2 = nullptr, *part1 = nullptr;  // split-K partials of conv dW (+ bias column)
+  int64_t part2_tc_cap = 0;                   // conv2 dW tensor-core partials capacity (chunks)
 };
 
 // ---------------------------------------------------------------- per-kernel timing
@@ -120,8 +121,18 @@ struct WaveArgs {
 // Kernel launchers (k_*.cu). All asynchronous on `st`. Return the number of launches.
 int cnn_wave_simt(const Layout& L, const WaveArgs& w, const float* xpack, const int32_t* ypack,
                   const float* theta_g, float* slots, CnnBufs& b, cudaStream_t st);
-// tcgen05 kernels (k_conv_tc.cu)
+// TMA tensor-map creation (k_conv_tc.cu); swz 0 none, 1 SWIZZLE_128B, 2 SWIZZLE_128B_ATOM_32B.
+bool tmap_encode(struct CUtensorMap_st* m, const void* base, int rank, const uint64_t* dims,
+                 const uint64_t* strides_b, const uint32_t* box, int swz);
+
+// tcgen05 kernels (k_conv_tc.cu, k_convdw_tc.cu)
 bool conv_tc_supported(const Layout& L);
+int conv2_dw_tc(const Layout& L, const WaveArgs& wa, const float* p1, const float* dY2, int64_t slots, float* part,
+                int64_t part_cap, int* nch_out, int* rpc_out, cudaStream_t st);
+int conv2_dw_reduce_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wsrc_stride, float* dst,
+                       const float* part, int nch, int rpc, cudaStream_t st);
+int64_t conv2_dw_tc_part_z(int64_t max_clients);
+int64_t conv2_dw_tc_z_floats();
 int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p1,
                  int64_t slots, float* p2, uint8_t* am2, cudaStream_t st);
 int conv2_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dY2,

@@ -429,14 +429,26 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   k_unpool<<<dim3(8, A * B), 256, 0, st>>>(b.dp1, b.p1, b.am1, d.H0, d.W0, d.C1, B, wa.bs, b.dY1), ++n;
   pf.end(K_UNPOOL1, 0, S * hw0 * d.C1 * (4.0 + 9.0 / 4.0), st);
   const int rpc = (B + b.nch - 1) / b.nch;
-  pf.begin(st);
-  launch(ConvDw{b.dY2, b.p1, nullptr, wa.bs, B, d.H1, d.W1, d.C1, d.C2, b.nch, rpc, b.part2}, d.C2,
-         25 * d.C1 + 1, A * b.nch, st), ++n;
-  pf.end(K_CONV2_DW, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
-  pf.begin(st);
-  k_dw_reduce_sgd<<<dim3(16, A), 256, 0, st>>>(b.part2, b.nch, rpc, wa.bs, d.C2, 25 * d.C1 + 1, w, L.o_c2w,
-                                               L.o_c2b, slots, L.P_pad, wa.lr), ++n;
-  pf.end(K_CONV2_DWR, 0, 8.0 * A * d.C2 * 25 * d.C1, st);
+  if (tc) {  // tcgen05 dW with all 800 (tap, c) rows resident in TMEM; SGD in the reduction
+    int nch2 = 0, rpc2 = 0;
+    pf.begin(st);
+    if (conv2_dw_tc(L, wa, b.p1, b.dY2, b.slots, b.part2, b.part2_tc_cap, &nch2, &rpc2, st) < 0) return -1;
+    ++n;
+    pf.end(K_CONV2_DW, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
+    pf.begin(st);
+    if (conv2_dw_reduce_tc(L, wa, w.base, w.stride, slots, b.part2, nch2, rpc2, st) < 0) return -1;
+    ++n;
+    pf.end(K_CONV2_DWR, 0, 8.0 * A * d.C2 * 25 * d.C1, st);
+  } else {
+    pf.begin(st);
+    launch(ConvDw{b.dY2, b.p1, nullptr, wa.bs, B, d.H1, d.W1, d.C1, d.C2, b.nch, rpc, b.part2}, d.C2,
+           25 * d.C1 + 1, A * b.nch, st), ++n;
+    pf.end(K_CONV2_DW, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
+    pf.begin(st);
+    k_dw_reduce_sgd<<<dim3(16, A), 256, 0, st>>>(b.part2, b.nch, rpc, wa.bs, d.C2, 25 * d.C1 + 1, w, L.o_c2w,
+                                                 L.o_c2b, slots, L.P_pad, wa.lr), ++n;
+    pf.end(K_CONV2_DWR, 0, 8.0 * A * d.C2 * 25 * d.C1, st);
+  }
   pf.begin(st);
   launch(ConvDw{b.dY1, xpack, wa.sidx, wa.bs, B, d.H0, d.W0, d.cpad, d.C1, b.nch, rpc, b.part1}, d.C1,
          25 * d.cpad + 1, A * b.nch, st), ++n;

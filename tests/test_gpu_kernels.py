@@ -89,6 +89,28 @@ def test_conv2_dx_tc(sizes):
     assert rel(dp1[valid], ref) < TOL
 
 
+def _grad_from_update(ctx, theta, client, lr):
+    """(θ_g − θ_k)/η for a single-step client = its mean gradient (canonical layout)."""
+    return params((theta.astype(np.float64) - ctx.fl_get_client_params(client).astype(np.float64)) / lr)
+
+
+@pytest.mark.parametrize("sizes", SIZES)
+def test_conv2_dw_tc(sizes):
+    ctx, theta = one_wave(sizes)
+    S = len(sizes) * B
+    p1 = ctx.fl_debug_read("p1", (S, 16, 16, 32))
+    dY2 = ctx.fl_debug_read("dY2", (S, 16, 16, 64))
+    lr = synth.preset("C2").lr
+    for a, n in enumerate(sizes):
+        rows = slice(a * B, a * B + int(n))
+        g = _grad_from_update(ctx, theta, a, lr)
+        dy = nchw(dY2[rows])
+        ref_w = torch.nn.grad.conv2d_weight(nchw(p1[rows]), (64, 32, 5, 5), dy, padding=2).numpy()
+        ref_b = dy.sum((0, 2, 3)).numpy()
+        assert rel(g["conv2.w"].numpy(), ref_w) < TOL, a
+        assert rel(g["conv2.b"].numpy(), ref_b) < TOL, a
+
+
 def test_tc_path_close_to_fp32_path():
     """Whole wave: tensor-core path vs FP32 SIMT path on the same client (drift only)."""
     ctx0, _ = one_wave(np.array([32]), 0)
