@@ -282,7 +282,7 @@ void fl_round_destroy(fl_ctx* c) {
   void* ptrs[] = {c->d_theta, c->d_canon_of, c->d_canon, c->d_slots, c->d_S, c->d_xpack, c->d_ypack, c->d_stage,
                   c->d_ystage, c->d_src_row, c->d_n, c->d_steps, c->d_slot_off, c->ws.d_sidx, c->ws.d_bs,
                   c->cb.a1, c->cb.p1, c->cb.a2, c->cb.p2, c->cb.h, c->cb.dh, c->cb.am1, c->cb.am2, c->cb.dp2,
-                  c->cb.dY2, c->cb.dp1, c->cb.dY1, c->cb.part1, c->cb.part2};
+                  c->cb.dY2, c->cb.dp1, c->cb.dY1, c->cb.part1, c->cb.part2, c->cb.xplanar};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_tab) cudaFreeHost(c->h_tab);
@@ -497,6 +497,8 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   // device capacity (grow-only; allocation happens on the first round of a given size)
   CK(grow_dev(c->d_slots, c->slots_cap, std::max<int64_t>(K, 1) * L.P_pad));
   CK(grow_dev(c->d_xpack, c->xpack_cap, std::max<int64_t>(R, 1) * L.D_pack));
+  if (L.model == FL_MODEL_CNN_CIFAR || L.model == FL_MODEL_CNN_SPEECH)
+    CK(grow_dev(c->cb.xplanar, c->cb.xplanar_cap, (c->xpack_cap / L.D_pack) * 16 * L.d.H0 * (L.d.W0 + 4)));
   CK(grow_dev(c->d_ypack, c->ypack_cap, R));
   CK(grow_dev(c->d_src_row, c->src_cap, R));
   CK(grow_dev(c->d_n, c->n_cap, K));
@@ -542,7 +544,8 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       CK(cudaMalloc(&b.part2, sizeof(float) * std::max<int64_t>(P2 * d.C2 * (25 * d.C1 + 1),
                                                                 tcz * conv2_dw_tc_z_floats())));
       b.part2_tc_cap = tcz;
-      CK(cudaMalloc(&b.part1, sizeof(float) * P2 * d.C1 * (25 * d.cpad + 1)));
+      CK(cudaMalloc(&b.part1, sizeof(float) * std::max<int64_t>(P2, tcz) * d.C1 * (25 * d.cpad + 1)));
+      b.part1_tc_cap = tcz;
       c->cb_part_cap = P2;
     }
   }
@@ -581,13 +584,14 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
     srow = nullptr;
   }
   c->prof.begin(st);
-  if (cnn) launches += pack_cnn(L, xsrc, srow, R, c->d_xpack, st);
+  if (cnn) launches += pack_cnn(L, xsrc, srow, R, c->d_xpack, c->cb.xplanar, st);
   else launches += gather_rows_f32(xsrc, srow, R, L.D_pack, c->d_xpack, st);
   launches += gather_i32(ysrc, srow, R, c->d_ypack, st);
   c->prof.end(K_PACK, 0, (double)R * (4.0 * (L.D_in + L.D_pack) + 8.0), st);
   CKL();
   CK(cudaEventRecord(c->ev_staged, st));
   // ---- local SGD
+  c->cb.xrows = c->xpack_cap / L.D_pack;
   int64_t tl = 0;
   if (K > 0) {
     if (cnn) {

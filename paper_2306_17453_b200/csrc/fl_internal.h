@@ -61,6 +61,10 @@ struct CnnBufs {
   float *dp2 = nullptr, *dY2 = nullptr, *dp1 = nullptr, *dY1 = nullptr;
   float *part2 = nullptr, *part1 = nullptr;  // split-K partials of conv dW (+ bias column)
   int64_t part2_tc_cap = 0;                   // conv2 dW tensor-core partials capacity (chunks)
+  int64_t part1_tc_cap = 0;                   // conv1 dW tensor-core partials capacity (chunks)
+  int64_t xrows = 0;                          // rows of the packed input (TMA extent)
+  float* xplanar = nullptr;                   // 4 shifted planar copies [xrows][4 s][4 c][H0][W0+4]
+  int64_t xplanar_cap = 0;
 };
 
 // ---------------------------------------------------------------- per-kernel timing
@@ -133,6 +137,11 @@ int conv2_dw_reduce_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, i
                        const float* part, int nch, int rpc, cudaStream_t st);
 int64_t conv2_dw_tc_part_z(int64_t max_clients);
 int64_t conv2_dw_tc_z_floats();
+bool conv1_tc_supported(const Layout& L);
+int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* xpack,
+                 int64_t xrows, float* a1, cudaStream_t st);
+int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64_t xrows, const float* dY1,
+                int64_t slots, float* part, int64_t part_cap, int* nch_out, int* rpc_out, cudaStream_t st);
 int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p1,
                  int64_t slots, float* p2, uint8_t* am2, cudaStream_t st);
 int conv2_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dY2,
@@ -141,7 +150,7 @@ int logreg_train(const Layout& L, const WaveSched& ws, int n_local, int B, float
                  const int32_t* ypack, const float* theta_g, float* slots, const int32_t* steps_dev,
                  const int64_t* wave_slot_off_dev, cudaStream_t st);
 int pack_cnn(const Layout& L, const float* x_src, const int64_t* src_row, int64_t rows, float* xpack,
-             cudaStream_t st);
+             float* xplanar, cudaStream_t st);
 int gather_rows_f32(const float* src, const int64_t* src_row, int64_t rows, int64_t dim, float* dst,
                     cudaStream_t st);
 int gather_i32(const int32_t* src, const int64_t* src_row, int64_t rows, int32_t* dst, cudaStream_t st);

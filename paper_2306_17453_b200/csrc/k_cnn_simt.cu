@@ -375,9 +375,15 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   const double wbytes = 4.0 * (double)A * (double)d.HID * d.F;  // one pass over the fc1 weights
   int n = 0;
   // ---- forward
+  const bool tc1 = wa.use_tc && conv1_tc_supported(L);
   pf.begin(st);
-  launch(ConvFwd{xpack, wa.sidx, wa.bs, B, d.H0, d.W0, d.cpad, d.C1, w, L.o_c1w, L.o_c1b, b.a1},
-         B * d.H0 * d.W0, d.C1, A, st), ++n;
+  if (tc1) {
+    if (conv1_fwd_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, xpack, b.xrows, b.a1, st) < 0) return -1;
+    ++n;
+  } else {
+    launch(ConvFwd{xpack, wa.sidx, wa.bs, B, d.H0, d.W0, d.cpad, d.C1, w, L.o_c1w, L.o_c1b, b.a1},
+           B * d.H0 * d.W0, d.C1, A, st), ++n;
+  }
   pf.end(K_CONV1_FWD, f_c1, 4.0 * S * hw0 * (d.cin + d.C1), st);
   pf.begin(st);
   k_pool<<<dim3(8, A * B), 256, 0, st>>>(b.a1, d.H0, d.W0, d.C1, B, wa.bs, b.p1, b.am1), ++n;
@@ -449,12 +455,18 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
                                                  L.o_c2b, slots, L.P_pad, wa.lr), ++n;
     pf.end(K_CONV2_DWR, 0, 8.0 * A * d.C2 * 25 * d.C1, st);
   }
+  int nch1 = b.nch, rpc1 = rpc;
   pf.begin(st);
-  launch(ConvDw{b.dY1, xpack, wa.sidx, wa.bs, B, d.H0, d.W0, d.cpad, d.C1, b.nch, rpc, b.part1}, d.C1,
-         25 * d.cpad + 1, A * b.nch, st), ++n;
+  if (tc1) {
+    if (conv1_dw_tc(L, wa, b.xplanar, b.xrows, b.dY1, b.slots, b.part1, b.part1_tc_cap, &nch1, &rpc1, st) < 0) return -1;
+    ++n;
+  } else {
+    launch(ConvDw{b.dY1, xpack, wa.sidx, wa.bs, B, d.H0, d.W0, d.cpad, d.C1, b.nch, rpc, b.part1}, d.C1,
+           25 * d.cpad + 1, A * b.nch, st), ++n;
+  }
   pf.end(K_CONV1_DW, f_c1, 4.0 * S * hw0 * (d.cin + d.C1), st);
   pf.begin(st);
-  k_dw_reduce_sgd<<<dim3(4, A), 256, 0, st>>>(b.part1, b.nch, rpc, wa.bs, d.C1, 25 * d.cpad + 1, w, L.o_c1w,
+  k_dw_reduce_sgd<<<dim3(4, A), 256, 0, st>>>(b.part1, nch1, rpc1, wa.bs, d.C1, 25 * d.cpad + 1, w, L.o_c1w,
                                               L.o_c1b, slots, L.P_pad, wa.lr), ++n;
   pf.end(K_CONV1_DWR, 0, 8.0 * A * d.C1 * 25 * d.cin, st);
   return n;

@@ -132,7 +132,7 @@ int fedavg_finalize(const double* S, int64_t P, const float* theta_g, const doub
 // CHW fp32 -> HWC with channels padded to 4 (16-byte pixels).
 // ---------------------------------------------------------------------------------
 __global__ void k_pack_cnn(const float* __restrict__ x, const int64_t* __restrict__ src_row, int64_t rows, int cin,
-                           int HW, float* __restrict__ out) {
+                           int HW, float* __restrict__ out, float* __restrict__ planar) {
   const int64_t tot = rows * HW;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / HW;
@@ -148,12 +148,37 @@ __global__ void k_pack_cnn(const float* __restrict__ x, const int64_t* __restric
   }
 }
 
+// Four horizontally pre-shifted planar copies of the packed input for the conv1 weight
+// gradient's TMA loads (a TMA box may not start at a non-16-byte-aligned innermost
+// coordinate, so shifts by 1..3 pixels are baked in):
+//   xs[r][s][c][h][w'] = x[r][h][w' + s - 2][c] (0 outside), s in [0,4), w' in [0, W+4).
+__global__ void k_pack_shifted_planar(const float* __restrict__ xpack, int64_t rows, int H, int W,
+                                      float* __restrict__ xs) {
+  const int WP = W + 4;
+  const int64_t per = (int64_t)16 * H * WP;
+  const int64_t tot = rows * per;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / per;
+    int rem = (int)(e - r * per);
+    const int wp = rem % WP;
+    rem /= WP;
+    const int h = rem % H;
+    rem /= H;
+    const int c = rem & 3, s = rem >> 2;
+    const int w = wp + s - 2;
+    xs[e] = (w >= 0 && w < W) ? xpack[((r * H + h) * W + w) * 4 + c] : 0.f;
+  }
+}
+
 int pack_cnn(const Layout& L, const float* x_src, const int64_t* src_row, int64_t rows, float* xpack,
-             cudaStream_t st) {
+             float* xplanar, cudaStream_t st) {
   if (rows <= 0) return 0;
   int HW = L.d.H0 * L.d.W0;
-  k_pack_cnn<<<grid_for(rows * HW, 256, 1 << 20), 256, 0, st>>>(x_src, src_row, rows, L.d.cin, HW, xpack);
-  return 1;
+  k_pack_cnn<<<grid_for(rows * HW, 256, 1 << 20), 256, 0, st>>>(x_src, src_row, rows, L.d.cin, HW, xpack, nullptr);
+  if (!xplanar) return 1;
+  k_pack_shifted_planar<<<grid_for(rows * 16 * L.d.H0 * (L.d.W0 + 4), 256, 1 << 20), 256, 0, st>>>(
+      xpack, rows, L.d.H0, L.d.W0, xplanar);
+  return 2;
 }
 
 __global__ void k_gather_rows(const float* __restrict__ src, const int64_t* __restrict__ src_row, int64_t rows,

@@ -111,6 +111,38 @@ def test_conv2_dw_tc(sizes):
         assert rel(g["conv2.b"].numpy(), ref_b) < TOL, a
 
 
+def client_x(sizes):
+    wl = synth.preset("C2", n_pop=len(sizes), n_cohort=len(sizes))
+    _, x, _ = synth.population(wl, sizes)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    return [torch.from_numpy(x[off[a]:off[a + 1]]).double().reshape(-1, 3, 32, 32) for a in range(len(sizes))]
+
+
+@pytest.mark.parametrize("sizes", SIZES)
+def test_conv1_forward_tc(sizes):
+    ctx, theta = one_wave(sizes)
+    S = len(sizes) * B
+    p1 = ctx.fl_debug_read("p1", (S, 16, 16, 32))
+    P = params(theta)
+    for a, xa in enumerate(client_x(sizes)):
+        ref = F.max_pool2d(F.relu(F.conv2d(xa, P["conv1.w"], P["conv1.b"], padding=2)), 2)
+        assert rel(p1[a * B:a * B + len(xa)], ref.permute(0, 2, 3, 1).numpy()) < TOL, a
+
+
+@pytest.mark.parametrize("sizes", SIZES)
+def test_conv1_dw_tc(sizes):
+    ctx, theta = one_wave(sizes)
+    S = len(sizes) * B
+    dY1 = ctx.fl_debug_read("dY1", (S, 32, 32, 32))
+    lr = synth.preset("C2").lr
+    for a, xa in enumerate(client_x(sizes)):
+        g = _grad_from_update(ctx, theta, a, lr)
+        dy = nchw(dY1[a * B:a * B + len(xa)])
+        ref_w = torch.nn.grad.conv2d_weight(xa, (32, 3, 5, 5), dy, padding=2).numpy()
+        assert rel(g["conv1.w"].numpy(), ref_w) < TOL, a
+        assert rel(g["conv1.b"].numpy(), dy.sum((0, 2, 3)).numpy()) < TOL, a
+
+
 def test_tc_path_close_to_fp32_path():
     """Whole wave: tensor-core path vs FP32 SIMT path on the same client (drift only)."""
     ctx0, _ = one_wave(np.array([32]), 0)
