@@ -282,7 +282,7 @@ void fl_round_destroy(fl_ctx* c) {
   void* ptrs[] = {c->d_theta, c->d_canon_of, c->d_canon, c->d_slots, c->d_S, c->d_xpack, c->d_ypack, c->d_stage,
                   c->d_ystage, c->d_src_row, c->d_n, c->d_steps, c->d_slot_off, c->ws.d_sidx, c->ws.d_bs,
                   c->cb.a1, c->cb.p1, c->cb.a2, c->cb.p2, c->cb.h, c->cb.dh, c->cb.am1, c->cb.am2, c->cb.dp2,
-                  c->cb.dY2, c->cb.dp1, c->cb.dY1, c->cb.part1, c->cb.part2, c->cb.xplanar};
+                  c->cb.dY2, c->cb.dp1, c->cb.dY1, c->cb.part1, c->cb.part2, c->cb.xplanar, c->cb.fc1_part};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_tab) cudaFreeHost(c->h_tab);
@@ -533,8 +533,18 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       CK(cudaMalloc(&b.dp2, sizeof(float) * S * hw2 * d.C2));
       CK(cudaMalloc(&b.h, sizeof(float) * S * d.HID));
       CK(cudaMalloc(&b.dh, sizeof(float) * S * d.HID));
+      // batch-padded tensor-core GEMMs read (and multiply by zero) rows past |b|: keep them finite
+      CK(cudaMemsetAsync(b.p2, 0, sizeof(float) * S * hw2 * d.C2, c->st));
+      CK(cudaMemsetAsync(b.dh, 0, sizeof(float) * S * d.HID, c->st));
+      CK(cudaMemsetAsync(b.p1, 0, sizeof(float) * S * hw1 * d.C1, c->st));
+      CK(cudaMemsetAsync(b.dY2, 0, sizeof(float) * S * hw1 * d.C2, c->st));
+      CK(cudaMemsetAsync(b.dY1, 0, sizeof(float) * S * hw0 * d.C1, c->st));
       c->cb_slots_cap = S;
       b.slots = S;
+    }
+    if (!b.fc1_part) {
+      b.fc1_part_floats = (int64_t)160 * 32 * d.HID;
+      CK(cudaMalloc(&b.fc1_part, sizeof(float) * b.fc1_part_floats));
     }
     const int64_t P2 = (int64_t)K * b.nch;
     if (P2 > c->cb_part_cap) {

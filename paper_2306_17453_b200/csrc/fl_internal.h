@@ -64,6 +64,8 @@ struct CnnBufs {
   int64_t part1_tc_cap = 0;                   // conv1 dW tensor-core partials capacity (chunks)
   int64_t xrows = 0;                          // rows of the packed input (TMA extent)
   float* xplanar = nullptr;                   // 4 shifted planar copies [xrows][4 s][4 c][H0][W0+4]
+  float* fc1_part = nullptr;                  // fc1 forward split-K partials
+  int64_t fc1_part_floats = 0;
   int64_t xplanar_cap = 0;
 };
 
@@ -142,6 +144,13 @@ int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_
                  int64_t xrows, float* a1, cudaStream_t st);
 int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64_t xrows, const float* dY1,
                 int64_t slots, float* part, int64_t part_cap, int* nch_out, int* rpc_out, cudaStream_t st);
+bool fc1_tc_supported(const Layout& L, int B);
+int fc1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p2,
+               int64_t slots, float* h, float* part, int64_t part_floats, cudaStream_t st, int* launches);
+int fc1_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dh,
+              const float* p2, const uint8_t* am2, int64_t slots, float* dY2, cudaStream_t st);
+int fc1_dw_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wstride, float* slots_w,
+              const float* dh, const float* p2, int64_t slots, cudaStream_t st);
 int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p1,
                  int64_t slots, float* p2, uint8_t* am2, cudaStream_t st);
 int conv2_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dY2,

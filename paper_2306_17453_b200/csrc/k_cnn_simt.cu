@@ -339,6 +339,8 @@ __global__ void __launch_bounds__(256) k_head(const float* __restrict__ h, const
     for (int q = 0; q < NCLS; ++q) s = fmaf(Ws[q * HID + n], dz[r * NCLS + q], s);
     dh[hi] = h[hi] > 0.f ? s : 0.f;
   }
+  // rows past the batch are zero, so batch-padded tensor-core GEMMs over K = rows add nothing
+  for (int e = b * HID + threadIdx.x; e < B * HID; e += blockDim.x) dh[(int64_t)z * B * HID + e] = 0.f;
   float* Wd = dst + (int64_t)z * P_pad;
   for (int e = threadIdx.x; e < NCLS * HID; e += blockDim.x) {
     const int q = e / HID, n = e - q * HID;
@@ -404,8 +406,17 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     k_pool<<<dim3(4, A * B), 256, 0, st>>>(b.a2, d.H1, d.W1, d.C2, B, wa.bs, b.p2, b.am2), ++n;
     pf.end(K_POOL2, 0, S * hw1 * d.C2 * (4.0 + 5.0 / 4.0), st);
   }
+  const bool tcf = wa.use_tc && fc1_tc_supported(L, B);
   pf.begin(st);
-  launch(FcFwd{b.p2, wa.bs, B, d.F, d.HID, w, L.o_f1w, L.o_f1b, b.h}, B, d.HID, A, st), ++n;
+  if (tcf) {
+    int nl = 0;
+    if (fc1_fwd_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, b.p2, b.slots, b.h, b.fc1_part, b.fc1_part_floats, st,
+                   &nl) < 0)
+      return -1;
+    n += nl;
+  } else {
+    launch(FcFwd{b.p2, wa.bs, B, d.F, d.HID, w, L.o_f1w, L.o_f1b, b.h}, B, d.HID, A, st), ++n;
+  }
   pf.end(K_FC1_FWD, f_f1, wbytes + 4.0 * S * (d.F + d.HID), st);
   size_t hsm = sizeof(float) * (size_t)(d.NCLS * d.HID + d.NCLS + B * d.NCLS);
   pf.begin(st);
@@ -414,14 +425,25 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   pf.end(K_HEAD, 3.0 * f_f2, 8.0 * A * d.NCLS * d.HID + 8.0 * S * d.HID, st);
   // ---- backward (each layer's dX reads W before its dW epilogue overwrites it)
   pf.begin(st);
-  launch(FcDx{b.dh, wa.bs, B, d.F, d.HID, w, L.o_f1w, b.dp2}, B, d.F, A, st), ++n;
-  pf.end(K_FC1_DX, f_f1, wbytes + 4.0 * S * (d.F + d.HID), st);
+  if (tcf) {  // fused: dp2 -> pool2/ReLU backward -> dY2 in the epilogue
+    if (fc1_dx_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, b.dh, b.p2, b.am2, b.slots, b.dY2, st) < 0) return -1;
+    ++n;
+    pf.end(K_FC1_DX, f_f1, wbytes + 4.0 * S * (d.F + d.HID) + S * hw1 * d.C2 * (9.0 / 4.0), st);
+  } else {
+    launch(FcDx{b.dh, wa.bs, B, d.F, d.HID, w, L.o_f1w, b.dp2}, B, d.F, A, st), ++n;
+    pf.end(K_FC1_DX, f_f1, wbytes + 4.0 * S * (d.F + d.HID), st);
+    pf.begin(st);
+    k_unpool<<<dim3(4, A * B), 256, 0, st>>>(b.dp2, b.p2, b.am2, d.H1, d.W1, d.C2, B, wa.bs, b.dY2), ++n;
+    pf.end(K_UNPOOL2, 0, S * hw1 * d.C2 * (4.0 + 9.0 / 4.0), st);
+  }
   pf.begin(st);
-  k_unpool<<<dim3(4, A * B), 256, 0, st>>>(b.dp2, b.p2, b.am2, d.H1, d.W1, d.C2, B, wa.bs, b.dY2), ++n;
-  pf.end(K_UNPOOL2, 0, S * hw1 * d.C2 * (4.0 + 9.0 / 4.0), st);
-  pf.begin(st);
-  launch(FcDwSgd{b.dh, b.p2, wa.bs, B, d.F, d.HID, w, slots, L.P_pad, L.o_f1w, L.o_f1b, wa.lr}, d.HID, d.F + 1, A,
-         st), ++n;
+  if (tcf) {
+    if (fc1_dw_tc(L, wa, w.base, w.stride, slots, b.dh, b.p2, b.slots, st) < 0) return -1;
+    ++n;
+  } else {
+    launch(FcDwSgd{b.dh, b.p2, wa.bs, B, d.F, d.HID, w, slots, L.P_pad, L.o_f1w, L.o_f1b, wa.lr}, d.HID, d.F + 1, A,
+           st), ++n;
+  }
   pf.end(K_FC1_DW, f_f1, 2.0 * wbytes + 4.0 * S * (d.F + d.HID), st);
   pf.begin(st);
   if (tc) {

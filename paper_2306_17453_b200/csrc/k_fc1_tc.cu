@@ -1,0 +1,412 @@
+// k_fc1_tc.cu — the CNN's fc1 layer (F = 4096 -> HID = 512) on tcgen05 kind::tf32:
+// forward, input gradient (with the pool2/ReLU backward fused in its epilogue) and the
+// weight gradient with the SGD step fused in its epilogue.
+//
+// fc1 holds 97% of the CNN's parameters, so every client step streams its 8 MB weight
+// matrix three times (forward, dX, dW read + write); these kernels are HBM-bound by design
+// and the batch (|b| <= 32) rides in the MMA N dimension ("swap AB"):
+//   forward  D[n][r]  = Σ_k W1[n][k] p2[r][k]      A = W1 tile   (K-major, SW128)
+//                                                   B = p2 rows   (K-major, SW128)
+//            split-K over k when few clients are active (deterministic partial sum).
+//   dX       D[k][r]  = Σ_n W1[n][k] dh[r][n]      A = W1ᵀ tile  (MN-major, BASE32B)
+//                                                   B = dh rows   (K-major, SW128)
+//            epilogue: dp2 -> dY2 through pool2's argmax and ReLU' (writes every dY2 cell).
+//   dW+SGD   D[n][k]  = Σ_r dh[r][n] p2[r][k]      A = dhᵀ, B = p2ᵀ (both MN-major), K = |b|
+//            epilogue: W1 <- W1 − η·D (θ_g read on the first wave), b1 from Σ_r dh.
+// Rows r >= |b| of a client's slots are zero in dh (k_head writes them) and finite in p2,
+// so padding the batch to 32 never changes a sum.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fl_internal.h"
+#include "tc_common.cuh"
+
+namespace flb {
+namespace {
+
+constexpr int NB = 32;   // batch slots per client in the MMA N (or K) dimension
+
+// ------------------------------------------------------------------ forward
+constexpr int FW_A = 128 * 128, FW_B = NB * 128, FW_STAGE = FW_A + FW_B, FW_NST = 6;
+constexpr int FW_BAR = FW_NST * FW_STAGE, FW_SMEM = FW_BAR + 128 + 1024;
+
+struct FwArgs {
+  const int32_t* bs;
+  int B, F, HID, wmul, ksplit, kpb;  // kpb: K-blocks (32 k) per split
+  const float* bias;
+  int64_t bias_stride;
+  float* h;       // [S][HID]  (ksplit == 1)
+  float* part;    // [A][ksplit][NB][HID] (ksplit > 1)
+};
+
+__global__ void __launch_bounds__(192, 1)
+    k_fc1_fwd_tc(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, FwArgs p) {
+  constexpr uint32_t IDESC = tc::idesc_tf32(128, NB, 0, 0);
+  const int a = blockIdx.y, mt = blockIdx.x / p.ksplit, ks = blockIdx.x % p.ksplit;
+  const int bs = p.bs[a];
+  if (bs == 0) return;
+  const int kb0 = ks * p.kpb, kb1 = min(p.F / 32, kb0 + p.kpb), nkb = kb1 - kb0;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + FW_BAR);
+  uint64_t* empty = full + FW_NST;
+  uint64_t* tfull = empty + FW_NST;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::prefetch_tmap(&mapW);
+      tc::prefetch_tmap(&mapX);
+      for (int i = 0; i < FW_NST; ++i) {
+        tc::mbar_init(full + i, 1);
+        tc::mbar_init(empty + i, 1);
+      }
+      tc::mbar_init(tfull, 1);
+      tc::fence_mbar_init();
+    }
+    __syncwarp();
+    tc::tmem_alloc<32>(tslot);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      for (int i = 0; i < nkb; ++i) {
+        const int st = i % FW_NST, ph = (i / FW_NST) & 1, kb = kb0 + i;
+        tc::mbar_wait(empty + st, ph ^ 1);
+        uint8_t* sa = smem + st * FW_STAGE;
+        tc::mbar_expect_tx(full + st, FW_STAGE);
+        tc::tma_load_3d(sa, &mapW, full + st, 32 * kb, 128 * mt, a * p.wmul);
+        tc::tma_load_3d(sa + FW_A, &mapX, full + st, 32 * kb, a * p.B, 0);
+      }
+    }
+  } else if (warp == 1) {
+    if (tc::elect_one()) {
+      for (int i = 0; i < nkb; ++i) {
+        const int st = i % FW_NST, ph = (i / FW_NST) & 1;
+        tc::mbar_wait(full + st, ph);
+        tc::tc_fence_after();
+        const uint32_t sa = tc::smem_u32(smem + st * FW_STAGE), sb = sa + FW_A;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc::mma_tf32(tbase, tc::sdesc(sa + k * 32, 0, 1024, tc::kSW128), tc::sdesc(sb + k * 32, 0, 1024, tc::kSW128),
+                       IDESC, (i | k) != 0);
+        tc::mma_commit(empty + st);
+      }
+      tc::mma_commit(tfull);
+    }
+  } else {
+    const int qd = warp & 3, n = mt * 128 + qd * 32 + lane;
+    tc::mbar_wait(tfull, 0);
+    tc::tc_fence_after();
+    float v[NB];
+    tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16), *reinterpret_cast<float(*)[16]>(v));
+    tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+    if (p.ksplit == 1) {
+      const float b = p.bias[(int64_t)a * p.bias_stride * p.wmul + n];
+      for (int r = 0; r < bs; ++r) {
+        const float x = v[r] + b;
+        p.h[((int64_t)a * p.B + r) * p.HID + n] = x > 0.f ? x : 0.f;
+      }
+    } else {
+      float* out = p.part + (((int64_t)a * p.ksplit + ks) * NB) * p.HID + n;
+      for (int r = 0; r < bs; ++r) out[(int64_t)r * p.HID] = v[r];
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<32>(tbase);
+}
+
+// h = ReLU(Σ_splits part + b1), fixed split order.
+__global__ void k_fc1_fwd_reduce(const float* __restrict__ part, const int32_t* __restrict__ bs, int B, int HID,
+                                 int ksplit, const float* bias, int64_t bias_stride, int wmul, float* h) {
+  const int a = blockIdx.y, n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= HID) return;
+  const float b = bias[(int64_t)a * bias_stride * wmul + n];
+  for (int r = 0; r < bs[a]; ++r) {
+    float s = 0.f;
+    for (int ks = 0; ks < ksplit; ++ks) s += part[(((int64_t)a * ksplit + ks) * NB + r) * HID + n];
+    s += b;
+    h[((int64_t)a * B + r) * HID + n] = s > 0.f ? s : 0.f;
+  }
+}
+
+// ------------------------------------------------------------------ dX (+ pool2 backward)
+constexpr int DX_A = 4 * 32 * 128, DX_B = NB * 128, DX_STAGE = DX_A + DX_B, DX_NST = 4;
+constexpr int DX_BAR = DX_NST * DX_STAGE, DX_SMEM = DX_BAR + 128 + 1024;
+
+struct DxArgs {
+  const int32_t* bs;
+  int B, HID, F, wmul;
+  int H2, W2, C2;           // pooled map (dp2 index k = (h*W2 + w)*C2 + c)
+  const float* p2;
+  const uint8_t* am2;
+  float* dY2;               // [S][2*H2][2*W2][C2]
+};
+
+__global__ void __launch_bounds__(192, 1)
+    k_fc1_dx_tc(const __grid_constant__ CUtensorMap mapWt, const __grid_constant__ CUtensorMap mapDh, DxArgs p) {
+  constexpr uint32_t IDESC = tc::idesc_tf32(128, NB, 1, 0);
+  const int a = blockIdx.y, mt = blockIdx.x;
+  const int bs = p.bs[a];
+  if (bs == 0) return;
+  const int nkb = p.HID / 32;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + DX_BAR);
+  uint64_t* empty = full + DX_NST;
+  uint64_t* tfull = empty + DX_NST;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::prefetch_tmap(&mapWt);
+      tc::prefetch_tmap(&mapDh);
+      for (int i = 0; i < DX_NST; ++i) {
+        tc::mbar_init(full + i, 1);
+        tc::mbar_init(empty + i, 1);
+      }
+      tc::mbar_init(tfull, 1);
+      tc::fence_mbar_init();
+    }
+    __syncwarp();
+    tc::tmem_alloc<32>(tslot);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int st = kb % DX_NST, ph = (kb / DX_NST) & 1;
+        tc::mbar_wait(empty + st, ph ^ 1);
+        uint8_t* sa = smem + st * DX_STAGE;
+        tc::mbar_expect_tx(full + st, DX_STAGE);
+        // W1ᵀ tile: 4 chunks of 32 k (MN) x 32 n rows (K), chunk stride 4096 B
+        tc::tma_load_4d(sa, &mapWt, full + st, 0, 32 * kb, 4 * mt, a * p.wmul);
+        tc::tma_load_3d(sa + DX_A, &mapDh, full + st, 32 * kb, a * p.B, 0);
+      }
+    }
+  } else if (warp == 1) {
+    if (tc::elect_one()) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int st = kb % DX_NST, ph = (kb / DX_NST) & 1;
+        tc::mbar_wait(full + st, ph);
+        tc::tc_fence_after();
+        const uint32_t sa = tc::smem_u32(smem + st * DX_STAGE), sb = sa + DX_A;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc::mma_tf32(tbase, tc::sdesc(sa + k * 1024, 4096, 512, tc::kSW128_32B),
+                       tc::sdesc(sb + k * 32, 0, 1024, tc::kSW128), IDESC, (kb | k) != 0);
+        tc::mma_commit(empty + st);
+      }
+      tc::mma_commit(tfull);
+    }
+  } else {
+    const int qd = warp & 3, k = mt * 128 + qd * 32 + lane;  // dp2 index (h, w, c)
+    tc::mbar_wait(tfull, 0);
+    tc::tc_fence_after();
+    float v[NB];
+    tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16), *reinterpret_cast<float(*)[16]>(v));
+    tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+    const int c = k % p.C2, pw = (k / p.C2) % p.W2, ph = k / (p.C2 * p.W2);
+    const int W1 = 2 * p.W2, H1 = 2 * p.H2;
+    for (int r = 0; r < bs; ++r) {
+      const int64_t s = (int64_t)a * p.B + r;
+      const float g = p.p2[s * p.F + k] > 0.f ? v[r] : 0.f;  // ReLU'(pooled) = ReLU'(argmax)
+      const int am = p.am2[s * p.F + k];
+      float* d = p.dY2 + ((s * H1 + 2 * ph) * W1 + 2 * pw) * p.C2 + c;
+      d[0] = am == 0 ? g : 0.f;
+      d[p.C2] = am == 1 ? g : 0.f;
+      d[(int64_t)W1 * p.C2] = am == 2 ? g : 0.f;
+      d[(int64_t)W1 * p.C2 + p.C2] = am == 3 ? g : 0.f;
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<32>(tbase);
+}
+
+// ------------------------------------------------------------------ dW + SGD
+constexpr int DW_N = 256;
+constexpr int DW_A = 4 * NB * 128, DW_B = (DW_N / 32) * NB * 128;  // 16 KB + 32 KB
+constexpr int DW_BAR = DW_A + DW_B, DW_SMEM = DW_BAR + 64 + 1024;
+
+struct DwArgs {
+  const int32_t* bs;
+  int B, HID, F, ntiles;
+  const float* wsrc;   // client 0 weights (θ_g on the first wave)
+  int64_t wstride;
+  float* dst;          // slots
+  int64_t P_pad, o_w, o_b;
+  const float* dh;     // [S][HID]
+  float lr;
+};
+
+__global__ void __launch_bounds__(192, 1)
+    k_fc1_dw_tc(const __grid_constant__ CUtensorMap mapDh, const __grid_constant__ CUtensorMap mapX, DwArgs p) {
+  constexpr uint32_t IDESC = tc::idesc_tf32(128, DW_N, 1, 1);
+  const int a = blockIdx.y, mt = blockIdx.x / p.ntiles, nt = blockIdx.x % p.ntiles;
+  const int bs = p.bs[a];
+  if (bs == 0) return;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + DW_BAR);
+  uint64_t* tfull = full + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_init(full, 1);
+      tc::mbar_init(tfull, 1);
+      tc::fence_mbar_init();
+    }
+    __syncwarp();
+    tc::tmem_alloc<DW_N>(tslot);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      tc::mbar_expect_tx(full, DW_A + DW_B);
+      tc::tma_load_3d(smem, &mapDh, full, 0, a * p.B, 4 * mt);                   // dhᵀ: 4 chunks of 32 n
+      tc::tma_load_3d(smem + DW_A, &mapX, full, 0, a * p.B, (DW_N / 32) * nt);   // p2ᵀ: 8 chunks of 32 k
+    }
+  } else if (warp == 1) {
+    if (tc::elect_one()) {
+      tc::mbar_wait(full, 0);
+      tc::tc_fence_after();
+      const uint32_t sa = tc::smem_u32(smem), sb = sa + DW_A;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)  // K = 32 batch slots
+        tc::mma_tf32(tbase, tc::sdesc(sa + k * 1024, NB * 128, 512, tc::kSW128_32B),
+                     tc::sdesc(sb + k * 1024, NB * 128, 512, tc::kSW128_32B), IDESC, k != 0);
+      tc::mma_commit(tfull);
+    }
+  } else {
+    const int qd = warp & 3, n = mt * 128 + qd * 32 + lane;
+    tc::mbar_wait(tfull, 0);
+    tc::tc_fence_after();
+    const int64_t row = p.o_w + (int64_t)n * p.F + nt * DW_N;
+    const float* src = p.wsrc + (int64_t)a * p.wstride + row;
+    float* dst = p.dst + (int64_t)a * p.P_pad + row;
+    for (int c0 = 0; c0 < DW_N; c0 += 16) {
+      float v[16];
+      tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + c0, v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 w = *reinterpret_cast<const float4*>(src + c0 + 4 * j);
+        *reinterpret_cast<float4*>(dst + c0 + 4 * j) =
+            make_float4(w.x - p.lr * v[4 * j], w.y - p.lr * v[4 * j + 1], w.z - p.lr * v[4 * j + 2],
+                        w.w - p.lr * v[4 * j + 3]);
+      }
+    }
+    if (nt == 0) {  // bias: Σ_r dh[r][n]
+      float g = 0.f;
+      for (int r = 0; r < bs; ++r) g += p.dh[((int64_t)a * p.B + r) * p.HID + n];
+      p.dst[(int64_t)a * p.P_pad + p.o_b + n] = p.wsrc[(int64_t)a * p.wstride + p.o_b + n] - p.lr * g;
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<DW_N>(tbase);
+}
+
+template <class K>
+void set_smem(K k, int bytes, bool& done) {
+  if (!done) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done = true;
+  }
+}
+
+}  // namespace
+
+bool fc1_tc_supported(const Layout& L, int B) {
+  const CnnDims& d = L.d;
+  return B == NB && d.HID % 128 == 0 && d.F % DW_N == 0 && d.H1 == 2 * d.H2 && d.W1 == 2 * d.W2;
+}
+
+int64_t fc1_tc_part_floats(int64_t max_clients, const Layout& L) { return (max_clients + 2 * 148) * 16 * NB * L.d.HID; }
+
+// forward: p2 -> h (split-K + reduce when few clients are active)
+int fc1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p2,
+               int64_t slots, float* h, float* part, int64_t part_floats, cudaStream_t st, int* launches) {
+  const CnnDims& d = L.d;
+  CUtensorMap mw, mx;
+  uint64_t dw[3] = {(uint64_t)d.F, (uint64_t)d.HID, (uint64_t)wclients};
+  uint64_t sw[2] = {(uint64_t)d.F * 4, (uint64_t)L.P_pad * 4};
+  uint32_t bw[3] = {32, 128, 1};
+  uint64_t dx[3] = {(uint64_t)d.F, (uint64_t)slots, 1};
+  uint64_t sx[2] = {(uint64_t)d.F * 4, (uint64_t)d.F * 4 * slots};
+  uint32_t bx[3] = {32, NB, 1};
+  if (!tmap_encode(&mw, wbase + L.o_f1w, 3, dw, sw, bw, 1) || !tmap_encode(&mx, p2, 3, dx, sx, bx, 1)) return -1;
+  const int mtiles = d.HID / 128, nkb = d.F / 32;
+  int ksplit = (2 * 148 + wa.A * mtiles - 1) / (wa.A * mtiles);
+  ksplit = ksplit < 1 ? 1 : (ksplit > 16 ? 16 : ksplit);
+  while (ksplit > 1 && (int64_t)wa.A * ksplit * NB * d.HID > part_floats) --ksplit;
+  const int kpb = (nkb + ksplit - 1) / ksplit;
+  ksplit = (nkb + kpb - 1) / kpb;
+  static bool attr = false;
+  set_smem(k_fc1_fwd_tc, FW_SMEM, attr);
+  const int wmul = wa.first ? 0 : 1;
+  FwArgs p{wa.bs, wa.B, d.F, d.HID, wmul, ksplit, kpb, wbase + L.o_f1b, L.P_pad, h, part};
+  k_fc1_fwd_tc<<<dim3(mtiles * ksplit, wa.A), 192, FW_SMEM, st>>>(mw, mx, p);
+  *launches = 1;
+  if (ksplit > 1) {
+    k_fc1_fwd_reduce<<<dim3((d.HID + 127) / 128, wa.A), 128, 0, st>>>(part, wa.bs, wa.B, d.HID, ksplit,
+                                                                       wbase + L.o_f1b, L.P_pad, wmul, h);
+    *launches = 2;
+  }
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+// dX: dh -> dp2 -> (pool2/ReLU backward) -> dY2
+int fc1_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dh,
+              const float* p2, const uint8_t* am2, int64_t slots, float* dY2, cudaStream_t st) {
+  const CnnDims& d = L.d;
+  CUtensorMap mw, md;
+  // W1 viewed as (k_in 32, n HID, k_out F/32, client): box {32, 32, 4, 1} = 4 MN chunks x 32 n rows
+  uint64_t dw[4] = {32, (uint64_t)d.HID, (uint64_t)d.F / 32, (uint64_t)wclients};
+  uint64_t sw[3] = {(uint64_t)d.F * 4, 128, (uint64_t)L.P_pad * 4};
+  uint32_t bw[4] = {32, 32, 4, 1};
+  uint64_t dd[3] = {(uint64_t)d.HID, (uint64_t)slots, 1};
+  uint64_t sd[2] = {(uint64_t)d.HID * 4, (uint64_t)d.HID * 4 * slots};
+  uint32_t bd[3] = {32, NB, 1};
+  if (!tmap_encode(&mw, wbase + L.o_f1w, 4, dw, sw, bw, 2) || !tmap_encode(&md, dh, 3, dd, sd, bd, 1)) return -1;
+  static bool attr = false;
+  set_smem(k_fc1_dx_tc, DX_SMEM, attr);
+  DxArgs p{wa.bs, wa.B, d.HID, d.F, wa.first ? 0 : 1, d.H2, d.W2, d.C2, p2, am2, dY2};
+  k_fc1_dx_tc<<<dim3(d.F / 128, wa.A), 192, DX_SMEM, st>>>(mw, md, p);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+// dW + SGD on W1, b1
+int fc1_dw_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wstride, float* slots_w,
+              const float* dh, const float* p2, int64_t slots, cudaStream_t st) {
+  const CnnDims& d = L.d;
+  CUtensorMap mh, mx;
+  // dhᵀ: (n_in 32, slot, n_out HID/32), box {32, 32 slots, 4}
+  uint64_t dh3[3] = {32, (uint64_t)slots, (uint64_t)d.HID / 32};
+  uint64_t sh3[2] = {(uint64_t)d.HID * 4, 128};
+  uint32_t bh3[3] = {32, NB, 4};
+  uint64_t dx3[3] = {32, (uint64_t)slots, (uint64_t)d.F / 32};
+  uint64_t sx3[2] = {(uint64_t)d.F * 4, 128};
+  uint32_t bx3[3] = {32, NB, DW_N / 32};
+  if (!tmap_encode(&mh, dh, 3, dh3, sh3, bh3, 2) || !tmap_encode(&mx, p2, 3, dx3, sx3, bx3, 2)) return -1;
+  static bool attr = false;
+  set_smem(k_fc1_dw_tc, DW_SMEM, attr);
+  const int ntiles = d.F / DW_N, mtiles = d.HID / 128;
+  DwArgs p{wa.bs, wa.B, d.HID, d.F, ntiles, wsrc, wstride, slots_w, L.P_pad, L.o_f1w, L.o_f1b, dh, wa.lr};
+  k_fc1_dw_tc<<<dim3(mtiles * ntiles, wa.A), 192, DW_SMEM, st>>>(mh, mx, p);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+}  // namespace flb

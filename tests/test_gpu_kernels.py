@@ -143,6 +143,58 @@ def test_conv1_dw_tc(sizes):
         assert rel(g["conv1.b"].numpy(), dy.sum((0, 2, 3)).numpy()) < TOL, a
 
 
+def p2_canonical(p2):  # [S][8][8][64] (h, w, c) -> [S][4096] in torch's (c, h, w) flatten order
+    return torch.from_numpy(np.ascontiguousarray(p2)).double().permute(0, 3, 1, 2).reshape(len(p2), -1)
+
+
+@pytest.mark.parametrize("sizes", SIZES)
+def test_fc1_forward_tc(sizes):
+    ctx, theta = one_wave(sizes)
+    S = len(sizes) * B
+    p2 = ctx.fl_debug_read("p2", (S, 8, 8, 64))
+    h = ctx.fl_debug_read("h", (S, 512))
+    P = params(theta)
+    for a, n in enumerate(sizes):
+        rows = slice(a * B, a * B + int(n))
+        ref = F.relu(F.linear(p2_canonical(p2[rows]), P["fc1.w"], P["fc1.b"])).numpy()
+        assert rel(h[rows], ref) < TOL, a
+
+
+@pytest.mark.parametrize("sizes", SIZES)
+def test_fc1_dx_pool_backward_tc(sizes):
+    ctx, theta = one_wave(sizes)
+    S = len(sizes) * B
+    p2 = ctx.fl_debug_read("p2", (S, 8, 8, 64))
+    am2 = ctx.fl_debug_read("am2", (S, 8, 8, 64), np.uint8)
+    dh = ctx.fl_debug_read("dh", (S, 512))
+    dY2 = ctx.fl_debug_read("dY2", (S, 16, 16, 64))
+    P = params(theta)
+    for a, n in enumerate(sizes):
+        rows = slice(a * B, a * B + int(n))
+        dp2 = (torch.from_numpy(dh[rows]).double() @ P["fc1.w"]).reshape(-1, 64, 8, 8).permute(0, 2, 3, 1).numpy()
+        dp2 = np.where(p2[rows] > 0, dp2, 0.0)  # ReLU' of the pooled maximum
+        ref = np.zeros((int(n), 16, 16, 64))
+        for t in range(4):  # window position (di, dj) = divmod(t, 2), reading A13 order
+            di, dj = divmod(t, 2)
+            ref[:, di::2, dj::2, :] = np.where(am2[rows] == t, dp2, 0.0)
+        assert rel(dY2[rows], ref) < TOL, a
+
+
+@pytest.mark.parametrize("sizes", SIZES)
+def test_fc1_dw_sgd_tc(sizes):
+    ctx, theta = one_wave(sizes)
+    S = len(sizes) * B
+    p2 = ctx.fl_debug_read("p2", (S, 8, 8, 64))
+    dh = ctx.fl_debug_read("dh", (S, 512))
+    lr = synth.preset("C2").lr
+    for a, n in enumerate(sizes):
+        rows = slice(a * B, a * B + int(n))
+        g = _grad_from_update(ctx, theta, a, lr)
+        dhr = torch.from_numpy(dh[rows]).double()
+        assert rel(g["fc1.w"].numpy(), (dhr.T @ p2_canonical(p2[rows])).numpy()) < TOL, a
+        assert rel(g["fc1.b"].numpy(), dhr.sum(0).numpy()) < TOL, a
+
+
 def test_tc_path_close_to_fp32_path():
     """Whole wave: tensor-core path vs FP32 SIMT path on the same client (drift only)."""
     ctx0, _ = one_wave(np.array([32]), 0)
