@@ -118,30 +118,60 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+# Kernel classes that run on the tensor cores when math = 0 (tcgen05 kind::tf32).
+TC_KINDS = {"conv1_fwd", "conv2_fwd", "conv2_dx", "conv2_dw", "conv1_dw", "fc1_fwd", "fc1_dx", "fc1_dw_sgd"}
+TF32_PER_BF16 = 1.1 / 2.25   # nominal dense tf32 / bf16 (B200_PROFILING.md table)
+
+
+def kernel_roofline(name, k, math, mp):
+    """One kernel class against its own roofline.
+
+    bound = the resource its ALGORITHMIC intensity (flops / bytes) saturates first:
+    tensor (TF32 peak = measured bf16 sustained x nominal tf32/bf16), HBM (measured
+    copy bandwidth), or, for FP32 CUDA-core GEMMs (math = 1), the FFMA rate."""
+    per_launch_s = k["ms"] / k["launches"] * 1e-3
+    hbm = mp["hbm_gbs"]
+    tensor = k["flops"] > 0 and name in TC_KINDS and math == 0
+    if tensor:
+        peak_f = mp.get("bf16_tflops_sustained", mp["bf16_tflops"]) * TF32_PER_BF16
+        src_f = "measured bf16_tflops_sustained x 1.1/2.25 (tf32/bf16 nominal)"
+    else:
+        peak_f = 148 * 128 * 2 * mp.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        src_f = "FP32 FFMA: 148 SM x 128 lanes x 2 x sm_max_mhz"
+    ridge = peak_f * 1e12 / (hbm * 1e9)
+    if k["flops"] == 0 or k["flops"] / max(k["bytes"], 1.0) < ridge:
+        achieved = k["bytes"] / k["launches"] / per_launch_s / 1e9
+        out = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+               "peak_source": "measured hbm_gbs (copy)"}
+    else:
+        achieved = k["flops"] / k["launches"] / per_launch_s / 1e12
+        out = {"bound": "tensor" if tensor else "alu", "achieved": achieved, "peak": peak_f, "unit": "TFLOP/s",
+               "peak_source": src_f}
+    out["frac"] = out["achieved"] / out["peak"]
+    return out
+
+
 def roofline(kstats, math, total_ms):
-    """Dominant kernel class by device time, against its roofline (DESIGN.md §Roofline)."""
+    """Dominant kernel class by device time, against its roofline."""
     mp, src = peaks()
     name, k = max(kstats.items(), key=lambda kv: kv[1]["ms"])
-    per_launch_ms = k["ms"] / k["launches"]
-    hbm_kinds = {"fedavg_accum", "pack", "pool1", "pool2", "unpool1", "unpool2", "conv1_dw_reduce_sgd",
-                 "conv2_dw_reduce_sgd"}
-    if name in hbm_kinds or k["flops"] == 0:
-        achieved = k["bytes"] / k["launches"] / (per_launch_ms * 1e-3) / 1e9
-        out = {"bound": "hbm", "achieved": achieved, "peak": mp["hbm_gbs"], "unit": "GB/s",
-               "peak_source": f"{src} hbm_gbs (copy)"}
-    elif math == 1 or True:
-        # Round 1: the training GEMMs run on FP32 CUDA cores (no tensor cores yet), so the
-        # ceiling is the FP32 FFMA rate: 148 SMs x 128 lanes x 2 FLOP x sm clock.
-        achieved = k["flops"] / k["launches"] / (per_launch_ms * 1e-3) / 1e12
-        peak = 148 * 128 * 2 * mp.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        out = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-               "peak_source": "FP32 FFMA: 148 SM x 128 lanes x 2 x sm_max_mhz (DESIGN.md)"}
-    out["frac"] = out["achieved"] / out["peak"]
+    out = kernel_roofline(name, k, math, mp)
+    out["peak_source"] = f"{src}: {out['peak_source']}"
     out["kernel"] = name
     out["share_of_round"] = k["ms"] / total_ms if total_ms else None
     out["launches_per_round"] = k["launches"]
     out["traffic"] = ncu_traffic(name)
     return out
+
+
+def kernel_table(kstats, math):
+    mp, _ = peaks()
+    tab = {}
+    for name, k in sorted(kstats.items(), key=lambda kv: -kv[1]["ms"]):
+        r = kernel_roofline(name, k, math, mp)
+        tab[name] = {"ms": round(k["ms"], 4), "launches": k["launches"], "bound": r["bound"],
+                     "achieved": round(r["achieved"], 2), "unit": r["unit"], "frac": round(r["frac"], 4)}
+    return tab
 
 
 def ncu_traffic(kernel_class):
@@ -324,14 +354,17 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
-                "vs_baseline": None, "dtype": "f32" if args.math == 1 or True else "tf32",
+                "vs_baseline": None,
+                "dtype": "f32" if args.math == 1 else "tf32",
+                "precision_note": "tensor-core GEMM operands tf32, fp32 accumulate; fp32 master weights, SGD, "
+                                  "softmax-CE; fp64 FedAvg accumulation",
                 "data": "synthetic (seeded, SURVEY §8d laws), device-resident",
                 "config": {"workload": desc, "clients": int(len(cohort)), "samples": int(sizes.sum()),
                            "B": wl.B, "E": wl.E, "lr": wl.lr, "model": wl.model, "parallelism": f"clients x{world}",
                            "l2": "per-round working set >> 126 MB L2 (no flush needed)"},
                 "round_stats": {k: st[k] for k in ["round_ms", "place_ms", "stage_ms", "train_ms", "agg_ms",
                                                    "allreduce_ms", "waves", "steps_local", "kernels"]},
-                "kernels": {k: {"ms": v["ms"], "launches": v["launches"]} for k, v in kstats.items()},
+                "kernels": kernel_table(kstats, args.math),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": int(st["kernels"]) * args.steps}
         print(json.dumps(line), flush=True)
