@@ -149,12 +149,12 @@ int fc1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t 
                int64_t slots, float* h, float* part, int64_t part_floats, cudaStream_t st, int* launches);
 int fc1_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dh,
               const float* p2, const uint8_t* am2, int64_t slots, float* dY2, cudaStream_t st);
-int fc1_dw_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wstride, float* slots_w,
-              const float* dh, const float* p2, int64_t slots, cudaStream_t st);
+int fc1_dw_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wclients_src, float* slots_w,
+              int64_t wclients_dst, const float* dh, const float* p2, int64_t slots, cudaStream_t st);
 int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p1,
                  int64_t slots, float* p2, uint8_t* am2, cudaStream_t st);
 int conv2_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dY2,
-                int64_t slots, float* dp1, cudaStream_t st);
+                int64_t slots, const float* p1, const uint8_t* am1, float* dY1, cudaStream_t st);
 int logreg_train(const Layout& L, const WaveSched& ws, int n_local, int B, float lr, const float* xpack,
                  const int32_t* ypack, const float* theta_g, float* slots, const int32_t* steps_dev,
                  const int64_t* wave_slot_off_dev, cudaStream_t st);

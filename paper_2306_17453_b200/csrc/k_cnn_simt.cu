@@ -295,7 +295,7 @@ __global__ void k_dw_reduce_sgd(const float* __restrict__ part, int nch, int rpc
 
 // Classifier head of one client per block: logits = h·W2ᵀ + b2, softmax-CE (mean over
 // |b|, reading A9), dz = (p − onehot)/|b|, dh = (dz·W2) ⊙ [h > 0], then SGD on W2, b2.
-__global__ void __launch_bounds__(256) k_head(const float* __restrict__ h, const int32_t* __restrict__ ypack,
+__global__ void __launch_bounds__(512) k_head(const float* __restrict__ h, const int32_t* __restrict__ ypack,
                                               const int32_t* __restrict__ sidx, const int32_t* __restrict__ bs,
                                               int B, int HID, int NCLS, WSrc w, int64_t o_w, int64_t o_b,
                                               float* dst, int64_t P_pad, float lr, float* __restrict__ dh) {
@@ -305,14 +305,17 @@ __global__ void __launch_bounds__(256) k_head(const float* __restrict__ h, const
   float* Ws = sm;                    // [NCLS][HID]
   float* bias = Ws + NCLS * HID;     // [NCLS]
   float* dz = bias + NCLS;           // [B][NCLS]
+  float* hs = dz + B * NCLS;         // [b][HID]: this client's fc1 activations, staged once
   const float* W = w.at(z, o_w);
   for (int e = threadIdx.x; e < NCLS * HID; e += blockDim.x) Ws[e] = W[e];
   for (int e = threadIdx.x; e < NCLS; e += blockDim.x) bias[e] = *w.at(z, o_b + e);
+  const float* hz = h + (int64_t)z * B * HID;
+  for (int e = threadIdx.x; e < b * HID; e += blockDim.x) hs[e] = hz[e];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int idx = warp; idx < b * NCLS; idx += nw) {
     const int r = idx / NCLS, q = idx - r * NCLS;
-    const float* hr = h + ((int64_t)z * B + r) * HID;
+    const float* hr = hs + r * HID;
     float s = 0.f;
     for (int n = lane; n < HID; n += 32) s = fmaf(Ws[q * HID + n], hr[n], s);
 #pragma unroll
@@ -334,10 +337,9 @@ __global__ void __launch_bounds__(256) k_head(const float* __restrict__ h, const
   __syncthreads();
   for (int e = threadIdx.x; e < b * HID; e += blockDim.x) {
     const int r = e / HID, n = e - r * HID;
-    const int64_t hi = ((int64_t)z * B + r) * HID + n;
     float s = 0.f;
     for (int q = 0; q < NCLS; ++q) s = fmaf(Ws[q * HID + n], dz[r * NCLS + q], s);
-    dh[hi] = h[hi] > 0.f ? s : 0.f;
+    dh[((int64_t)z * B + r) * HID + n] = hs[e] > 0.f ? s : 0.f;
   }
   // rows past the batch are zero, so batch-padded tensor-core GEMMs over K = rows add nothing
   for (int e = b * HID + threadIdx.x; e < B * HID; e += blockDim.x) dh[(int64_t)z * B * HID + e] = 0.f;
@@ -345,7 +347,7 @@ __global__ void __launch_bounds__(256) k_head(const float* __restrict__ h, const
   for (int e = threadIdx.x; e < NCLS * HID; e += blockDim.x) {
     const int q = e / HID, n = e - q * HID;
     float g = 0.f;
-    for (int r = 0; r < b; ++r) g = fmaf(dz[r * NCLS + q], h[((int64_t)z * B + r) * HID + n], g);
+    for (int r = 0; r < b; ++r) g = fmaf(dz[r * NCLS + q], hs[r * HID + n], g);
     Wd[o_w + e] = Ws[e] - lr * g;
   }
   if (threadIdx.x < NCLS) {
@@ -418,9 +420,14 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     launch(FcFwd{b.p2, wa.bs, B, d.F, d.HID, w, L.o_f1w, L.o_f1b, b.h}, B, d.HID, A, st), ++n;
   }
   pf.end(K_FC1_FWD, f_f1, wbytes + 4.0 * S * (d.F + d.HID), st);
-  size_t hsm = sizeof(float) * (size_t)(d.NCLS * d.HID + d.NCLS + B * d.NCLS);
+  const size_t hsm = sizeof(float) * (size_t)(d.NCLS * d.HID + d.NCLS + B * d.NCLS + B * d.HID);
+  static size_t hsm_set = 0;
+  if (hsm > hsm_set) {
+    cudaFuncSetAttribute(k_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+    hsm_set = hsm;
+  }
   pf.begin(st);
-  k_head<<<A, 256, hsm, st>>>(b.h, ypack, wa.sidx, wa.bs, B, d.HID, d.NCLS, w, L.o_f2w, L.o_f2b, slots, L.P_pad,
+  k_head<<<A, 512, hsm, st>>>(b.h, ypack, wa.sidx, wa.bs, B, d.HID, d.NCLS, w, L.o_f2w, L.o_f2b, slots, L.P_pad,
                               wa.lr, b.dh), ++n;
   pf.end(K_HEAD, 3.0 * f_f2, 8.0 * A * d.NCLS * d.HID + 8.0 * S * d.HID, st);
   // ---- backward (each layer's dX reads W before its dW epilogue overwrites it)
@@ -438,7 +445,8 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   }
   pf.begin(st);
   if (tcf) {
-    if (fc1_dw_tc(L, wa, w.base, w.stride, slots, b.dh, b.p2, b.slots, st) < 0) return -1;
+    if (fc1_dw_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, slots, wa.wclients, b.dh, b.p2, b.slots, st) < 0)
+      return -1;
     ++n;
   } else {
     launch(FcDwSgd{b.dh, b.p2, wa.bs, B, d.F, d.HID, w, slots, L.P_pad, L.o_f1w, L.o_f1b, wa.lr}, d.HID, d.F + 1, A,
@@ -446,16 +454,17 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   }
   pf.end(K_FC1_DW, f_f1, 2.0 * wbytes + 4.0 * S * (d.F + d.HID), st);
   pf.begin(st);
-  if (tc) {
-    if (conv2_dx_tc(L, wa, w.base, wcl, b.dY2, b.slots, b.dp1, st) < 0) return -1;
+  if (tc) {  // pool1/ReLU backward fused into the epilogue: writes dY1 directly
+    if (conv2_dx_tc(L, wa, w.base, wcl, b.dY2, b.slots, b.p1, b.am1, b.dY1, st) < 0) return -1;
     ++n;
+    pf.end(K_CONV2_DX, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2) + S * hw0 * d.C1 * 4.0 + S * hw1 * d.C1 * 5.0, st);
   } else {
     launch(ConvDx{b.dY2, wa.bs, B, d.H1, d.W1, d.C1, d.C2, w, L.o_c2w, b.dp1}, B * d.H1 * d.W1, d.C1, A, st), ++n;
+    pf.end(K_CONV2_DX, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
+    pf.begin(st);
+    k_unpool<<<dim3(8, A * B), 256, 0, st>>>(b.dp1, b.p1, b.am1, d.H0, d.W0, d.C1, B, wa.bs, b.dY1), ++n;
+    pf.end(K_UNPOOL1, 0, S * hw0 * d.C1 * (4.0 + 9.0 / 4.0), st);
   }
-  pf.end(K_CONV2_DX, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
-  pf.begin(st);
-  k_unpool<<<dim3(8, A * B), 256, 0, st>>>(b.dp1, b.p1, b.am1, d.H0, d.W0, d.C1, B, wa.bs, b.dY1), ++n;
-  pf.end(K_UNPOOL1, 0, S * hw0 * d.C1 * (4.0 + 9.0 / 4.0), st);
   const int rpc = (B + b.nch - 1) / b.nch;
   if (tc) {  // tcgen05 dW with all 800 (tap, c) rows resident in TMEM; SGD in the reduction
     int nch2 = 0, rpc2 = 0;
@@ -488,7 +497,8 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   }
   pf.end(K_CONV1_DW, f_c1, 4.0 * S * hw0 * (d.cin + d.C1), st);
   pf.begin(st);
-  k_dw_reduce_sgd<<<dim3(4, A), 256, 0, st>>>(b.part1, nch1, rpc1, wa.bs, d.C1, 25 * d.cpad + 1, w, L.o_c1w,
+  k_dw_reduce_sgd<<<dim3((d.C1 * (25 * d.cpad + 1) + 127) / 128, A), 128, 0, st>>>(
+      b.part1, nch1, rpc1, wa.bs, d.C1, 25 * d.cpad + 1, w, L.o_c1w,
                                               L.o_c1b, slots, L.P_pad, wa.lr), ++n;
   pf.end(K_CONV1_DWR, 0, 8.0 * A * d.C1 * 25 * d.cin, st);
   return n;

@@ -155,18 +155,24 @@ __global__ void k_pack_cnn(const float* __restrict__ x, const int64_t* __restric
 __global__ void k_pack_shifted_planar(const float* __restrict__ xpack, int64_t rows, int H, int W,
                                       float* __restrict__ xs) {
   const int WP = W + 4;
-  const int64_t per = (int64_t)16 * H * WP;
+  const int64_t per = (int64_t)H * WP;  // one thread per (row r, h, w'): 16 outputs (s, c)
   const int64_t tot = rows * per;
+  const int64_t plane = (int64_t)H * WP;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / per;
-    int rem = (int)(e - r * per);
-    const int wp = rem % WP;
-    rem /= WP;
-    const int h = rem % H;
-    rem /= H;
-    const int c = rem & 3, s = rem >> 2;
-    const int w = wp + s - 2;
-    xs[e] = (w >= 0 && w < W) ? xpack[((r * H + h) * W + w) * 4 + c] : 0.f;
+    const int rem = (int)(e - r * per);
+    const int wp = rem % WP, h = rem / WP;
+    const float4* src = reinterpret_cast<const float4*>(xpack) + (r * H + h) * W;
+    float* out = xs + r * 16 * plane + (int64_t)h * WP + wp;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int w = wp + s - 2;
+      const float4 v = (w >= 0 && w < W) ? src[w] : make_float4(0.f, 0.f, 0.f, 0.f);
+      out[(4 * s + 0) * plane] = v.x;
+      out[(4 * s + 1) * plane] = v.y;
+      out[(4 * s + 2) * plane] = v.z;
+      out[(4 * s + 3) * plane] = v.w;
+    }
   }
 }
 
@@ -176,7 +182,7 @@ int pack_cnn(const Layout& L, const float* x_src, const int64_t* src_row, int64_
   int HW = L.d.H0 * L.d.W0;
   k_pack_cnn<<<grid_for(rows * HW, 256, 1 << 20), 256, 0, st>>>(x_src, src_row, rows, L.d.cin, HW, xpack, nullptr);
   if (!xplanar) return 1;
-  k_pack_shifted_planar<<<grid_for(rows * 16 * L.d.H0 * (L.d.W0 + 4), 256, 1 << 20), 256, 0, st>>>(
+  k_pack_shifted_planar<<<grid_for(rows * L.d.H0 * (L.d.W0 + 4), 256, 1 << 20), 256, 0, st>>>(
       xpack, rows, L.d.H0, L.d.W0, xplanar);
   return 2;
 }

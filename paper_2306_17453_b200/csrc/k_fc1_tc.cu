@@ -124,15 +124,12 @@ __global__ void __launch_bounds__(192, 1)
 // h = ReLU(Σ_splits part + b1), fixed split order.
 __global__ void k_fc1_fwd_reduce(const float* __restrict__ part, const int32_t* __restrict__ bs, int B, int HID,
                                  int ksplit, const float* bias, int64_t bias_stride, int wmul, float* h) {
-  const int a = blockIdx.y, n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= HID) return;
-  const float b = bias[(int64_t)a * bias_stride * wmul + n];
-  for (int r = 0; r < bs[a]; ++r) {
-    float s = 0.f;
-    for (int ks = 0; ks < ksplit; ++ks) s += part[(((int64_t)a * ksplit + ks) * NB + r) * HID + n];
-    s += b;
-    h[((int64_t)a * B + r) * HID + n] = s > 0.f ? s : 0.f;
-  }
+  const int a = blockIdx.z, r = blockIdx.y, n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= HID || r >= bs[a]) return;
+  float s = 0.f;
+  for (int ks = 0; ks < ksplit; ++ks) s += part[(((int64_t)a * ksplit + ks) * NB + r) * HID + n];
+  s += bias[(int64_t)a * bias_stride * wmul + n];
+  h[((int64_t)a * B + r) * HID + n] = s > 0.f ? s : 0.f;
 }
 
 // ------------------------------------------------------------------ dX (+ pool2 backward)
@@ -233,29 +230,38 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ------------------------------------------------------------------ dW + SGD
+// One CTA: a 128 (n) x 256 (k) tile of W1.  The tile (128 KB) is brought into shared
+// memory by TMA alongside the operands, updated there by the epilogue warps
+// (W <- W − η·D, 16-byte accesses in the SW128 pattern, conflict-free), and written back
+// by TMA: the HBM stream is one bulk read and one bulk write of W1 per client step.
 constexpr int DW_N = 256;
 constexpr int DW_A = 4 * NB * 128, DW_B = (DW_N / 32) * NB * 128;  // 16 KB + 32 KB
-constexpr int DW_BAR = DW_A + DW_B, DW_SMEM = DW_BAR + 64 + 1024;
+constexpr int DW_W = (DW_N / 32) * 128 * 128;                        // 8 chunks of [128 n][32 k] = 128 KB
+constexpr int DW_BAR = DW_W + DW_A + DW_B, DW_SMEM = DW_BAR + 64 + 1024;
 
 struct DwArgs {
   const int32_t* bs;
-  int B, HID, F, ntiles;
-  const float* wsrc;   // client 0 weights (θ_g on the first wave)
-  int64_t wstride;
-  float* dst;          // slots
-  int64_t P_pad, o_w, o_b;
+  int B, HID, F, ntiles, wmul;
+  const float* bsrc;   // client 0 bias (θ_g on the first wave); client a at + a*bstride
+  int64_t bstride;
+  float* bdst;         // slot 0 bias; client a at + a*P_pad
+  int64_t P_pad;
   const float* dh;     // [S][HID]
   float lr;
 };
 
 __global__ void __launch_bounds__(192, 1)
-    k_fc1_dw_tc(const __grid_constant__ CUtensorMap mapDh, const __grid_constant__ CUtensorMap mapX, DwArgs p) {
+    k_fc1_dw_tc(const __grid_constant__ CUtensorMap mapDh, const __grid_constant__ CUtensorMap mapX,
+                const __grid_constant__ CUtensorMap mapWsrc, const __grid_constant__ CUtensorMap mapWdst, DwArgs p) {
   constexpr uint32_t IDESC = tc::idesc_tf32(128, DW_N, 1, 1);
   const int a = blockIdx.y, mt = blockIdx.x / p.ntiles, nt = blockIdx.x % p.ntiles;
   const int bs = p.bs[a];
   if (bs == 0) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sw = smem;                  // W tile
+  uint8_t* sa = smem + DW_W;           // dhᵀ
+  uint8_t* sbp = sa + DW_A;            // p2ᵀ
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + DW_BAR);
   uint64_t* tfull = full + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
@@ -275,43 +281,54 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tbase = *tslot;
   if (warp == 0) {
     if (tc::elect_one()) {
-      tc::mbar_expect_tx(full, DW_A + DW_B);
-      tc::tma_load_3d(smem, &mapDh, full, 0, a * p.B, 4 * mt);                   // dhᵀ: 4 chunks of 32 n
-      tc::tma_load_3d(smem + DW_A, &mapX, full, 0, a * p.B, (DW_N / 32) * nt);   // p2ᵀ: 8 chunks of 32 k
+      tc::mbar_expect_tx(full, DW_W + DW_A + DW_B);
+      tc::tma_load_3d(sa, &mapDh, full, 0, a * p.B, 4 * mt);                   // dhᵀ: 4 chunks of 32 n
+      tc::tma_load_3d(sbp, &mapX, full, 0, a * p.B, (DW_N / 32) * nt);         // p2ᵀ: 8 chunks of 32 k
+      for (int j = 0; j < DW_N / 32; ++j)                                       // W tile, 8 x [128 n][32 k]
+        tc::tma_load_3d(sw + j * 16384, &mapWsrc, full, nt * DW_N + 32 * j, 128 * mt, a * p.wmul);
     }
   } else if (warp == 1) {
     if (tc::elect_one()) {
       tc::mbar_wait(full, 0);
       tc::tc_fence_after();
-      const uint32_t sa = tc::smem_u32(smem), sb = sa + DW_A;
+      const uint32_t ua = tc::smem_u32(sa), ub = tc::smem_u32(sbp);
 #pragma unroll
       for (int k = 0; k < 4; ++k)  // K = 32 batch slots
-        tc::mma_tf32(tbase, tc::sdesc(sa + k * 1024, NB * 128, 512, tc::kSW128_32B),
-                     tc::sdesc(sb + k * 1024, NB * 128, 512, tc::kSW128_32B), IDESC, k != 0);
+        tc::mma_tf32(tbase, tc::sdesc(ua + k * 1024, NB * 128, 512, tc::kSW128_32B),
+                     tc::sdesc(ub + k * 1024, NB * 128, 512, tc::kSW128_32B), IDESC, k != 0);
       tc::mma_commit(tfull);
     }
   } else {
-    const int qd = warp & 3, n = mt * 128 + qd * 32 + lane;
+    const int qd = warp & 3, row = qd * 32 + lane, n = mt * 128 + row;
+    tc::mbar_wait(full, 0);  // W tile landed (MMA completion implies it, but be explicit)
     tc::mbar_wait(tfull, 0);
     tc::tc_fence_after();
-    const int64_t row = p.o_w + (int64_t)n * p.F + nt * DW_N;
-    const float* src = p.wsrc + (int64_t)a * p.wstride + row;
-    float* dst = p.dst + (int64_t)a * p.P_pad + row;
-    for (int c0 = 0; c0 < DW_N; c0 += 16) {
-      float v[16];
-      tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + c0, v);
+    for (int j = 0; j < DW_N / 32; ++j) {
+      float v[32];
+      tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + 32 * j, *reinterpret_cast<float(*)[16]>(v));
+      tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + 32 * j + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+      uint8_t* rowp = sw + j * 16384 + row * 128;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float4 w = *reinterpret_cast<const float4*>(src + c0 + 4 * j);
-        *reinterpret_cast<float4*>(dst + c0 + 4 * j) =
-            make_float4(w.x - p.lr * v[4 * j], w.y - p.lr * v[4 * j + 1], w.z - p.lr * v[4 * j + 2],
-                        w.w - p.lr * v[4 * j + 3]);
+      for (int q = 0; q < 8; ++q) {  // 16-byte piece q of the row sits at (q ^ row%8) (SW128)
+        float4* w4 = reinterpret_cast<float4*>(rowp + ((q ^ (row & 7)) << 4));
+        float4 w = *w4;
+        w.x -= p.lr * v[4 * q];
+        w.y -= p.lr * v[4 * q + 1];
+        w.z -= p.lr * v[4 * q + 2];
+        w.w -= p.lr * v[4 * q + 3];
+        *w4 = w;
       }
+    }
+    tc::fence_async_smem();  // generic-proxy writes -> TMA store
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (warp == 2 && tc::elect_one()) {
+      for (int j = 0; j < DW_N / 32; ++j) tc::tma_store_3d(&mapWdst, sw + j * 16384, nt * DW_N + 32 * j, 128 * mt, a);
+      tc::tma_store_commit_wait();
     }
     if (nt == 0) {  // bias: Σ_r dh[r][n]
       float g = 0.f;
       for (int r = 0; r < bs; ++r) g += p.dh[((int64_t)a * p.B + r) * p.HID + n];
-      p.dst[(int64_t)a * p.P_pad + p.o_b + n] = p.wsrc[(int64_t)a * p.wstride + p.o_b + n] - p.lr * g;
+      p.bdst[(int64_t)a * p.P_pad + n] = p.bsrc[(int64_t)a * p.bstride * p.wmul + n] - p.lr * g;
     }
   }
   tc::tc_fence_before();
@@ -361,7 +378,7 @@ int fc1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t 
   k_fc1_fwd_tc<<<dim3(mtiles * ksplit, wa.A), 192, FW_SMEM, st>>>(mw, mx, p);
   *launches = 1;
   if (ksplit > 1) {
-    k_fc1_fwd_reduce<<<dim3((d.HID + 127) / 128, wa.A), 128, 0, st>>>(part, wa.bs, wa.B, d.HID, ksplit,
+    k_fc1_fwd_reduce<<<dim3((d.HID + 127) / 128, wa.B, wa.A), 128, 0, st>>>(part, wa.bs, wa.B, d.HID, ksplit,
                                                                        wbase + L.o_f1b, L.P_pad, wmul, h);
     *launches = 2;
   }
@@ -389,10 +406,10 @@ int fc1_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t w
 }
 
 // dW + SGD on W1, b1
-int fc1_dw_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wstride, float* slots_w,
-              const float* dh, const float* p2, int64_t slots, cudaStream_t st) {
+int fc1_dw_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wclients_src, float* slots_w,
+              int64_t wclients_dst, const float* dh, const float* p2, int64_t slots, cudaStream_t st) {
   const CnnDims& d = L.d;
-  CUtensorMap mh, mx;
+  CUtensorMap mh, mx, mws, mwd;
   // dhᵀ: (n_in 32, slot, n_out HID/32), box {32, 32 slots, 4}
   uint64_t dh3[3] = {32, (uint64_t)slots, (uint64_t)d.HID / 32};
   uint64_t sh3[2] = {(uint64_t)d.HID * 4, 128};
@@ -400,12 +417,21 @@ int fc1_dw_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t ws
   uint64_t dx3[3] = {32, (uint64_t)slots, (uint64_t)d.F / 32};
   uint64_t sx3[2] = {(uint64_t)d.F * 4, 128};
   uint32_t bx3[3] = {32, NB, DW_N / 32};
-  if (!tmap_encode(&mh, dh, 3, dh3, sh3, bh3, 2) || !tmap_encode(&mx, p2, 3, dx3, sx3, bx3, 2)) return -1;
+  // W1 of every client (or θ_g): (k F, n HID, client), box {32 k, 128 n, 1}, SW128
+  uint64_t dws[3] = {(uint64_t)d.F, (uint64_t)d.HID, (uint64_t)wclients_src};
+  uint64_t dwd[3] = {(uint64_t)d.F, (uint64_t)d.HID, (uint64_t)wclients_dst};
+  uint64_t sww[2] = {(uint64_t)d.F * 4, (uint64_t)L.P_pad * 4};
+  uint32_t bww[3] = {32, 128, 1};
+  if (!tmap_encode(&mh, dh, 3, dh3, sh3, bh3, 2) || !tmap_encode(&mx, p2, 3, dx3, sx3, bx3, 2) ||
+      !tmap_encode(&mws, wsrc + L.o_f1w, 3, dws, sww, bww, 1) ||
+      !tmap_encode(&mwd, slots_w + L.o_f1w, 3, dwd, sww, bww, 1))
+    return -1;
   static bool attr = false;
   set_smem(k_fc1_dw_tc, DW_SMEM, attr);
   const int ntiles = d.F / DW_N, mtiles = d.HID / 128;
-  DwArgs p{wa.bs, wa.B, d.HID, d.F, ntiles, wsrc, wstride, slots_w, L.P_pad, L.o_f1w, L.o_f1b, dh, wa.lr};
-  k_fc1_dw_tc<<<dim3(mtiles * ntiles, wa.A), 192, DW_SMEM, st>>>(mh, mx, p);
+  DwArgs p{wa.bs, wa.B, d.HID, d.F, ntiles, wa.first ? 0 : 1, wsrc + L.o_f1b, L.P_pad, slots_w + L.o_f1b,
+           L.P_pad, dh, wa.lr};
+  k_fc1_dw_tc<<<dim3(mtiles * ntiles, wa.A), 192, DW_SMEM, st>>>(mh, mx, mws, mwd, p);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

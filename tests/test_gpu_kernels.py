@@ -77,16 +77,28 @@ def test_conv2_forward_pool_tc(sizes):
     assert np.mean(am2[valid][positive] == pos[positive]) > 0.995
 
 
+def unpool_ref(dp, p, am):
+    """pool backward (reading A13): route dp to the argmax of each 2x2 window if p > 0."""
+    g = np.where(p > 0, dp, 0.0)
+    out = np.zeros((len(dp), 2 * dp.shape[1], 2 * dp.shape[2], dp.shape[3]))
+    for t in range(4):
+        di, dj = divmod(t, 2)
+        out[:, di::2, dj::2, :] = np.where(am == t, g, 0.0)
+    return out
+
+
 @pytest.mark.parametrize("sizes", SIZES)
-def test_conv2_dx_tc(sizes):
+def test_conv2_dx_pool1_backward_tc(sizes):
     ctx, theta = one_wave(sizes)
     S = len(sizes) * B
     dY2 = ctx.fl_debug_read("dY2", (S, 16, 16, 64))
-    dp1 = ctx.fl_debug_read("dp1", (S, 16, 16, 32))
+    p1 = ctx.fl_debug_read("p1", (S, 16, 16, 32))
+    am1 = ctx.fl_debug_read("am1", (S, 16, 16, 32), np.uint8)
+    dY1 = ctx.fl_debug_read("dY1", (S, 32, 32, 32))
     P = params(theta)
     valid = np.concatenate([np.arange(a * B, a * B + int(n)) for a, n in enumerate(sizes)])
-    ref = F.conv_transpose2d(nchw(dY2[valid]), P["conv2.w"], padding=2).permute(0, 2, 3, 1).numpy()
-    assert rel(dp1[valid], ref) < TOL
+    dp1 = F.conv_transpose2d(nchw(dY2[valid]), P["conv2.w"], padding=2).permute(0, 2, 3, 1).numpy()
+    assert rel(dY1[valid], unpool_ref(dp1, p1[valid], am1[valid])) < TOL
 
 
 def _grad_from_update(ctx, theta, client, lr):
