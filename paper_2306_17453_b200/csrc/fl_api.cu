@@ -10,6 +10,7 @@
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -90,6 +91,34 @@ bool make_layout(int model, Layout* L) {
   for (int64_t i = 0; i < (int64_t)d.NCLS * d.HID; ++i) m[(size_t)(L->o_f2w + i)] = c_f2w + i;
   for (int q = 0; q < d.NCLS; ++q) m[(size_t)(L->o_f2b + q)] = c_f2b + q;
   return true;
+}
+
+CnnBufs cnn_group_view(const CnnBufs& b, const CnnDims& d, int B, int64_t base_client, int64_t nclients, int g,
+                       int64_t per_group_z, int64_t part2_z_floats, int64_t part1_z_floats) {
+  CnnBufs v = b;
+  const int64_t s0 = base_client * B;
+  const int64_t hw0 = (int64_t)d.H0 * d.W0, hw1 = (int64_t)d.H1 * d.W1, hw2 = (int64_t)d.H2 * d.W2;
+  v.a1 = b.a1 + s0 * hw0 * d.C1;
+  v.dY1 = b.dY1 + s0 * hw0 * d.C1;
+  v.p1 = b.p1 + s0 * hw1 * d.C1;
+  v.am1 = b.am1 + s0 * hw1 * d.C1;
+  v.dp1 = b.dp1 + s0 * hw1 * d.C1;
+  v.a2 = b.a2 + s0 * hw1 * d.C2;
+  v.dY2 = b.dY2 + s0 * hw1 * d.C2;
+  v.p2 = b.p2 + s0 * hw2 * d.C2;
+  v.am2 = b.am2 + s0 * hw2 * d.C2;
+  v.dp2 = b.dp2 + s0 * hw2 * d.C2;
+  v.h = b.h + s0 * d.HID;
+  v.dh = b.dh + s0 * d.HID;
+  v.dz = b.dz + s0 * d.NCLS;
+  v.slots = nclients * B;
+  v.clients = nclients;
+  v.part2 = b.part2 + (int64_t)g * per_group_z * part2_z_floats;
+  v.part1 = b.part1 + (int64_t)g * per_group_z * part1_z_floats;
+  v.part2_tc_cap = per_group_z;
+  v.part1_tc_cap = per_group_z;
+  v.fc1_part = b.fc1_part + (int64_t)g * b.fc1_part_floats;
+  return v;
 }
 
 }  // namespace flb
@@ -198,6 +227,12 @@ struct fl_ctx {
   fl_round_stats stats{};
   KProf prof;
   std::string err;
+  // concurrent client groups (CNN): streams forked from / joined into st
+  int ngroups = 4;
+  std::vector<cudaStream_t> gstream;
+  std::vector<cudaEvent_t> ev_join;
+  cudaEvent_t ev_fork = nullptr;
+  int64_t part_group_z = 0;
 };
 
 // ---------------------------------------------------------------- error helpers
@@ -282,7 +317,8 @@ void fl_round_destroy(fl_ctx* c) {
   void* ptrs[] = {c->d_theta, c->d_canon_of, c->d_canon, c->d_slots, c->d_S, c->d_xpack, c->d_ypack, c->d_stage,
                   c->d_ystage, c->d_src_row, c->d_n, c->d_steps, c->d_slot_off, c->ws.d_sidx, c->ws.d_bs,
                   c->cb.a1, c->cb.p1, c->cb.a2, c->cb.p2, c->cb.h, c->cb.dh, c->cb.am1, c->cb.am2, c->cb.dp2,
-                  c->cb.dY2, c->cb.dp1, c->cb.dY1, c->cb.part1, c->cb.part2, c->cb.xplanar, c->cb.fc1_part};
+                  c->cb.dY2, c->cb.dp1, c->cb.dY1, c->cb.part1, c->cb.part2, c->cb.xplanar, c->cb.fc1_part,
+                  c->cb.dz};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_tab) cudaFreeHost(c->h_tab);
@@ -292,6 +328,11 @@ void fl_round_destroy(fl_ctx* c) {
   for (cudaEvent_t e : evs)
     if (e) cudaEventDestroy(e);
   if (c->host_registered) cudaHostUnregister((void*)c->x);
+  for (cudaStream_t s : c->gstream)
+    if (s) cudaStreamDestroy(s);
+  for (cudaEvent_t e : c->ev_join)
+    if (e) cudaEventDestroy(e);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
 }
@@ -346,6 +387,14 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   cudaEvent_t* evs[] = {&c->ev_entry, &c->ev_start, &c->ev_staged, &c->ev_trained, &c->ev_agg0,
                         &c->ev_acc1, &c->ev_ar0, &c->ev_ar1, &c->ev_end, &c->ev_tab};
   for (cudaEvent_t* e : evs) CK(cudaEventCreate(e));
+  if (const char* ng = getenv("FL_GROUPS")) c->ngroups = std::max(1, atoi(ng));
+  CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  c->gstream.assign((size_t)c->ngroups, nullptr);
+  c->ev_join.assign((size_t)c->ngroups, nullptr);
+  for (int g = 0; g < c->ngroups; ++g) {
+    CK(cudaStreamCreateWithFlags(&c->gstream[(size_t)g], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_join[(size_t)g], cudaEventDisableTiming));
+  }
   if (!c->pop_dev) {
     // borrowed host population: pin it so per-round staging copies run at full PCIe rate
     size_t xb = (size_t)c->pop_off.back() * (size_t)c->L.D_in * sizeof(float);
@@ -418,6 +467,17 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   std::iota(c->exec.begin(), c->exec.end(), 0);
   auto nb = [&](int64_t i) { return (c->n_samples[(size_t)c->local_ids[(size_t)i]] + B - 1) / B; };
   std::stable_sort(c->exec.begin(), c->exec.end(), [&](int64_t a, int64_t b) { return nb(a) > nb(b); });
+  // Deal the longest-first order round-robin into groups (concurrent streams); each group is
+  // contiguous in execution order and itself longest-first, so its active set is a prefix.
+  const bool cnn_model = (L.model == FL_MODEL_CNN_CIFAR || L.model == FL_MODEL_CNN_SPEECH);
+  const int NG = cnn_model ? (int)std::max<int64_t>(1, std::min<int64_t>(c->ngroups, K)) : 1;
+  if (NG > 1) {
+    std::vector<int64_t> ex2;
+    ex2.reserve((size_t)K);
+    for (int g = 0; g < NG; ++g)
+      for (int64_t e = g; e < K; e += NG) ex2.push_back(c->exec[(size_t)e]);
+    c->exec.swap(ex2);
+  }
   c->steps_exec.resize((size_t)K);
   c->n_exec.resize((size_t)K);
   c->pseg.assign((size_t)K + 1, 0);
@@ -431,17 +491,31 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   }
   const int64_t R = c->pseg[(size_t)K];
   WaveSched& ws = c->ws;
-  ws.n_waves = K ? c->steps_exec[0] : 0;
-  ws.A.assign((size_t)ws.n_waves, 0);
-  ws.slot_off.assign((size_t)ws.n_waves + 1, 0);
-  ws.bs_off.assign((size_t)ws.n_waves + 1, 0);
-  for (int64_t t = 0; t < ws.n_waves; ++t) {
-    int32_t A = 0;
-    while (A < K && c->steps_exec[(size_t)A] > t) ++A;  // prefix property of the exec order
-    ws.A[(size_t)t] = A;
-    ws.slot_off[(size_t)t + 1] = ws.slot_off[(size_t)t] + (int64_t)A * B;
-    ws.bs_off[(size_t)t + 1] = ws.bs_off[(size_t)t] + A;
+  ws.ngroups = NG;
+  ws.gbase.assign((size_t)NG + 1, 0);
+  ws.gn.assign((size_t)NG, 0);
+  ws.gw0.assign((size_t)NG + 1, 0);
+  ws.gnw.assign((size_t)NG, 0);
+  ws.A.clear();
+  ws.slot_off.assign(1, 0);
+  ws.bs_off.assign(1, 0);
+  for (int g = 0; g < NG; ++g) {
+    const int64_t n_g = K > g ? (K - g + NG - 1) / NG : 0;
+    ws.gn[(size_t)g] = n_g;
+    ws.gbase[(size_t)g + 1] = ws.gbase[(size_t)g] + n_g;
+    const int64_t b0 = ws.gbase[(size_t)g];
+    const int64_t nw = n_g ? c->steps_exec[(size_t)b0] : 0;
+    ws.gnw[(size_t)g] = nw;
+    ws.gw0[(size_t)g + 1] = ws.gw0[(size_t)g] + nw;
+    for (int64_t t = 0; t < nw; ++t) {
+      int32_t A = 0;
+      while (A < n_g && c->steps_exec[(size_t)(b0 + A)] > t) ++A;  // prefix property within the group
+      ws.A.push_back(A);
+      ws.slot_off.push_back(ws.slot_off.back() + (int64_t)A * B);
+      ws.bs_off.push_back(ws.bs_off.back() + A);
+    }
   }
+  ws.n_waves = (int64_t)ws.A.size();
   const int64_t n_sidx = ws.slot_off[(size_t)ws.n_waves], n_bs = ws.bs_off[(size_t)ws.n_waves];
   // pinned table layout: src_row[R] i64 | n[K] i64 | slot_off[W+1] i64 | sidx i32 | bs i32 | steps[K] i32
   size_t need = sizeof(int64_t) * (size_t)(R + K + ws.n_waves + 1) + sizeof(int32_t) * (size_t)(n_sidx + n_bs + K) + 64;
@@ -470,27 +544,30 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   for (int64_t t = 0; t <= ws.n_waves; ++t) h_soff[t] = ws.slot_off[(size_t)t];
   // batches: epoch ep of client e uses permutation π_{e,ep} (A5) sliced into m_e batches
   std::vector<int32_t> perm;
-  for (int64_t e = 0; e < K; ++e) {
-    const int64_t n = c->n_exec[(size_t)e], m = (n + B - 1) / B;
-    const int64_t id = c->local_ids[(size_t)c->exec[(size_t)e]];
-    perm.resize((size_t)n);
-    for (int64_t ep = 0; ep < E; ++ep) {
-      if (c->cfg.shuffle) shuffle_perm(c->cfg.seed, (uint64_t)round_index, (uint64_t)id, (uint64_t)ep, n, perm.data());
-      else std::iota(perm.begin(), perm.end(), 0);
-      for (int64_t j = 0; j < m; ++j) {
-        const int64_t t = ep * m + j;
-        int32_t* srow = h_sidx + ws.slot_off[(size_t)t] + e * B;
-        int32_t bsz = 0;
-        for (int64_t r = 0; r < B; ++r) {
-          const int64_t i = j * B + r;
-          if (i < n) {
-            srow[r] = (int32_t)(c->pseg[(size_t)e] + perm[(size_t)i]);
-            ++bsz;
-          } else {
-            srow[r] = -1;
+  for (int g = 0; g < NG; ++g) {
+    for (int64_t el = 0; el < ws.gn[(size_t)g]; ++el) {
+      const int64_t e = ws.gbase[(size_t)g] + el;
+      const int64_t n = c->n_exec[(size_t)e], m = (n + B - 1) / B;
+      const int64_t id = c->local_ids[(size_t)c->exec[(size_t)e]];
+      perm.resize((size_t)n);
+      for (int64_t ep = 0; ep < E; ++ep) {
+        if (c->cfg.shuffle) shuffle_perm(c->cfg.seed, (uint64_t)round_index, (uint64_t)id, (uint64_t)ep, n, perm.data());
+        else std::iota(perm.begin(), perm.end(), 0);
+        for (int64_t j = 0; j < m; ++j) {
+          const int64_t k = ws.gw0[(size_t)g] + ep * m + j;  // flat wave of this step
+          int32_t* srow = h_sidx + ws.slot_off[(size_t)k] + el * B;
+          int32_t bsz = 0;
+          for (int64_t r = 0; r < B; ++r) {
+            const int64_t i = j * B + r;
+            if (i < n) {
+              srow[r] = (int32_t)(c->pseg[(size_t)e] + perm[(size_t)i]);
+              ++bsz;
+            } else {
+              srow[r] = -1;
+            }
           }
+          h_bs[ws.bs_off[(size_t)k] + el] = bsz;
         }
-        h_bs[ws.bs_off[(size_t)t] + e] = bsz;
       }
     }
   }
@@ -517,7 +594,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
     b.nch = (int)std::min<int64_t>(8, B);
     const int64_t S = (int64_t)K * B;  // wave 0 has every local client active
     if (S > c->cb_slots_cap) {
-      void* old[] = {b.a1, b.p1, b.a2, b.p2, b.h, b.dh, b.am1, b.am2, b.dp2, b.dY2, b.dp1, b.dY1};
+      void* old[] = {b.a1, b.p1, b.a2, b.p2, b.h, b.dh, b.am1, b.am2, b.dp2, b.dY2, b.dp1, b.dY1, b.dz};
       for (void* p : old)
         if (p) cudaFree(p);
       const int64_t hw0 = (int64_t)d.H0 * d.W0, hw1 = (int64_t)d.H1 * d.W1, hw2 = (int64_t)d.H2 * d.W2;
@@ -533,6 +610,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       CK(cudaMalloc(&b.dp2, sizeof(float) * S * hw2 * d.C2));
       CK(cudaMalloc(&b.h, sizeof(float) * S * d.HID));
       CK(cudaMalloc(&b.dh, sizeof(float) * S * d.HID));
+      CK(cudaMalloc(&b.dz, sizeof(float) * S * d.NCLS));
       // batch-padded tensor-core GEMMs read (and multiply by zero) rows past |b|: keep them finite
       CK(cudaMemsetAsync(b.p2, 0, sizeof(float) * S * hw2 * d.C2, c->st));
       CK(cudaMemsetAsync(b.dh, 0, sizeof(float) * S * d.HID, c->st));
@@ -542,22 +620,21 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       c->cb_slots_cap = S;
       b.slots = S;
     }
-    if (!b.fc1_part) {
+    // split-K partials: one region per group, each holding the larger of the SIMT path's
+    // K_g·nch chunks and the tensor-core path's K_g + 2·148 chunks
+    const int64_t kg = (K + NG - 1) / NG;
+    const int64_t pg = std::max<int64_t>(kg * b.nch, conv2_dw_tc_part_z(kg));
+    if (pg * NG > c->cb_part_cap) {
+      void* old[] = {b.part1, b.part2, b.fc1_part};
+      for (void* p : old)
+        if (p) cudaFree(p);
+      CK(cudaMalloc(&b.part2, sizeof(float) * NG * pg * std::max<int64_t>(d.C2 * (25 * d.C1 + 1), conv2_dw_tc_z_floats())));
+      CK(cudaMalloc(&b.part1, sizeof(float) * NG * pg * d.C1 * (25 * d.cpad + 1)));
       b.fc1_part_floats = (int64_t)160 * 32 * d.HID;
-      CK(cudaMalloc(&b.fc1_part, sizeof(float) * b.fc1_part_floats));
+      CK(cudaMalloc(&b.fc1_part, sizeof(float) * NG * b.fc1_part_floats));
+      c->cb_part_cap = pg * NG;
     }
-    const int64_t P2 = (int64_t)K * b.nch;
-    if (P2 > c->cb_part_cap) {
-      if (b.part1) cudaFree(b.part1);
-      if (b.part2) cudaFree(b.part2);
-      const int64_t tcz = conv2_dw_tc_part_z(K);
-      CK(cudaMalloc(&b.part2, sizeof(float) * std::max<int64_t>(P2 * d.C2 * (25 * d.C1 + 1),
-                                                                tcz * conv2_dw_tc_z_floats())));
-      b.part2_tc_cap = tcz;
-      CK(cudaMalloc(&b.part1, sizeof(float) * std::max<int64_t>(P2, tcz) * d.C1 * (25 * d.cpad + 1)));
-      b.part1_tc_cap = tcz;
-      c->cb_part_cap = P2;
-    }
+    c->part_group_z = pg;
   }
   c->place_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 
@@ -605,14 +682,30 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   int64_t tl = 0;
   if (K > 0) {
     if (cnn) {
-      for (int64_t t = 0; t < ws.n_waves; ++t) {
-        int64_t sum_bs = 0;
-        for (int32_t a = 0; a < ws.A[(size_t)t]; ++a) sum_bs += h_bs[ws.bs_off[(size_t)t] + a];
-        WaveArgs wa{ws.A[(size_t)t], (int)B, t == 0, ws.d_sidx + ws.slot_off[(size_t)t], ws.d_bs + ws.bs_off[(size_t)t],
-                    c->cfg.lr, sum_bs, &c->prof, c->cfg.math == 0, c->slots_cap / L.P_pad};
-        int nl = cnn_wave_simt(L, wa, c->d_xpack, c->d_ypack, c->d_theta, c->d_slots, c->cb, st);
-        if (nl < 0) return set_err(c, FL_ERR_CUDA, "tensor-core kernel launch / tensor map failed (wave %lld)", (long long)t);
-        tl += nl;
+      // groups run concurrently on their own streams, forked from and joined into st
+      CK(cudaEventRecord(c->ev_fork, st));
+      for (int g = 0; g < ws.ngroups; ++g) {
+        if (ws.gn[(size_t)g] == 0) continue;
+        cudaStream_t gs = c->gstream[(size_t)g];
+        CK(cudaStreamWaitEvent(gs, c->ev_fork, 0));
+        const int64_t base = ws.gbase[(size_t)g];
+        CnnBufs gv = cnn_group_view(c->cb, L.d, (int)B, base, ws.gn[(size_t)g], g, c->part_group_z,
+                                    conv2_dw_tc_z_floats(), (int64_t)L.d.C1 * (25 * L.d.cpad + 1));
+        for (int64_t t = 0; t < ws.gnw[(size_t)g]; ++t) {
+          const int64_t k = ws.gw0[(size_t)g] + t;
+          int64_t sum_bs = 0;
+          for (int32_t a = 0; a < ws.A[(size_t)k]; ++a) sum_bs += h_bs[ws.bs_off[(size_t)k] + a];
+          WaveArgs wa{ws.A[(size_t)k], (int)B, t == 0, ws.d_sidx + ws.slot_off[(size_t)k],
+                      ws.d_bs + ws.bs_off[(size_t)k], c->cfg.lr, sum_bs, &c->prof, c->cfg.math == 0,
+                      ws.gn[(size_t)g]};
+          int nl = cnn_wave_simt(L, wa, c->d_xpack, c->d_ypack, c->d_theta, c->d_slots + base * L.P_pad, gv, gs);
+          if (nl < 0)
+            return set_err(c, FL_ERR_CUDA, "tensor-core kernel launch / tensor map failed (group %d wave %lld)", g,
+                           (long long)t);
+          tl += nl;
+        }
+        CK(cudaEventRecord(c->ev_join[(size_t)g], gs));
+        CK(cudaStreamWaitEvent(st, c->ev_join[(size_t)g], 0));
       }
     } else {
       c->prof.begin(st);

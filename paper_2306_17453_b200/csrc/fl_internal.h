@@ -42,13 +42,18 @@ bool make_layout(int model, Layout* L);
 // Wave t = SGD step t of every local client with more than t steps.  Local clients
 // are executed in order of steps descending, so wave t's active clients are the
 // prefix [0, A_t).  Slot (a, r) = a*B + r holds row r of client a's current batch.
+// Local clients are dealt round-robin (in longest-first order) into G groups that run their
+// waves concurrently on separate streams; group g owns execution indices [base[g],
+// base[g]+n[g]) and flat waves [w0[g], w0[g]+nw[g]).
 struct WaveSched {
-  int64_t n_waves = 0;
-  std::vector<int32_t> A;          // active clients per wave
+  int64_t n_waves = 0;             // flat waves over all groups
+  std::vector<int32_t> A;          // active clients per wave (prefix of its group)
   std::vector<int64_t> slot_off;   // offset of the wave's [A_t*B] sample table
   std::vector<int64_t> bs_off;     // offset of the wave's [A_t] batch-size table
   int32_t* d_sidx = nullptr;       // device: packed sample row or -1
   int32_t* d_bs = nullptr;         // device: |b| of each active client
+  int ngroups = 1;
+  std::vector<int64_t> gbase, gn, gw0, gnw;
 };
 
 // ---------------------------------------------------------------- CNN buffers
@@ -59,6 +64,7 @@ struct CnnBufs {
   float *a1 = nullptr, *p1 = nullptr, *a2 = nullptr, *p2 = nullptr, *h = nullptr, *dh = nullptr;
   uint8_t *am1 = nullptr, *am2 = nullptr;
   float *dp2 = nullptr, *dY2 = nullptr, *dp1 = nullptr, *dY1 = nullptr;
+  float* dz = nullptr;  // [S][NCLS] softmax-CE gradient of the logits
   float *part2 = nullptr, *part1 = nullptr;  // split-K partials of conv dW (+ bias column)
   int64_t part2_tc_cap = 0;                   // conv2 dW tensor-core partials capacity (chunks)
   int64_t part1_tc_cap = 0;                   // conv1 dW tensor-core partials capacity (chunks)
@@ -68,6 +74,12 @@ struct CnnBufs {
   int64_t fc1_part_floats = 0;
   int64_t xplanar_cap = 0;
 };
+
+// The buffers of one client group: every per-slot pointer advanced to the group's first
+// slot, its own split-K partial regions (group g of `per_group` chunk capacity), tensor-map
+// extents = the group's slots.
+CnnBufs cnn_group_view(const CnnBufs& b, const CnnDims& d, int B, int64_t base_client, int64_t nclients, int g,
+                       int64_t per_group_z, int64_t part2_z_floats, int64_t part1_z_floats);
 
 // ---------------------------------------------------------------- per-kernel timing
 // Optional instrumentation: every launch bracketed by CUDA events on the launch stream,
@@ -141,7 +153,7 @@ int64_t conv2_dw_tc_part_z(int64_t max_clients);
 int64_t conv2_dw_tc_z_floats();
 bool conv1_tc_supported(const Layout& L);
 int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* xpack,
-                 int64_t xrows, float* a1, cudaStream_t st);
+                 int64_t xrows, float* p1, uint8_t* am1, cudaStream_t st);
 int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64_t xrows, const float* dY1,
                 int64_t slots, float* part, int64_t part_cap, int* nch_out, int* rpc_out, cudaStream_t st);
 bool fc1_tc_supported(const Layout& L, int B);

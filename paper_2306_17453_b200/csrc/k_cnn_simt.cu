@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "dev_util.cuh"
 #include "fl_internal.h"
 
 namespace flb {
@@ -286,10 +287,106 @@ __global__ void k_dw_reduce_sgd(const float* __restrict__ part, int nch, int rpc
   const int tot = O * N;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {
     float g = 0.f;
-    for (int ch = 0; ch < nvalid; ++ch) g += part[((int64_t)a * nch + ch) * tot + e];
+    g = ordered_sum(part + (int64_t)a * nch * tot + e, nvalid, tot);
     const int m = e / N, n = e - m * N;
     const int64_t off = n < N - 1 ? o_w + (int64_t)m * (N - 1) + n : o_b + m;
     dst[(int64_t)a * P_pad + off] = *w.at(a, off) - lr * g;
+  }
+}
+
+// Classifier head, forward half, parallel over (client, chunk of HR batch rows): logits =
+// h·W2ᵀ + b2, softmax-CE (mean over |b|, reading A9), dz = (p − onehot)/|b| -> dzbuf,
+// dh = (dz·W2) ⊙ [h > 0]; rows past |b| get dz = dh = 0.  Reads W2 before the update.
+constexpr int HR = 4;
+__global__ void __launch_bounds__(256) k_head_fwd(const float* __restrict__ h, const int32_t* __restrict__ ypack,
+                                                  const int32_t* __restrict__ sidx, const int32_t* __restrict__ bs,
+                                                  int B, int HID, int NCLS, WSrc w, int64_t o_w, int64_t o_b,
+                                                  float* __restrict__ dzbuf, float* __restrict__ dh) {
+  extern __shared__ float sm[];
+  const int z = blockIdx.x, r0 = blockIdx.y * HR, b = bs[z];
+  if (r0 >= B) return;
+  float* Ws = sm;                  // [NCLS][HID]
+  float* zs = Ws + NCLS * HID;     // [HR][NCLS]
+  float* hs = zs + HR * NCLS;      // [HR][HID] staged activations
+  const int nr = max(0, min(HR, b - r0));
+  if (nr > 0) {
+    // every global load issued before any use (one round trip), then compute from smem
+    const float4* W4 = reinterpret_cast<const float4*>(w.at(z, o_w));
+    for (int e = threadIdx.x; e < NCLS * HID / 4; e += blockDim.x) reinterpret_cast<float4*>(Ws)[e] = W4[e];
+    const float4* h4 = reinterpret_cast<const float4*>(h + ((int64_t)z * B + r0) * HID);
+    for (int e = threadIdx.x; e < nr * HID / 4; e += blockDim.x) reinterpret_cast<float4*>(hs)[e] = h4[e];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int idx = warp; idx < nr * NCLS; idx += nw) {
+      const int rr = idx / NCLS, q = idx - rr * NCLS;
+      const float* hr = hs + rr * HID;
+      float s = 0.f;
+      for (int n = lane; n < HID; n += 32) s = fmaf(Ws[q * HID + n], hr[n], s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) zs[rr * NCLS + q] = s + *w.at(z, o_b + q);
+    }
+    __syncthreads();
+    if (threadIdx.x < nr) {
+      float* zr = zs + threadIdx.x * NCLS;
+      const int y = ypack[sidx[z * B + r0 + threadIdx.x]];
+      float mx = zr[0];
+      for (int q = 1; q < NCLS; ++q) mx = fmaxf(mx, zr[q]);
+      float s = 0.f;
+      for (int q = 0; q < NCLS; ++q) s += expf(zr[q] - mx);
+      const float inv = 1.f / (float)b;
+      for (int q = 0; q < NCLS; ++q) zr[q] = (expf(zr[q] - mx) / s - (q == y ? 1.f : 0.f)) * inv;
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < HR * NCLS; e += blockDim.x) {
+    const int rr = e / NCLS;
+    if (r0 + rr < B) dzbuf[((int64_t)z * B + r0) * NCLS + e] = rr < nr ? zs[e] : 0.f;
+  }
+  for (int e = threadIdx.x; e < HR * HID; e += blockDim.x) {
+    const int rr = e / HID, n = e - rr * HID;
+    if (r0 + rr >= B) continue;
+    const int64_t hi = ((int64_t)z * B + r0 + rr) * HID + n;
+    float s = 0.f;
+    if (rr < nr) {
+      for (int q = 0; q < NCLS; ++q) s = fmaf(Ws[q * HID + n], zs[rr * NCLS + q], s);
+      s = hs[rr * HID + n] > 0.f ? s : 0.f;
+    }
+    dh[hi] = s;
+  }
+}
+
+// Classifier head, update half, parallel over (client, 64-column chunk): W2 <- W2 − η·dzᵀh,
+// b2 <- b2 − η·Σ_r dz (chunk 0).
+__global__ void __launch_bounds__(256) k_head_sgd(const float* __restrict__ h, const float* __restrict__ dzbuf,
+                                                  const int32_t* __restrict__ bs, int B, int HID, int NCLS, WSrc w,
+                                                  int64_t o_w, int64_t o_b, float* dst, int64_t P_pad, float lr) {
+  extern __shared__ float sm[];
+  const int z = blockIdx.x, n0 = blockIdx.y * 64, b = bs[z];
+  if (b == 0) return;
+  float* dzs = sm;                 // [b][NCLS]
+  float* hs = dzs + B * NCLS;      // [b][64] columns n0.. of h
+  float* Wd = dst + (int64_t)z * P_pad;
+  const float* dzz = dzbuf + (int64_t)z * B * NCLS;
+  const float* hz = h + (int64_t)z * B * HID;
+  for (int e = threadIdx.x; e < b * NCLS; e += blockDim.x) dzs[e] = dzz[e];
+  for (int e = threadIdx.x; e < b * 64; e += blockDim.x) {
+    const int r = e >> 6, n = n0 + (e & 63);
+    hs[e] = n < HID ? hz[(int64_t)r * HID + n] : 0.f;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < NCLS * 64; e += blockDim.x) {
+    const int q = e / 64, nl = e & 63, n = n0 + nl;
+    if (n >= HID) continue;
+    float g = 0.f;
+    for (int r = 0; r < b; ++r) g = fmaf(dzs[r * NCLS + q], hs[r * 64 + nl], g);
+    Wd[o_w + q * HID + n] = *w.at(z, o_w + q * HID + n) - lr * g;
+  }
+  if (blockIdx.y == 0 && threadIdx.x < NCLS) {
+    const int q = threadIdx.x;
+    float g = 0.f;
+    for (int r = 0; r < b; ++r) g += dzs[r * NCLS + q];
+    Wd[o_b + q] = *w.at(z, o_b + q) - lr * g;
   }
 }
 
@@ -381,17 +478,18 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   // ---- forward
   const bool tc1 = wa.use_tc && conv1_tc_supported(L);
   pf.begin(st);
-  if (tc1) {
-    if (conv1_fwd_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, xpack, b.xrows, b.a1, st) < 0) return -1;
+  if (tc1) {  // bias + ReLU + pool fused into the epilogue
+    if (conv1_fwd_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, xpack, b.xrows, b.p1, b.am1, st) < 0) return -1;
     ++n;
+    pf.end(K_CONV1_FWD, f_c1, 4.0 * S * hw0 * d.cin + 5.0 * S * hw1 * d.C1, st);
   } else {
     launch(ConvFwd{xpack, wa.sidx, wa.bs, B, d.H0, d.W0, d.cpad, d.C1, w, L.o_c1w, L.o_c1b, b.a1},
            B * d.H0 * d.W0, d.C1, A, st), ++n;
+    pf.end(K_CONV1_FWD, f_c1, 4.0 * S * hw0 * (d.cin + d.C1), st);
+    pf.begin(st);
+    k_pool<<<dim3(8, A * B), 256, 0, st>>>(b.a1, d.H0, d.W0, d.C1, B, wa.bs, b.p1, b.am1), ++n;
+    pf.end(K_POOL1, 0, S * hw0 * d.C1 * (4.0 + 5.0 / 4.0), st);
   }
-  pf.end(K_CONV1_FWD, f_c1, 4.0 * S * hw0 * (d.cin + d.C1), st);
-  pf.begin(st);
-  k_pool<<<dim3(8, A * B), 256, 0, st>>>(b.a1, d.H0, d.W0, d.C1, B, wa.bs, b.p1, b.am1), ++n;
-  pf.end(K_POOL1, 0, S * hw0 * d.C1 * (4.0 + 5.0 / 4.0), st);
   const bool tc = wa.use_tc && conv_tc_supported(L);
   const int64_t wcl = wa.first ? 1 : wa.wclients;
   if (tc) {  // tcgen05 implicit GEMM with fused bias + ReLU + pool epilogue
@@ -420,15 +518,17 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     launch(FcFwd{b.p2, wa.bs, B, d.F, d.HID, w, L.o_f1w, L.o_f1b, b.h}, B, d.HID, A, st), ++n;
   }
   pf.end(K_FC1_FWD, f_f1, wbytes + 4.0 * S * (d.F + d.HID), st);
-  const size_t hsm = sizeof(float) * (size_t)(d.NCLS * d.HID + d.NCLS + B * d.NCLS + B * d.HID);
+  const size_t hsm = sizeof(float) * (size_t)(d.NCLS * d.HID + HR * d.NCLS + HR * d.HID);
   static size_t hsm_set = 0;
   if (hsm > hsm_set) {
-    cudaFuncSetAttribute(k_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+    cudaFuncSetAttribute(k_head_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
     hsm_set = hsm;
   }
   pf.begin(st);
-  k_head<<<A, 512, hsm, st>>>(b.h, ypack, wa.sidx, wa.bs, B, d.HID, d.NCLS, w, L.o_f2w, L.o_f2b, slots, L.P_pad,
-                              wa.lr, b.dh), ++n;
+  k_head_fwd<<<dim3(A, (B + HR - 1) / HR), 256, hsm, st>>>(b.h, ypack, wa.sidx, wa.bs, B, d.HID, d.NCLS, w, L.o_f2w,
+                                                          L.o_f2b, b.dz, b.dh), ++n;
+  k_head_sgd<<<dim3(A, (d.HID + 63) / 64), 256, sizeof(float) * B * (d.NCLS + 64), st>>>(b.h, b.dz, wa.bs, B, d.HID, d.NCLS, w, L.o_f2w, L.o_f2b,
+                                                          slots, L.P_pad, wa.lr), ++n;
   pf.end(K_HEAD, 3.0 * f_f2, 8.0 * A * d.NCLS * d.HID + 8.0 * S * d.HID, st);
   // ---- backward (each layer's dX reads W before its dW epilogue overwrites it)
   pf.begin(st);

@@ -30,7 +30,8 @@ constexpr int H = 32, W = 32, C1 = 32, ROWB = W * 16;  // 512 B per image row of
 constexpr int F_COPY = (H + 4) * ROWB;          // 18432 B, 36 rows
 constexpr int F_A = 5 * F_COPY;                 // 92160
 constexpr int F_B = 30 * 512;                   // (kw, kh = 0..5) x [32 o][4 c]
-constexpr int F_BAR = F_A + F_B;
+constexpr int F_XCH = F_A + F_B;                // epilogue exchange buffer [4][32][16] fp32
+constexpr int F_BAR = F_XCH + 4 * 32 * 16 * 4;
 constexpr int F_SMEM = F_BAR + 64 + 1024;
 
 struct C1Args {
@@ -39,7 +40,8 @@ struct C1Args {
   int B, wmul;
   const float* bias;  // client 0 bias; client a at + a*stride*wmul
   int64_t bias_stride;
-  float* a1;          // [S][32][32][32] pre-activation
+  float* p1;          // [S][16][16][32] pooled ReLU output
+  uint8_t* am1;       // [S][16][16][32] window argmax
 };
 
 __global__ void __launch_bounds__(192, 2)
@@ -94,19 +96,43 @@ __global__ void __launch_bounds__(192, 2)
     const int qd = warp & 3;
     tc::mbar_wait(tfull, 0);
     tc::tc_fence_after();
+    // bias + ReLU + 2x2 max-pool (first maximum in row-major window order, reading A13).
+    // Tile j holds image rows 4j..4j+3, one row per warp; the vertical window partner is
+    // in the next warp, so each 16-channel chunk is exchanged through shared memory.
     const float* bias = p.bias + (int64_t)a * p.bias_stride * p.wmul;
+    float* xb = reinterpret_cast<float*>(smem + F_XCH);  // [4 rows][32 w][16 c]
+    const int t = threadIdx.x - 64;                    // 0..127 over the epilogue warps
     for (int j = 0; j < 8; ++j) {
-      const int px = j * 128 + qd * 32 + lane;  // = h*32 + w
-      float* dst = p.a1 + ((int64_t)s * H * W + px) * C1;
-#pragma unroll
+#pragma unroll 1
       for (int n0 = 0; n0 < C1; n0 += 16) {
         float v[16];
         tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + j * C1 + n0, v);
-        float4* d4 = reinterpret_cast<float4*>(dst + n0);
+        float4* xr = reinterpret_cast<float4*>(xb + (qd * 32 + lane) * 16);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          d4[i] = make_float4(v[4 * i] + bias[n0 + 4 * i], v[4 * i + 1] + bias[n0 + 4 * i + 1],
+          xr[i] = make_float4(v[4 * i] + bias[n0 + 4 * i], v[4 * i + 1] + bias[n0 + 4 * i + 1],
                               v[4 * i + 2] + bias[n0 + 4 * i + 2], v[4 * i + 3] + bias[n0 + 4 * i + 3]);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        // thread t -> pooled row (t >> 6), pooled column ((t >> 2) & 15), channels 4(t & 3)..+3
+        const int pr = t >> 6, pc = (t >> 2) & 15, c4 = t & 3;
+        const float* q00 = xb + ((2 * pr) * 32 + 2 * pc) * 16 + 4 * c4;
+        float4 r;
+        uint32_t am = 0;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const float x00 = q00[cc], x01 = q00[16 + cc], x10 = q00[32 * 16 + cc], x11 = q00[33 * 16 + cc];
+          float bv = x00;
+          uint32_t bi = 0;
+          if (x01 > bv) { bv = x01; bi = 1; }
+          if (x10 > bv) { bv = x10; bi = 2; }
+          if (x11 > bv) { bv = x11; bi = 3; }
+          reinterpret_cast<float*>(&r)[cc] = bv > 0.f ? bv : 0.f;
+          am |= bi << (8 * cc);
+        }
+        const int64_t o = (((int64_t)s * 16 + 2 * j + pr) * 16 + pc) * C1 + n0 + 4 * c4;
+        *reinterpret_cast<float4*>(p.p1 + o) = r;
+        *reinterpret_cast<uint32_t*>(p.am1 + o) = am;
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // buffer reused by the next chunk
       }
     }
   }
@@ -240,7 +266,7 @@ __global__ void __launch_bounds__(192, 1)
 
 // conv1 forward (+ bias) on tensor cores: packed input rows -> a1 (pre-activation).
 int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* xpack,
-                 int64_t xrows, float* a1, cudaStream_t st) {
+                 int64_t xrows, float* p1, uint8_t* am1, cudaStream_t st) {
   CUtensorMap mx, mw;
   uint64_t dx[4] = {4, W, H, (uint64_t)xrows};
   uint64_t sx[3] = {16, 16 * W, 16 * W * H};
@@ -254,7 +280,7 @@ int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_
     cudaFuncSetAttribute(k_conv1_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM);
     attr = true;
   }
-  C1Args p{wa.sidx, wa.bs, wa.B, wa.first ? 0 : 1, wbase + L.o_c1b, L.P_pad, a1};
+  C1Args p{wa.sidx, wa.bs, wa.B, wa.first ? 0 : 1, wbase + L.o_c1b, L.P_pad, p1, am1};
   k_conv1_fwd_tc<<<dim3(wa.B, wa.A), 192, F_SMEM, st>>>(mx, mw, p);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "dev_util.cuh"
 #include "fl_internal.h"
 #include "tc_common.cuh"
 
@@ -164,7 +165,7 @@ __global__ void k_dw2_reduce_sgd(const float* __restrict__ part, int nch, int rp
   const float* pa = part + (int64_t)a * nch * NROW * NO;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < NROW * NO; e += gridDim.x * blockDim.x) {
     float g = 0.f;
-    for (int c = 0; c < nvalid; ++c) g += pa[(int64_t)c * NROW * NO + e];
+    g = ordered_sum(pa + e, nvalid, (int64_t)NROW * NO);
     const int row = e / NO, o = e - row * NO;
     const int64_t idx = row < 800 ? o_w + (int64_t)o * 800 + row : o_b + o;
     dst[(int64_t)a * P_pad + idx] = wsrc[(int64_t)a * wstride + idx] - lr * g;

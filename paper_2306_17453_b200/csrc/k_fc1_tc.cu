@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "dev_util.cuh"
 #include "fl_internal.h"
 #include "tc_common.cuh"
 
@@ -127,7 +128,7 @@ __global__ void k_fc1_fwd_reduce(const float* __restrict__ part, const int32_t* 
   const int a = blockIdx.z, r = blockIdx.y, n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= HID || r >= bs[a]) return;
   float s = 0.f;
-  for (int ks = 0; ks < ksplit; ++ks) s += part[(((int64_t)a * ksplit + ks) * NB + r) * HID + n];
+  s = ordered_sum(part + (((int64_t)a * ksplit) * NB + r) * HID + n, ksplit, (int64_t)NB * HID);
   s += bias[(int64_t)a * bias_stride * wmul + n];
   h[((int64_t)a * B + r) * HID + n] = s > 0.f ? s : 0.f;
 }
@@ -206,6 +207,15 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     const int qd = warp & 3, k = mt * 128 + qd * 32 + lane;  // dp2 index (h, w, c)
+    // the pool2 state of this column does not depend on the MMA: fetch it while it runs
+    bool pos[NB];
+    uint8_t amr[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      const int64_t s = (int64_t)a * p.B + r;
+      pos[r] = r < bs ? p.p2[s * p.F + k] > 0.f : false;
+      amr[r] = r < bs ? p.am2[s * p.F + k] : 0;
+    }
     tc::mbar_wait(tfull, 0);
     tc::tc_fence_after();
     float v[NB];
@@ -213,10 +223,12 @@ __global__ void __launch_bounds__(192, 1)
     tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + 16, *reinterpret_cast<float(*)[16]>(v + 16));
     const int c = k % p.C2, pw = (k / p.C2) % p.W2, ph = k / (p.C2 * p.W2);
     const int W1 = 2 * p.W2, H1 = 2 * p.H2;
-    for (int r = 0; r < bs; ++r) {
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      if (r >= bs) break;
       const int64_t s = (int64_t)a * p.B + r;
-      const float g = p.p2[s * p.F + k] > 0.f ? v[r] : 0.f;  // ReLU'(pooled) = ReLU'(argmax)
-      const int am = p.am2[s * p.F + k];
+      const float g = pos[r] ? v[r] : 0.f;  // ReLU'(pooled) = ReLU'(argmax)
+      const int am = amr[r];
       float* d = p.dY2 + ((s * H1 + 2 * ph) * W1 + 2 * pw) * p.C2 + c;
       d[0] = am == 0 ? g : 0.f;
       d[p.C2] = am == 1 ? g : 0.f;
