@@ -74,6 +74,7 @@ struct ConvSmem {
 
 struct ConvTcArgs {
   const int32_t* bs;
+  int A;                  // active clients (tiles = A·B (client, sample) pairs)
   int B;
   int wmul;               // 0: every client reads θ_g (first wave), 1: client slot
   const float* bias;      // bias of client 0; client a at bias + a*bias_stride
@@ -91,20 +92,25 @@ __global__ void __launch_bounds__(192, 1)
     k_conv5_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, ConvTcArgs p) {
   constexpr int NB = BMN ? 32 : N;
   using S = ConvSmem<N, NB>;
-  constexpr uint32_t TMEM_COLS = (2 * N <= 32) ? 32 : (2 * N <= 64 ? 64 : (2 * N <= 128 ? 128 : 256));
+  // two accumulator buffers x two M-halves x N columns
+  constexpr uint32_t TMEM_COLS = (4 * N <= 32) ? 32 : (4 * N <= 64 ? 64 : (4 * N <= 128 ? 128 : 256));
   constexpr uint32_t IDESC = tc::idesc_tf32(128, N, 0, BMN);
   constexpr int NKB = 5 * CH;
 
-  const int r = blockIdx.x, a = blockIdx.y;
-  if (r >= p.bs[a]) return;
-  const int s = a * p.B + r;
+  // Persistent: CTA b handles tiles t = b, b + grid, ... of the A·B (client, sample) tiles
+  // (samples past a client's |b| are skipped identically by every role).  The smem stage
+  // ring runs across tiles and the TMEM accumulators are double-buffered, so the loads of
+  // tile i+1 and the epilogue of tile i-1 overlap the MMAs of tile i.
+  const int T = p.A * p.B;
+  auto valid = [&](int t) { return (t % p.B) < p.bs[t / p.B]; };
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
   uint64_t* empty = full + NSTAGE;
-  uint64_t* tfull = empty + NSTAGE;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* afull = empty + NSTAGE;   // [2] accumulator buffer ready for the epilogue
+  uint64_t* aempty = afull + 2;       // [2] accumulator buffer drained by the epilogue
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(aempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) {
@@ -115,7 +121,10 @@ __global__ void __launch_bounds__(192, 1)
         tc::mbar_init(full + i, 1);
         tc::mbar_init(empty + i, 1);
       }
-      tc::mbar_init(tfull, 1);
+      for (int i = 0; i < 2; ++i) {
+        tc::mbar_init(afull + i, 1);
+        tc::mbar_init(aempty + i, 128);
+      }
       tc::fence_mbar_init();
     }
     __syncwarp();
@@ -129,51 +138,72 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     // ---------------- TMA producer
     if (tc::elect_one()) {
-      for (int kb = 0; kb < NKB; ++kb) {
-        const int st = kb % NSTAGE, ph = (kb / NSTAGE) & 1;
-        const int kw = kb / CH, q = kb % CH;
-        tc::mbar_wait(empty + st, ph ^ 1);
-        uint8_t* sa = smem + st * S::STAGE;
-        uint8_t* sb = sa + A_BYTES;
-        tc::mbar_expect_tx(full + st, S::STAGE);
-        tc::tma_load_4d(sa, &mapX, full + st, 32 * q, kw - 2, -2, s);
-        for (int kh = 0; kh < 5; ++kh) {
-          const int tap = FLIP ? (4 - kh) * 5 + (4 - kw) : kh * 5 + kw;
-          tc::tma_load_4d(sb + kh * S::B_TAP, &mapW, full + st, 0, tap, BMN ? 32 * q : 0, a * p.wmul);
+      int it = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x) {
+        if (!valid(t)) continue;
+        const int a = t / p.B, s = t;  // slot index = a*B + r = t
+        for (int kb = 0; kb < NKB; ++kb, ++it) {
+          const int st = it % NSTAGE, ph = (it / NSTAGE) & 1;
+          const int kw = kb / CH, q = kb % CH;
+          tc::mbar_wait(empty + st, ph ^ 1);
+          uint8_t* sa = smem + st * S::STAGE;
+          uint8_t* sb = sa + A_BYTES;
+          tc::mbar_expect_tx(full + st, S::STAGE);
+          tc::tma_load_4d(sa, &mapX, full + st, 32 * q, kw - 2, -2, s);
+          for (int kh = 0; kh < 5; ++kh) {
+            const int tap = FLIP ? (4 - kh) * 5 + (4 - kw) : kh * 5 + kw;
+            tc::tma_load_4d(sb + kh * S::B_TAP, &mapW, full + st, 0, tap, BMN ? 32 * q : 0, a * p.wmul);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread)
     if (tc::elect_one()) {
-      for (int kb = 0; kb < NKB; ++kb) {
-        const int st = kb % NSTAGE, ph = (kb / NSTAGE) & 1;
-        tc::mbar_wait(full + st, ph);
+      int it = 0, tc_ = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x) {
+        if (!valid(t)) continue;
+        const int buf = tc_ & 1, aph = (tc_ >> 1) & 1;
+        tc::mbar_wait(aempty + buf, aph ^ 1);  // epilogue finished reading this buffer
         tc::tc_fence_after();
-        const uint32_t sa = tc::smem_u32(smem + st * S::STAGE);
-        const uint32_t sb = sa + A_BYTES;
+        const uint32_t acc0 = tbase + buf * 2 * N;
+        for (int kb = 0; kb < NKB; ++kb, ++it) {
+          const int st = it % NSTAGE, ph = (it / NSTAGE) & 1;
+          tc::mbar_wait(full + st, ph);
+          tc::tc_fence_after();
+          const uint32_t sa = tc::smem_u32(smem + st * S::STAGE);
+          const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-        for (int kh = 0; kh < 5; ++kh)
+          for (int kh = 0; kh < 5; ++kh)
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t bd = BMN ? tc::sdesc(sb + kh * S::B_TAP + k * 1024, NB * 128, 512, tc::kSW128_32B)
-                                    : tc::sdesc(sb + kh * S::B_TAP + k * 32, 0, 1024, tc::kSW128);
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t bd = BMN ? tc::sdesc(sb + kh * S::B_TAP + k * 1024, NB * 128, 512, tc::kSW128_32B)
+                                      : tc::sdesc(sb + kh * S::B_TAP + k * 32, 0, 1024, tc::kSW128);
 #pragma unroll
-            for (int mh = 0; mh < 2; ++mh) {
-              const uint64_t ad = tc::sdesc(sa + (mh * 8 + kh) * WW * 128 + k * 32, 0, 1024, tc::kSW128);
-              tc::mma_tf32(tbase + mh * N, ad, bd, IDESC, (kb | kh | k) != 0);
+              for (int mh = 0; mh < 2; ++mh) {
+                const uint64_t ad = tc::sdesc(sa + (mh * 8 + kh) * WW * 128 + k * 32, 0, 1024, tc::kSW128);
+                tc::mma_tf32(acc0 + mh * N, ad, bd, IDESC, (kb | kh | k) != 0);
+              }
             }
-          }
-        tc::mma_commit(empty + st);  // stage free once these MMAs have read it
+          tc::mma_commit(empty + st);  // stage free once these MMAs have read it
+        }
+        tc::mma_commit(afull + buf);   // accumulators of this tile complete
+        ++tc_;
       }
-      tc::mma_commit(tfull);         // accumulators complete
     }
   } else {
     // ---------------- epilogue: TMEM -> registers -> global
     const int qd = warp & 3;                 // TMEM lane quarter of this warp
-    tc::mbar_wait(tfull, 0);
-    tc::tc_fence_after();
     const int i = qd * 32 + lane;            // accumulator row = pixel within the M-half
+    int tc_ = 0;
+    for (int t = blockIdx.x; t < T; t += gridDim.x) {
+    if (!valid(t)) continue;
+    const int a = t / p.B, s = t;
+    const int buf = tc_ & 1, aph = (tc_ >> 1) & 1;
+    ++tc_;
+    tc::mbar_wait(afull + buf, aph);
+    tc::tc_fence_after();
+    const uint32_t tacc = tbase + buf * 2 * N;
     const float* bias = p.bias + (int64_t)a * p.bias_stride * p.wmul;
 #pragma unroll
     for (int mh = 0; mh < 2; ++mh) {
@@ -181,7 +211,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
       for (int n0 = 0; n0 < N; n0 += 16) {
         float v[16];
-        tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + mh * N + n0, v);
+        tc::tmem_ld16(tacc + ((uint32_t)(qd * 32) << 16) + mh * N + n0, v);
         if (POOL) {
           // window (2i..2i+1, 2j..2j+1) = lanes l, l^1, l^16, l^17 of this warp
           float pv[16];
@@ -231,16 +261,19 @@ __global__ void __launch_bounds__(192, 1)
             am[4 * j + 3] = aw >> 24;
           }
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
+          for (int u = 0; u < 4; ++u) {
             float4* dst = reinterpret_cast<float4*>(
-                p.out + ((((int64_t)s * 2 * HH + 2 * h + (t >> 1)) * 2 * WW + 2 * w + (t & 1)) * N + n0));
+                p.out + ((((int64_t)s * 2 * HH + 2 * h + (u >> 1)) * 2 * WW + 2 * w + (u & 1)) * N + n0));
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              dst[j] = make_float4(am[4 * j] == t ? g[4 * j] : 0.f, am[4 * j + 1] == t ? g[4 * j + 1] : 0.f,
-                                   am[4 * j + 2] == t ? g[4 * j + 2] : 0.f, am[4 * j + 3] == t ? g[4 * j + 3] : 0.f);
+              dst[j] = make_float4(am[4 * j] == u ? g[4 * j] : 0.f, am[4 * j + 1] == u ? g[4 * j + 1] : 0.f,
+                                   am[4 * j + 2] == u ? g[4 * j + 2] : 0.f, am[4 * j + 3] == u ? g[4 * j + 3] : 0.f);
           }
         }
       }
+    }
+    tc::tc_fence_before();
+    tc::mbar_arrive(aempty + buf);  // this thread's TMEM reads of the buffer are done
     }
   }
   tc::tc_fence_before();
@@ -258,7 +291,8 @@ cudaError_t launch_conv5(const CUtensorMap& mx, const CUtensorMap& mw, const Con
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  kfn<<<dim3(p.B, A), 192, smem, st>>>(mx, mw, p);
+  const int tiles = A * p.B;
+  kfn<<<dim3(tiles < 148 ? tiles : 148), 192, smem, st>>>(mx, mw, p);
   return cudaGetLastError();
 }
 
@@ -291,7 +325,7 @@ int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_
                  int64_t slots, float* p2, uint8_t* am2, cudaStream_t st) {
   CUtensorMap mx, mw;
   if (!make_plane_map(&mx, p1, 32, slots) || !make_w2_map(&mw, L, wbase, wclients, 64, 1)) return -1;
-  ConvTcArgs p{wa.bs, wa.B, wa.first ? 0 : 1, wbase + L.o_c2b, L.P_pad, p2, am2};
+  ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, wbase + L.o_c2b, L.P_pad, p2, am2};
   return launch_conv5<64, 1, 0, 0, 1>(mx, mw, p, wa.A, st) == cudaSuccess ? 1 : -1;
 }
 
@@ -300,7 +334,7 @@ int conv2_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t
                 int64_t slots, const float* p1, const uint8_t* am1, float* dY1, cudaStream_t st) {
   CUtensorMap mx, mw;
   if (!make_plane_map(&mx, dY2, 64, slots) || !make_w2_map(&mw, L, wbase, wclients, 32, 2)) return -1;
-  ConvTcArgs p{wa.bs, wa.B, wa.first ? 0 : 1, nullptr, 0, dY1, nullptr, p1, am1};
+  ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, nullptr, 0, dY1, nullptr, p1, am1};
   return launch_conv5<32, 2, 1, 1, 0>(mx, mw, p, wa.A, st) == cudaSuccess ? 1 : -1;
 }
 
