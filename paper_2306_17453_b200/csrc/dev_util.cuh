@@ -20,4 +20,10 @@ __device__ __forceinline__ float ordered_sum(const float* __restrict__ p, int n,
   return g;
 }
 
+// Programmatic dependent launch (kernels launched with launch_pdl): let the next kernel in
+// the stream start its prologue / block until the previous kernel's writes are visible.
+// Both are no-ops for a kernel launched without the PDL attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace flb

@@ -228,8 +228,16 @@ struct fl_ctx {
   KProf prof;
   std::string err;
   // concurrent client groups (CNN): streams forked from / joined into st
-  int ngroups = 4;
-  std::vector<cudaStream_t> gstream;
+  // Measured on C2 (scripts/group_sweep.py): 4 solo + 2 shared groups is best; more than 8
+  // streams in total alias onto the device's 8 hardware queues and serialise.
+  int ngroups = 2;  // round-robin groups (FL_GROUPS)
+  int nsolo = 4;    // longest clients given their own high-priority group (FL_SOLO)
+  // PDL only for waves of at most this many clients (FL_PDL_MAXA; default all). With the
+  // trigger at the end of each CTA it helps every wave (C2 19.98 -> 19.18 ms, one 2000-sample
+  // client 9.3 -> 7.6 ms); an early trigger parked dependent CTAs on smem and starved the
+  // concurrent streams (C2 22 ms).
+  int pdl_max_a = 1 << 30;
+  std::vector<cudaStream_t> gstream;  // [nsolo high-priority | ngroups normal]
   std::vector<cudaEvent_t> ev_join;
   cudaEvent_t ev_fork = nullptr;
   int64_t part_group_z = 0;
@@ -388,11 +396,17 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
                         &c->ev_acc1, &c->ev_ar0, &c->ev_ar1, &c->ev_end, &c->ev_tab};
   for (cudaEvent_t* e : evs) CK(cudaEventCreate(e));
   if (const char* ng = getenv("FL_GROUPS")) c->ngroups = std::max(1, atoi(ng));
+  if (const char* ns = getenv("FL_SOLO")) c->nsolo = std::max(0, atoi(ns));
+  if (const char* pm = getenv("FL_PDL_MAXA")) c->pdl_max_a = atoi(pm);
+  c->nsolo = std::min(c->nsolo, std::max(0, 8 - c->ngroups));
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
-  c->gstream.assign((size_t)c->ngroups, nullptr);
-  c->ev_join.assign((size_t)c->ngroups, nullptr);
-  for (int g = 0; g < c->ngroups; ++g) {
-    CK(cudaStreamCreateWithFlags(&c->gstream[(size_t)g], cudaStreamNonBlocking));
+  const int nstreams = c->nsolo + c->ngroups;
+  c->gstream.assign((size_t)nstreams, nullptr);
+  c->ev_join.assign((size_t)nstreams, nullptr);
+  int prio_lo = 0, prio_hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  for (int g = 0; g < nstreams; ++g) {
+    CK(cudaStreamCreateWithPriority(&c->gstream[(size_t)g], cudaStreamNonBlocking, g < c->nsolo ? prio_hi : prio_lo));
     CK(cudaEventCreateWithFlags(&c->ev_join[(size_t)g], cudaEventDisableTiming));
   }
   if (!c->pop_dev) {
@@ -467,15 +481,21 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   std::iota(c->exec.begin(), c->exec.end(), 0);
   auto nb = [&](int64_t i) { return (c->n_samples[(size_t)c->local_ids[(size_t)i]] + B - 1) / B; };
   std::stable_sort(c->exec.begin(), c->exec.end(), [&](int64_t a, int64_t b) { return nb(a) > nb(b); });
-  // Deal the longest-first order round-robin into groups (concurrent streams); each group is
-  // contiguous in execution order and itself longest-first, so its active set is a prefix.
+  // Groups = concurrent streams. The NS longest clients (the round's critical path) each get
+  // a group of their own on a high-priority stream; the rest of the longest-first order is
+  // dealt round-robin into NR groups. Each group is contiguous in execution order and itself
+  // longest-first, so its active set in every wave is a prefix.
   const bool cnn_model = (L.model == FL_MODEL_CNN_CIFAR || L.model == FL_MODEL_CNN_SPEECH);
-  const int NG = cnn_model ? (int)std::max<int64_t>(1, std::min<int64_t>(c->ngroups, K)) : 1;
-  if (NG > 1) {
+  const int NS = cnn_model ? (int)std::min<int64_t>(c->nsolo, std::max<int64_t>(0, K - 1)) : 0;
+  const int NR = cnn_model ? (int)std::max<int64_t>(1, std::min<int64_t>(c->ngroups, K - NS)) : 1;
+  const int NG = NS + NR;
+  std::vector<int64_t> gsize((size_t)NG, 0);
+  {
     std::vector<int64_t> ex2;
     ex2.reserve((size_t)K);
-    for (int g = 0; g < NG; ++g)
-      for (int64_t e = g; e < K; e += NG) ex2.push_back(c->exec[(size_t)e]);
+    for (int g = 0; g < NS; ++g) ex2.push_back(c->exec[(size_t)g]), gsize[(size_t)g] = 1;
+    for (int r = 0; r < NR; ++r)
+      for (int64_t e = NS + r; e < K; e += NR) ex2.push_back(c->exec[(size_t)e]), ++gsize[(size_t)(NS + r)];
     c->exec.swap(ex2);
   }
   c->steps_exec.resize((size_t)K);
@@ -499,9 +519,11 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   ws.A.clear();
   ws.slot_off.assign(1, 0);
   ws.bs_off.assign(1, 0);
+  ws.gstream.assign((size_t)NG, 0);
   for (int g = 0; g < NG; ++g) {
-    const int64_t n_g = K > g ? (K - g + NG - 1) / NG : 0;
+    const int64_t n_g = gsize[(size_t)g];
     ws.gn[(size_t)g] = n_g;
+    ws.gstream[(size_t)g] = g < NS ? g : c->nsolo + (g - NS);
     ws.gbase[(size_t)g + 1] = ws.gbase[(size_t)g] + n_g;
     const int64_t b0 = ws.gbase[(size_t)g];
     const int64_t nw = n_g ? c->steps_exec[(size_t)b0] : 0;
@@ -622,7 +644,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
     }
     // split-K partials: one region per group, each holding the larger of the SIMT path's
     // K_g·nch chunks and the tensor-core path's K_g + 2·148 chunks
-    const int64_t kg = (K + NG - 1) / NG;
+    const int64_t kg = *std::max_element(gsize.begin(), gsize.end());
     const int64_t pg = std::max<int64_t>(kg * b.nch, conv2_dw_tc_part_z(kg));
     if (pg * NG > c->cb_part_cap) {
       void* old[] = {b.part1, b.part2, b.fc1_part};
@@ -682,29 +704,44 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   int64_t tl = 0;
   if (K > 0) {
     if (cnn) {
-      // groups run concurrently on their own streams, forked from and joined into st
+      // groups run concurrently on their own streams, forked from and joined into st. Waves
+      // are issued wave-major across groups so every stream has work queued from the start.
+      // A profiled round runs the groups serialised on st, so each kernel's event interval is
+      // its own duration (bench.py's roofline), not time shared with other streams.
       CK(cudaEventRecord(c->ev_fork, st));
+      std::vector<CnnBufs> gv((size_t)ws.ngroups);
+      std::vector<cudaStream_t> gst((size_t)ws.ngroups, st);
+      int64_t max_w = 0;
       for (int g = 0; g < ws.ngroups; ++g) {
         if (ws.gn[(size_t)g] == 0) continue;
-        cudaStream_t gs = c->gstream[(size_t)g];
-        CK(cudaStreamWaitEvent(gs, c->ev_fork, 0));
-        const int64_t base = ws.gbase[(size_t)g];
-        CnnBufs gv = cnn_group_view(c->cb, L.d, (int)B, base, ws.gn[(size_t)g], g, c->part_group_z,
-                                    conv2_dw_tc_z_floats(), (int64_t)L.d.C1 * (25 * L.d.cpad + 1));
-        for (int64_t t = 0; t < ws.gnw[(size_t)g]; ++t) {
-          const int64_t k = ws.gw0[(size_t)g] + t;
+        if (!c->prof.on) {
+          gst[(size_t)g] = c->gstream[(size_t)ws.gstream[(size_t)g]];
+          CK(cudaStreamWaitEvent(gst[(size_t)g], c->ev_fork, 0));
+        }
+        gv[(size_t)g] = cnn_group_view(c->cb, L.d, (int)B, ws.gbase[(size_t)g], ws.gn[(size_t)g], g, c->part_group_z,
+                                       conv2_dw_tc_z_floats(), (int64_t)L.d.C1 * (25 * L.d.cpad + 1));
+        max_w = std::max(max_w, ws.gnw[(size_t)g]);
+      }
+      for (int64_t t = 0; t < max_w; ++t) {
+        for (int g = 0; g < ws.ngroups; ++g) {
+          if (ws.gn[(size_t)g] == 0 || t >= ws.gnw[(size_t)g]) continue;
+          const int64_t k = ws.gw0[(size_t)g] + t, base = ws.gbase[(size_t)g];
           int64_t sum_bs = 0;
           for (int32_t a = 0; a < ws.A[(size_t)k]; ++a) sum_bs += h_bs[ws.bs_off[(size_t)k] + a];
           WaveArgs wa{ws.A[(size_t)k], (int)B, t == 0, ws.d_sidx + ws.slot_off[(size_t)k],
                       ws.d_bs + ws.bs_off[(size_t)k], c->cfg.lr, sum_bs, &c->prof, c->cfg.math == 0,
-                      ws.gn[(size_t)g]};
-          int nl = cnn_wave_simt(L, wa, c->d_xpack, c->d_ypack, c->d_theta, c->d_slots + base * L.P_pad, gv, gs);
+                      ws.gn[(size_t)g], ws.A[(size_t)k] <= c->pdl_max_a};
+          int nl = cnn_wave_simt(L, wa, c->d_xpack, c->d_ypack, c->d_theta, c->d_slots + base * L.P_pad,
+                                 gv[(size_t)g], gst[(size_t)g]);
           if (nl < 0)
             return set_err(c, FL_ERR_CUDA, "tensor-core kernel launch / tensor map failed (group %d wave %lld)", g,
                            (long long)t);
           tl += nl;
         }
-        CK(cudaEventRecord(c->ev_join[(size_t)g], gs));
+      }
+      for (int g = 0; g < ws.ngroups; ++g) {
+        if (ws.gn[(size_t)g] == 0 || gst[(size_t)g] == st) continue;
+        CK(cudaEventRecord(c->ev_join[(size_t)g], gst[(size_t)g]));
         CK(cudaStreamWaitEvent(st, c->ev_join[(size_t)g], 0));
       }
     } else {

@@ -4,10 +4,39 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace flb {
+
+// Programmatic dependent launch: the kernel may begin while its stream predecessor drains;
+// it must call pdl_trigger() / pdl_wait() (dev_util.cuh) before touching any data the
+// predecessor produces. FL_PDL=0 turns it off (plain stream order).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FL_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(bool on, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = (on && pdl_enabled()) ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------- model geometry
 // CNN family (McMahan CNN on CIFAR / speech, reading A10): conv5x5 'same' + ReLU +
@@ -54,6 +83,7 @@ struct WaveSched {
   int32_t* d_bs = nullptr;         // device: |b| of each active client
   int ngroups = 1;
   std::vector<int64_t> gbase, gn, gw0, gnw;
+  std::vector<int> gstream;        // stream index of each group
 };
 
 // ---------------------------------------------------------------- CNN buffers
@@ -134,6 +164,7 @@ struct WaveArgs {
   KProf* prof;
   bool use_tc;       // tensor-core (tcgen05) kernels where built for this geometry
   int64_t wclients;  // client slots allocated (weights tensor-map extent)
+  bool pdl;          // launch this wave's kernels with programmatic dependent launch
 };
 
 // Kernel launchers (k_*.cu). All asynchronous on `st`. Return the number of launches.

@@ -282,6 +282,7 @@ __global__ void k_unpool(const float* __restrict__ dp, const float* __restrict__
 // Σ of the split-K partials, then fused SGD on the conv weights and bias.
 __global__ void k_dw_reduce_sgd(const float* __restrict__ part, int nch, int rpc, const int32_t* __restrict__ bs,
                                 int O, int N, WSrc w, int64_t o_w, int64_t o_b, float* dst, int64_t P_pad, float lr) {
+  pdl_wait();  // (PDL) previous kernel's writes visible; the implicit trigger is at exit
   const int a = blockIdx.y;
   const int nvalid = (bs[a] + rpc - 1) / rpc;
   const int tot = O * N;
@@ -302,6 +303,7 @@ __global__ void __launch_bounds__(256) k_head_fwd(const float* __restrict__ h, c
                                                   const int32_t* __restrict__ sidx, const int32_t* __restrict__ bs,
                                                   int B, int HID, int NCLS, WSrc w, int64_t o_w, int64_t o_b,
                                                   float* __restrict__ dzbuf, float* __restrict__ dh) {
+  pdl_wait();  // (PDL) previous kernel's writes visible; the implicit trigger is at exit
   extern __shared__ float sm[];
   const int z = blockIdx.x, r0 = blockIdx.y * HR, b = bs[z];
   if (r0 >= B) return;
@@ -361,6 +363,7 @@ __global__ void __launch_bounds__(256) k_head_fwd(const float* __restrict__ h, c
 __global__ void __launch_bounds__(256) k_head_sgd(const float* __restrict__ h, const float* __restrict__ dzbuf,
                                                   const int32_t* __restrict__ bs, int B, int HID, int NCLS, WSrc w,
                                                   int64_t o_w, int64_t o_b, float* dst, int64_t P_pad, float lr) {
+  pdl_wait();  // (PDL) previous kernel's writes visible; the implicit trigger is at exit
   extern __shared__ float sm[];
   const int z = blockIdx.x, n0 = blockIdx.y * 64, b = bs[z];
   if (b == 0) return;
@@ -525,9 +528,9 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     hsm_set = hsm;
   }
   pf.begin(st);
-  k_head_fwd<<<dim3(A, (B + HR - 1) / HR), 256, hsm, st>>>(b.h, ypack, wa.sidx, wa.bs, B, d.HID, d.NCLS, w, L.o_f2w,
+  launch_pdl(wa.pdl, k_head_fwd, dim3(A, (B + HR - 1) / HR), 256, hsm, st, b.h, ypack, wa.sidx, wa.bs, B, d.HID, d.NCLS, w, L.o_f2w,
                                                           L.o_f2b, b.dz, b.dh), ++n;
-  k_head_sgd<<<dim3(A, (d.HID + 63) / 64), 256, sizeof(float) * B * (d.NCLS + 64), st>>>(b.h, b.dz, wa.bs, B, d.HID, d.NCLS, w, L.o_f2w, L.o_f2b,
+  launch_pdl(wa.pdl, k_head_sgd, dim3(A, (d.HID + 63) / 64), 256, sizeof(float) * B * (d.NCLS + 64), st, b.h, b.dz, wa.bs, B, d.HID, d.NCLS, w, L.o_f2w, L.o_f2b,
                                                           slots, L.P_pad, wa.lr), ++n;
   pf.end(K_HEAD, 3.0 * f_f2, 8.0 * A * d.NCLS * d.HID + 8.0 * S * d.HID, st);
   // ---- backward (each layer's dX reads W before its dW epilogue overwrites it)
@@ -557,7 +560,7 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   if (tc) {  // pool1/ReLU backward fused into the epilogue: writes dY1 directly
     if (conv2_dx_tc(L, wa, w.base, wcl, b.dY2, b.slots, b.p1, b.am1, b.dY1, st) < 0) return -1;
     ++n;
-    pf.end(K_CONV2_DX, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2) + S * hw0 * d.C1 * 4.0 + S * hw1 * d.C1 * 5.0, st);
+    pf.end(K_CONV2_DX, f_c2, 4.0 * S * hw1 * d.C2 + S * hw0 * d.C1 * 4.0 + S * hw1 * d.C1 * 5.0, st);  // dY2, p1+am1 in; dY1 out
   } else {
     launch(ConvDx{b.dY2, wa.bs, B, d.H1, d.W1, d.C1, d.C2, w, L.o_c2w, b.dp1}, B * d.H1 * d.W1, d.C1, A, st), ++n;
     pf.end(K_CONV2_DX, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
@@ -582,7 +585,7 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
            25 * d.C1 + 1, A * b.nch, st), ++n;
     pf.end(K_CONV2_DW, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
     pf.begin(st);
-    k_dw_reduce_sgd<<<dim3(16, A), 256, 0, st>>>(b.part2, b.nch, rpc, wa.bs, d.C2, 25 * d.C1 + 1, w, L.o_c2w,
+    launch_pdl(wa.pdl, k_dw_reduce_sgd, dim3(16, A), 256, 0, st, b.part2, b.nch, rpc, wa.bs, d.C2, 25 * d.C1 + 1, w, L.o_c2w,
                                                  L.o_c2b, slots, L.P_pad, wa.lr), ++n;
     pf.end(K_CONV2_DWR, 0, 8.0 * A * d.C2 * 25 * d.C1, st);
   }
@@ -597,7 +600,7 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   }
   pf.end(K_CONV1_DW, f_c1, 4.0 * S * hw0 * (d.cin + d.C1), st);
   pf.begin(st);
-  k_dw_reduce_sgd<<<dim3((d.C1 * (25 * d.cpad + 1) + 127) / 128, A), 128, 0, st>>>(
+  launch_pdl(wa.pdl, k_dw_reduce_sgd, dim3((d.C1 * (25 * d.cpad + 1) + 127) / 128, A), 128, 0, st, 
       b.part1, nch1, rpc1, wa.bs, d.C1, 25 * d.cpad + 1, w, L.o_c1w,
                                               L.o_c1b, slots, L.P_pad, wa.lr), ++n;
   pf.end(K_CONV1_DWR, 0, 8.0 * A * d.C1 * 25 * d.cin, st);

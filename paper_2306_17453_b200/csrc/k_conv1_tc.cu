@@ -5,9 +5,10 @@
 // the no-swizzle (interleaved) operand layouts, again fed by TMA shifted copies of the
 // input plane (zero padding from TMA's out-of-bounds fill):
 //
-// Forward (M = pixels, N = 32 channels, K = (tap, c)):  one CTA = one sample (1024 px =
-//   8 M-tiles of 4 image rows, 8 accumulators x 32 columns).  copy_kw[h'][w][c] =
-//   x[h'-2][w+kw-2][c], h' in [0,36).  A of tap (kh, kw) for tile j = copy_kw shifted by
+// Forward (M = pixels, N = 32 channels, K = (tap, c)):  one CTA = one half-plane of a
+//   sample (512 px = 4 M-tiles of 4 image rows, 4 accumulators x 32 columns).
+//   copy_kw[h'][w][c] = x[16*half+h'-2][w+kw-2][c], h' in [0,21).  A of tap (kh, kw) for
+//   tile j = copy_kw shifted by
 //   (4j+kh) image rows; one MMA (K = 8) pairs taps (kh, kw) and (kh+1, kw) (LBO = one
 //   image row); kh = 5 is a zero-weight pad tap.  B = weights per tap as [o][4] (TMA box
 //   of the [o][tap][c] tensor, out-of-range taps read as zeros).  Epilogue: + bias -> a1.
@@ -27,8 +28,11 @@ namespace {
 constexpr int H = 32, W = 32, C1 = 32, ROWB = W * 16;  // 512 B per image row of 4-channel pixels
 
 // ------------------------------------------------------------------ forward
-constexpr int F_COPY = (H + 4) * ROWB;          // 18432 B, 36 rows
-constexpr int F_A = 5 * F_COPY;                 // 92160
+// One CTA = one half-plane (16 image rows = 4 M-tiles) of a sample, so two CTAs fit per SM
+// and one's loads / epilogue overlap the other's MMAs.
+constexpr int F_ROWS = 16 + 5;                  // output rows + halo + the kh = 5 pad tap
+constexpr int F_COPY = F_ROWS * ROWB;           // 10752 B
+constexpr int F_A = 5 * F_COPY;                 // 53760
 constexpr int F_B = 30 * 512;                   // (kw, kh = 0..5) x [32 o][4 c]
 constexpr int F_XCH = F_A + F_B;                // epilogue exchange buffer [4][32][16] fp32
 constexpr int F_BAR = F_XCH + 4 * 32 * 16 * 4;
@@ -47,9 +51,12 @@ struct C1Args {
 __global__ void __launch_bounds__(192, 2)
     k_conv1_fwd_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, C1Args p) {
   constexpr uint32_t IDESC = tc::idesc_tf32(128, C1, 0, 0);
-  const int r = blockIdx.x, a = blockIdx.y;
+  const int r = blockIdx.x >> 1, half = blockIdx.x & 1, a = blockIdx.y;
   if (r >= p.bs[a]) return;
   const int s = a * p.B + r;
+  // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
+  // would stall other streams' kernels) or touching anything it writes.
+  pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + F_BAR);
@@ -63,7 +70,7 @@ __global__ void __launch_bounds__(192, 2)
       tc::fence_mbar_init();
     }
     __syncwarp();
-    tc::tmem_alloc<256>(tslot);
+    tc::tmem_alloc<128>(tslot);
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -73,7 +80,8 @@ __global__ void __launch_bounds__(192, 2)
     if (tc::elect_one()) {
       const int row = p.sidx[s];
       tc::mbar_expect_tx(full, F_A + F_B);
-      for (int kw = 0; kw < 5; ++kw) tc::tma_load_4d(smem + kw * F_COPY, &mapX, full, 0, kw - 2, -2, row);
+      for (int kw = 0; kw < 5; ++kw)
+        tc::tma_load_4d(smem + kw * F_COPY, &mapX, full, 0, kw - 2, 16 * half - 2, row);
       for (int kw = 0; kw < 5; ++kw)
         for (int kh = 0; kh < 6; ++kh)  // tap 25..29 (kh = 5) is out of range -> zeros
           tc::tma_load_4d(smem + F_A + (kw * 6 + kh) * 512, &mapW, full, 0, kh * 5 + kw, 0, a * p.wmul);
@@ -83,7 +91,7 @@ __global__ void __launch_bounds__(192, 2)
       tc::mbar_wait(full, 0);
       tc::tc_fence_after();
       const uint32_t sa = tc::smem_u32(smem), sb = sa + F_A;
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < 4; ++j)
         for (int kw = 0; kw < 5; ++kw)
           for (int kp = 0; kp < 3; ++kp) {  // taps (2kp, kw) and (2kp+1, kw)
             const uint64_t ad = tc::sdesc(sa + kw * F_COPY + (4 * j + 2 * kp) * ROWB, ROWB, 128, tc::kSWNONE);
@@ -97,12 +105,12 @@ __global__ void __launch_bounds__(192, 2)
     tc::mbar_wait(tfull, 0);
     tc::tc_fence_after();
     // bias + ReLU + 2x2 max-pool (first maximum in row-major window order, reading A13).
-    // Tile j holds image rows 4j..4j+3, one row per warp; the vertical window partner is
+    // Tile j holds image rows 16*half + 4j..+3, one row per warp; the vertical window partner is
     // in the next warp, so each 16-channel chunk is exchanged through shared memory.
     const float* bias = p.bias + (int64_t)a * p.bias_stride * p.wmul;
     float* xb = reinterpret_cast<float*>(smem + F_XCH);  // [4 rows][32 w][16 c]
     const int t = threadIdx.x - 64;                    // 0..127 over the epilogue warps
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < 4; ++j) {
 #pragma unroll 1
       for (int n0 = 0; n0 < C1; n0 += 16) {
         float v[16];
@@ -129,7 +137,7 @@ __global__ void __launch_bounds__(192, 2)
           reinterpret_cast<float*>(&r)[cc] = bv > 0.f ? bv : 0.f;
           am |= bi << (8 * cc);
         }
-        const int64_t o = (((int64_t)s * 16 + 2 * j + pr) * 16 + pc) * C1 + n0 + 4 * c4;
+        const int64_t o = (((int64_t)s * 16 + 8 * half + 2 * j + pr) * 16 + pc) * C1 + n0 + 4 * c4;
         *reinterpret_cast<float4*>(p.p1 + o) = r;
         *reinterpret_cast<uint32_t*>(p.am1 + o) = am;
         asm volatile("bar.sync 1, 128;" ::: "memory");  // buffer reused by the next chunk
@@ -138,7 +146,8 @@ __global__ void __launch_bounds__(192, 2)
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<256>(tbase);
+  pdl_trigger();  // late trigger: a dependent kernel's CTAs park on SM resources until it runs
+  if (warp == 0) tc::tmem_dealloc<128>(tbase);
 }
 
 // ------------------------------------------------------------------ weight gradient
@@ -171,6 +180,9 @@ __global__ void __launch_bounds__(192, 1)
   const int r0 = ch * p.rpc, r1 = min(p.bs[a], r0 + p.rpc);
   if (r0 >= r1) return;
   const int nkb = (r1 - r0) * H;
+  // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
+  // would stall other streams' kernels) or touching anything it writes.
+  pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + D_BAR);
@@ -259,6 +271,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc::tc_fence_before();
   __syncthreads();
+  pdl_trigger();  // late trigger: a dependent kernel's CTAs park on SM resources until it runs
   if (warp == 0) tc::tmem_dealloc<32>(tbase);
 }
 
@@ -270,7 +283,7 @@ int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_
   CUtensorMap mx, mw;
   uint64_t dx[4] = {4, W, H, (uint64_t)xrows};
   uint64_t sx[3] = {16, 16 * W, 16 * W * H};
-  uint32_t bx[4] = {4, W, H + 4, 1};
+  uint32_t bx[4] = {4, W, F_ROWS, 1};
   uint64_t dw[4] = {4, 25, 32, (uint64_t)wclients};  // c1w[o][tap][4] of every client slot
   uint64_t sw[3] = {16, 400, (uint64_t)L.P_pad * 4};
   uint32_t bw[4] = {4, 1, 32, 1};
@@ -281,7 +294,7 @@ int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_
     attr = true;
   }
   C1Args p{wa.sidx, wa.bs, wa.B, wa.first ? 0 : 1, wbase + L.o_c1b, L.P_pad, p1, am1};
-  k_conv1_fwd_tc<<<dim3(wa.B, wa.A), 192, F_SMEM, st>>>(mx, mw, p);
+  launch_pdl(wa.pdl, k_conv1_fwd_tc, dim3(2 * wa.B, wa.A), 192, F_SMEM, st, mx, mw, p);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -308,7 +321,7 @@ int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64
     attr = true;
   }
   C1DwArgs p{wa.sidx, wa.bs, wa.B, nch, rpc, part};
-  k_conv1_dw_tc<<<dim3(nch, wa.A), 192, D_SMEM, st>>>(mx, md, p);
+  launch_pdl(wa.pdl, k_conv1_dw_tc, dim3(nch, wa.A), 192, D_SMEM, st, mx, md, p);
   *nch_out = nch;
   *rpc_out = rpc;
   return cudaGetLastError() == cudaSuccess ? 1 : -1;

@@ -104,6 +104,9 @@ __global__ void __launch_bounds__(192, 1)
   const int T = p.A * p.B;
   auto valid = [&](int t) { return (t % p.B) < p.bs[t / p.B]; };
 
+  // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
+  // would stall other streams' kernels) or touching anything it writes.
+  pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
@@ -278,11 +281,12 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc::tc_fence_before();
   __syncthreads();
+  pdl_trigger();  // late trigger: a dependent kernel's CTAs park on SM resources until it runs
   if (warp == 0) tc::tmem_dealloc<TMEM_COLS>(tbase);
 }
 
 template <int N, int CH, int BMN, int FLIP, int POOL>
-cudaError_t launch_conv5(const CUtensorMap& mx, const CUtensorMap& mw, const ConvTcArgs& p, int A, cudaStream_t st) {
+cudaError_t launch_conv5(const CUtensorMap& mx, const CUtensorMap& mw, const ConvTcArgs& p, int A, bool pdl, cudaStream_t st) {
   constexpr int NB = BMN ? 32 : N;
   const int smem = ConvSmem<N, NB>::TOTAL;
   auto kfn = k_conv5_tc<N, CH, BMN, FLIP, POOL>;
@@ -292,7 +296,7 @@ cudaError_t launch_conv5(const CUtensorMap& mx, const CUtensorMap& mw, const Con
     attr = true;
   }
   const int tiles = A * p.B;
-  kfn<<<dim3(tiles < 148 ? tiles : 148), 192, smem, st>>>(mx, mw, p);
+  launch_pdl(pdl, kfn, dim3(tiles < 148 ? tiles : 148), 192, smem, st, mx, mw, p);
   return cudaGetLastError();
 }
 
@@ -326,7 +330,7 @@ int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_
   CUtensorMap mx, mw;
   if (!make_plane_map(&mx, p1, 32, slots) || !make_w2_map(&mw, L, wbase, wclients, 64, 1)) return -1;
   ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, wbase + L.o_c2b, L.P_pad, p2, am2};
-  return launch_conv5<64, 1, 0, 0, 1>(mx, mw, p, wa.A, st) == cudaSuccess ? 1 : -1;
+  return launch_conv5<64, 1, 0, 0, 1>(mx, mw, p, wa.A, wa.pdl, st) == cudaSuccess ? 1 : -1;
 }
 
 // conv2 dX (transposed conv) on tensor cores: dY2 -> dp1.
@@ -335,7 +339,7 @@ int conv2_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t
   CUtensorMap mx, mw;
   if (!make_plane_map(&mx, dY2, 64, slots) || !make_w2_map(&mw, L, wbase, wclients, 32, 2)) return -1;
   ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, nullptr, 0, dY1, nullptr, p1, am1};
-  return launch_conv5<32, 2, 1, 1, 0>(mx, mw, p, wa.A, st) == cudaSuccess ? 1 : -1;
+  return launch_conv5<32, 2, 1, 1, 0>(mx, mw, p, wa.A, wa.pdl, st) == cudaSuccess ? 1 : -1;
 }
 
 }  // namespace flb

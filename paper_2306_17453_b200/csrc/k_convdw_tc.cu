@@ -55,6 +55,9 @@ __global__ void __launch_bounds__(192, 1)
   if (r0 >= r1) return;
   const int nkb = (r1 - r0) * 8;
 
+  // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
+  // would stall other streams' kernels) or touching anything it writes.
+  pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
@@ -153,6 +156,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc::tc_fence_before();
   __syncthreads();
+  pdl_trigger();  // late trigger: a dependent kernel's CTAs park on SM resources until it runs
   if (warp == 0) tc::tmem_dealloc<512>(tbase);
 }
 
@@ -160,6 +164,7 @@ __global__ void __launch_bounds__(192, 1)
 __global__ void k_dw2_reduce_sgd(const float* __restrict__ part, int nch, int rpc, const int32_t* __restrict__ bs,
                                  const float* wsrc, int64_t wstride, float* dst, int64_t P_pad, int64_t o_w,
                                  int64_t o_b, float lr) {
+  pdl_wait();  // (PDL) previous kernel's writes visible; the implicit trigger is at exit
   const int a = blockIdx.y;
   const int nvalid = (bs[a] + rpc - 1) / rpc;
   const float* pa = part + (int64_t)a * nch * NROW * NO;
@@ -200,7 +205,7 @@ int conv2_dw_tc(const Layout& L, const WaveArgs& wa, const float* p1, const floa
     attr = true;
   }
   DwArgs p{wa.bs, wa.B, nch, rpc, part};
-  k_conv2_dw_tc<<<dim3(nch, wa.A), 192, SMEM, st>>>(mx, md, p);
+  launch_pdl(wa.pdl, k_conv2_dw_tc, dim3(nch, wa.A), 192, SMEM, st, mx, md, p);
   *nch_out = nch;
   *rpc_out = rpc;
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
@@ -208,7 +213,7 @@ int conv2_dw_tc(const Layout& L, const WaveArgs& wa, const float* p1, const floa
 
 int conv2_dw_reduce_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wsrc_stride, float* dst,
                        const float* part, int nch, int rpc, cudaStream_t st) {
-  k_dw2_reduce_sgd<<<dim3((NROW * NO + 255) / 256, wa.A), 256, 0, st>>>(part, nch, rpc, wa.bs, wsrc, wsrc_stride,
+  launch_pdl(wa.pdl, k_dw2_reduce_sgd, dim3((NROW * NO + 255) / 256, wa.A), 256, 0, st, part, nch, rpc, wa.bs, wsrc, wsrc_stride,
                                                                        dst, L.P_pad, L.o_c2w, L.o_c2b, wa.lr);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }

@@ -48,6 +48,9 @@ __global__ void __launch_bounds__(192, 1)
   const int bs = p.bs[a];
   if (bs == 0) return;
   const int kb0 = ks * p.kpb, kb1 = min(p.F / 32, kb0 + p.kpb), nkb = kb1 - kb0;
+  // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
+  // would stall other streams' kernels) or touching anything it writes.
+  pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + FW_BAR);
@@ -119,12 +122,14 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc::tc_fence_before();
   __syncthreads();
+  pdl_trigger();  // late trigger: a dependent kernel's CTAs park on SM resources until it runs
   if (warp == 0) tc::tmem_dealloc<32>(tbase);
 }
 
 // h = ReLU(Σ_splits part + b1), fixed split order.
 __global__ void k_fc1_fwd_reduce(const float* __restrict__ part, const int32_t* __restrict__ bs, int B, int HID,
                                  int ksplit, const float* bias, int64_t bias_stride, int wmul, float* h) {
+  pdl_wait();  // (PDL) previous kernel's writes visible; the implicit trigger is at exit
   const int a = blockIdx.z, r = blockIdx.y, n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= HID || r >= bs[a]) return;
   float s = 0.f;
@@ -153,6 +158,9 @@ __global__ void __launch_bounds__(192, 1)
   const int bs = p.bs[a];
   if (bs == 0) return;
   const int nkb = p.HID / 32;
+  // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
+  // would stall other streams' kernels) or touching anything it writes.
+  pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + DX_BAR);
@@ -238,6 +246,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc::tc_fence_before();
   __syncthreads();
+  pdl_trigger();  // late trigger: a dependent kernel's CTAs park on SM resources until it runs
   if (warp == 0) tc::tmem_dealloc<32>(tbase);
 }
 
@@ -246,7 +255,7 @@ __global__ void __launch_bounds__(192, 1)
 // memory by TMA alongside the operands, updated there by the epilogue warps
 // (W <- W − η·D, 16-byte accesses in the SW128 pattern, conflict-free), and written back
 // by TMA: the HBM stream is one bulk read and one bulk write of W1 per client step.
-constexpr int DW_N = 256;
+constexpr int DW_N = 128;  // 128 x 128 W1 tile: ~97 KB smem, two CTAs per SM overlap load / MMA / store
 constexpr int DW_A = 4 * NB * 128, DW_B = (DW_N / 32) * NB * 128;  // 16 KB + 32 KB
 constexpr int DW_W = (DW_N / 32) * 128 * 128;                        // 8 chunks of [128 n][32 k] = 128 KB
 constexpr int DW_BAR = DW_W + DW_A + DW_B, DW_SMEM = DW_BAR + 64 + 1024;
@@ -269,6 +278,9 @@ __global__ void __launch_bounds__(192, 1)
   const int a = blockIdx.y, mt = blockIdx.x / p.ntiles, nt = blockIdx.x % p.ntiles;
   const int bs = p.bs[a];
   if (bs == 0) return;
+  // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
+  // would stall other streams' kernels) or touching anything it writes.
+  pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sw = smem;                  // W tile
@@ -345,6 +357,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc::tc_fence_before();
   __syncthreads();
+  pdl_trigger();  // late trigger: a dependent kernel's CTAs park on SM resources until it runs
   if (warp == 0) tc::tmem_dealloc<DW_N>(tbase);
 }
 
@@ -387,10 +400,10 @@ int fc1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t 
   set_smem(k_fc1_fwd_tc, FW_SMEM, attr);
   const int wmul = wa.first ? 0 : 1;
   FwArgs p{wa.bs, wa.B, d.F, d.HID, wmul, ksplit, kpb, wbase + L.o_f1b, L.P_pad, h, part};
-  k_fc1_fwd_tc<<<dim3(mtiles * ksplit, wa.A), 192, FW_SMEM, st>>>(mw, mx, p);
+  launch_pdl(wa.pdl, k_fc1_fwd_tc, dim3(mtiles * ksplit, wa.A), 192, FW_SMEM, st, mw, mx, p);
   *launches = 1;
   if (ksplit > 1) {
-    k_fc1_fwd_reduce<<<dim3((d.HID + 127) / 128, wa.B, wa.A), 128, 0, st>>>(part, wa.bs, wa.B, d.HID, ksplit,
+    launch_pdl(wa.pdl, k_fc1_fwd_reduce, dim3((d.HID + 127) / 128, wa.B, wa.A), 128, 0, st, part, wa.bs, wa.B, d.HID, ksplit,
                                                                        wbase + L.o_f1b, L.P_pad, wmul, h);
     *launches = 2;
   }
@@ -413,7 +426,7 @@ int fc1_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t w
   static bool attr = false;
   set_smem(k_fc1_dx_tc, DX_SMEM, attr);
   DxArgs p{wa.bs, wa.B, d.HID, d.F, wa.first ? 0 : 1, d.H2, d.W2, d.C2, p2, am2, dY2};
-  k_fc1_dx_tc<<<dim3(d.F / 128, wa.A), 192, DX_SMEM, st>>>(mw, md, p);
+  launch_pdl(wa.pdl, k_fc1_dx_tc, dim3(d.F / 128, wa.A), 192, DX_SMEM, st, mw, md, p);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -443,7 +456,7 @@ int fc1_dw_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wc
   const int ntiles = d.F / DW_N, mtiles = d.HID / 128;
   DwArgs p{wa.bs, wa.B, d.HID, d.F, ntiles, wa.first ? 0 : 1, wsrc + L.o_f1b, L.P_pad, slots_w + L.o_f1b,
            L.P_pad, dh, wa.lr};
-  k_fc1_dw_tc<<<dim3(mtiles * ntiles, wa.A), 192, DW_SMEM, st>>>(mh, mx, mws, mwd, p);
+  launch_pdl(wa.pdl, k_fc1_dw_tc, dim3(mtiles * ntiles, wa.A), 192, DW_SMEM, st, mh, mx, mws, mwd, p);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -3,6 +3,8 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+
+#include "dev_util.cuh"
 #include <stdint.h>
 
 namespace flb {
