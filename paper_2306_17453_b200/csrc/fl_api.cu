@@ -118,6 +118,7 @@ CnnBufs cnn_group_view(const CnnBufs& b, const CnnDims& d, int B, int64_t base_c
   v.part2_tc_cap = per_group_z;
   v.part1_tc_cap = per_group_z;
   v.fc1_part = b.fc1_part + (int64_t)g * b.fc1_part_floats;
+  v.c1wt = b.c1wt ? b.c1wt + base_client * C1WT_FLOATS : nullptr;
   return v;
 }
 
@@ -325,7 +326,7 @@ void fl_round_destroy(fl_ctx* c) {
   void* ptrs[] = {c->d_theta, c->d_canon_of, c->d_canon, c->d_slots, c->d_S, c->d_xpack, c->d_ypack, c->d_stage,
                   c->d_ystage, c->d_src_row, c->d_n, c->d_steps, c->d_slot_off, c->ws.d_sidx, c->ws.d_bs,
                   c->cb.a1, c->cb.p1, c->cb.a2, c->cb.p2, c->cb.h, c->cb.dh, c->cb.am1, c->cb.am2, c->cb.dp2,
-                  c->cb.dY2, c->cb.dp1, c->cb.dY1, c->cb.part1, c->cb.part2, c->cb.xplanar, c->cb.fc1_part,
+                  c->cb.dY2, c->cb.dp1, c->cb.dY1, c->cb.part1, c->cb.part2, c->cb.xplanar, c->cb.fc1_part, c->cb.c1wt, c->cb.c1wt_g,
                   c->cb.dz};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -657,6 +658,14 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       c->cb_part_cap = pg * NG;
     }
     c->part_group_z = pg;
+    if (K > b.c1wt_cap) {  // pad taps must read as zero: cleared once per allocation
+      if (b.c1wt) cudaFree(b.c1wt);
+      b.c1wt = nullptr;
+      CK(cudaMalloc(&b.c1wt, sizeof(float) * K * C1WT_FLOATS));
+      b.c1wt_cap = K;
+      CK(cudaMemsetAsync(b.c1wt, 0, sizeof(float) * K * C1WT_FLOATS, c->st));
+    }
+    if (!b.c1wt_g) CK(cudaMalloc(&b.c1wt_g, sizeof(float) * C1WT_FLOATS));
   }
   c->place_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 
@@ -695,6 +704,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   c->prof.begin(st);
   if (cnn) launches += pack_cnn(L, xsrc, srow, R, c->d_xpack, c->cb.xplanar, st);
   else launches += gather_rows_f32(xsrc, srow, R, L.D_pack, c->d_xpack, st);
+  if (cnn && c->cfg.math == 0 && conv1_tc_supported(L)) launches += c1wt_pack(c->d_theta + L.o_c1w, c->cb.c1wt_g, st);
   launches += gather_i32(ysrc, srow, R, c->d_ypack, st);
   c->prof.end(K_PACK, 0, (double)R * (4.0 * (L.D_in + L.D_pack) + 8.0), st);
   CKL();

@@ -103,6 +103,9 @@ struct CnnBufs {
   float* fc1_part = nullptr;                  // fc1 forward split-K partials
   int64_t fc1_part_floats = 0;
   int64_t xplanar_cap = 0;
+  float* c1wt = nullptr;    // [client slot][C1WT_FLOATS] tap-major conv1 weights (written by the SGD)
+  float* c1wt_g = nullptr;  // [C1WT_FLOATS] the same for θ_g (first wave)
+  int64_t c1wt_cap = 0;
 };
 
 // The buffers of one client group: every per-slot pointer advanced to the group's first
@@ -183,7 +186,10 @@ int conv2_dw_reduce_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, i
 int64_t conv2_dw_tc_part_z(int64_t max_clients);
 int64_t conv2_dw_tc_z_floats();
 bool conv1_tc_supported(const Layout& L);
-int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* xpack,
+// conv1 forward B operand: per-client tap-major weights [kw][kh = 0..5][32 o][4 c] (pad tap zero)
+constexpr int C1WT_FLOATS = 30 * 32 * 4;
+int c1wt_pack(const float* c1w, float* out, cudaStream_t st);
+int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, const float* wt, const float* xpack,
                  int64_t xrows, float* p1, uint8_t* am1, cudaStream_t st);
 int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64_t xrows, const float* dY1,
                 int64_t slots, float* part, int64_t part_cap, int* nch_out, int* rpc_out, cudaStream_t st);

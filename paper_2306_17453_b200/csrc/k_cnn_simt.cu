@@ -281,7 +281,8 @@ __global__ void k_unpool(const float* __restrict__ dp, const float* __restrict__
 
 // Σ of the split-K partials, then fused SGD on the conv weights and bias.
 __global__ void k_dw_reduce_sgd(const float* __restrict__ part, int nch, int rpc, const int32_t* __restrict__ bs,
-                                int O, int N, WSrc w, int64_t o_w, int64_t o_b, float* dst, int64_t P_pad, float lr) {
+                                int O, int N, WSrc w, int64_t o_w, int64_t o_b, float* dst, int64_t P_pad, float lr,
+                                float* __restrict__ wt) {
   pdl_wait();  // (PDL) previous kernel's writes visible; the implicit trigger is at exit
   const int a = blockIdx.y;
   const int nvalid = (bs[a] + rpc - 1) / rpc;
@@ -291,7 +292,12 @@ __global__ void k_dw_reduce_sgd(const float* __restrict__ part, int nch, int rpc
     g = ordered_sum(part + (int64_t)a * nch * tot + e, nvalid, tot);
     const int m = e / N, n = e - m * N;
     const int64_t off = n < N - 1 ? o_w + (int64_t)m * (N - 1) + n : o_b + m;
-    dst[(int64_t)a * P_pad + off] = *w.at(a, off) - lr * g;
+    const float nv = *w.at(a, off) - lr * g;
+    dst[(int64_t)a * P_pad + off] = nv;
+    if (wt && n < N - 1) {  // conv1 (cpad = 4): also the forward's tap-major copy
+      const int tap = n >> 2, kh = tap / 5, kw = tap - kh * 5;
+      wt[(int64_t)a * C1WT_FLOATS + ((kw * 6 + kh) * 32 + m) * 4 + (n & 3)] = nv;
+    }
   }
 }
 
@@ -482,7 +488,7 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   const bool tc1 = wa.use_tc && conv1_tc_supported(L);
   pf.begin(st);
   if (tc1) {  // bias + ReLU + pool fused into the epilogue
-    if (conv1_fwd_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, xpack, b.xrows, b.p1, b.am1, st) < 0) return -1;
+    if (conv1_fwd_tc(L, wa, w.base, wa.first ? b.c1wt_g : b.c1wt, xpack, b.xrows, b.p1, b.am1, st) < 0) return -1;
     ++n;
     pf.end(K_CONV1_FWD, f_c1, 4.0 * S * hw0 * d.cin + 5.0 * S * hw1 * d.C1, st);
   } else {
@@ -586,7 +592,7 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     pf.end(K_CONV2_DW, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
     pf.begin(st);
     launch_pdl(wa.pdl, k_dw_reduce_sgd, dim3(16, A), 256, 0, st, b.part2, b.nch, rpc, wa.bs, d.C2, 25 * d.C1 + 1, w, L.o_c2w,
-                                                 L.o_c2b, slots, L.P_pad, wa.lr), ++n;
+                                                 L.o_c2b, slots, L.P_pad, wa.lr, nullptr), ++n;
     pf.end(K_CONV2_DWR, 0, 8.0 * A * d.C2 * 25 * d.C1, st);
   }
   int nch1 = b.nch, rpc1 = rpc;
@@ -602,7 +608,7 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   pf.begin(st);
   launch_pdl(wa.pdl, k_dw_reduce_sgd, dim3((d.C1 * (25 * d.cpad + 1) + 127) / 128, A), 128, 0, st, 
       b.part1, nch1, rpc1, wa.bs, d.C1, 25 * d.cpad + 1, w, L.o_c1w,
-                                              L.o_c1b, slots, L.P_pad, wa.lr), ++n;
+                                              L.o_c1b, slots, L.P_pad, wa.lr, tc1 ? b.c1wt : nullptr), ++n;
   pf.end(K_CONV1_DWR, 0, 8.0 * A * d.C1 * 25 * d.cin, st);
   return n;
 }

@@ -28,45 +28,63 @@ namespace {
 constexpr int H = 32, W = 32, C1 = 32, ROWB = W * 16;  // 512 B per image row of 4-channel pixels
 
 // ------------------------------------------------------------------ forward
-// One CTA = one half-plane (16 image rows = 4 M-tiles) of a sample, so two CTAs fit per SM
-// and one's loads / epilogue overlap the other's MMAs.
-constexpr int F_ROWS = 16 + 5;                  // output rows + halo + the kh = 5 pad tap
-constexpr int F_COPY = F_ROWS * ROWB;           // 10752 B
-constexpr int F_A = 5 * F_COPY;                 // 53760
-constexpr int F_B = 30 * 512;                   // (kw, kh = 0..5) x [32 o][4 c]
-constexpr int F_XCH = F_A + F_B;                // epilogue exchange buffer [4][32][16] fp32
-constexpr int F_BAR = F_XCH + 4 * 32 * 16 * 4;
-constexpr int F_SMEM = F_BAR + 64 + 1024;
+// Persistent: CTA b handles tiles t = b, b + grid, ... of the A·B·4 (client, sample,
+// quadrant) tiles; a quadrant = 16 image rows x 16 columns = two M=128 tiles of 8 rows x 16
+// px.  With a 16-pixel row pitch the 8-pixel core-matrix groups of an M tile are uniformly
+// strided (SBO = 128 B), and the 2x2 pool window of accumulator row l lies in lanes l, l^1,
+// l^16, l^17 of one warp, so the epilogue pools with shuffles.  Stages (4) hold the 5
+// shifted copies of the quadrant's input (+halo) and the client's tap-major weights (one bulk
+// copy from the c1wt side buffer the previous step's SGD wrote); TMEM accumulators are
+// double-buffered so loads, MMAs and the epilogue of consecutive tiles overlap.
+constexpr int Q_ROWS = 16 + 5;                  // 16 output rows + halo + the kh = 5 pad tap
+constexpr int Q_ROWB = 16 * 16;                 // 256 B per 16-pixel row
+constexpr int Q_COPY = Q_ROWS * Q_ROWB;         // 5376
+constexpr int Q_A = 5 * Q_COPY;                 // 26880
+constexpr int Q_B = C1WT_FLOATS * 4;            // 15360: [kw][kh = 0..5][32 o][4 c]
+constexpr int Q_STAGE = Q_A + Q_B;              // 42240
+constexpr int Q_NST = 4;
+constexpr int Q_BAR = Q_NST * Q_STAGE;
+constexpr int Q_SMEM = Q_BAR + 128 + 1024;
+static_assert(Q_STAGE % 128 == 0, "TMA destinations stay 128-byte aligned");
 
 struct C1Args {
   const int32_t* sidx;
   const int32_t* bs;
-  int B, wmul;
+  int A, B, wmul;
+  const float* wt;    // tap-major weights of client 0; client a at + a*C1WT_FLOATS*wmul
   const float* bias;  // client 0 bias; client a at + a*stride*wmul
   int64_t bias_stride;
   float* p1;          // [S][16][16][32] pooled ReLU output
   uint8_t* am1;       // [S][16][16][32] window argmax
 };
 
-__global__ void __launch_bounds__(192, 2)
-    k_conv1_fwd_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, C1Args p) {
+__global__ void __launch_bounds__(192, 1)
+    k_conv1_fwd_tc(const __grid_constant__ CUtensorMap mapX, C1Args p) {
   constexpr uint32_t IDESC = tc::idesc_tf32(128, C1, 0, 0);
-  const int r = blockIdx.x >> 1, half = blockIdx.x & 1, a = blockIdx.y;
-  if (r >= p.bs[a]) return;
-  const int s = a * p.B + r;
+  const int T = p.A * p.B * 4;
+  auto valid = [&](int t) { return ((t >> 2) % p.B) < p.bs[t / (4 * p.B)]; };
   // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
   // would stall other streams' kernels) or touching anything it writes.
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + F_BAR);
-  uint64_t* tfull = full + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Q_BAR);
+  uint64_t* empty = full + Q_NST;
+  uint64_t* afull = empty + Q_NST;
+  uint64_t* aempty = afull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(aempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) {
     if (lane == 0) {
-      tc::mbar_init(full, 1);
-      tc::mbar_init(tfull, 1);
+      tc::prefetch_tmap(&mapX);
+      for (int i = 0; i < Q_NST; ++i) {
+        tc::mbar_init(full + i, 1);
+        tc::mbar_init(empty + i, 1);
+      }
+      for (int i = 0; i < 2; ++i) {
+        tc::mbar_init(afull + i, 1);
+        tc::mbar_init(aempty + i, 128);
+      }
       tc::fence_mbar_init();
     }
     __syncwarp();
@@ -77,77 +95,115 @@ __global__ void __launch_bounds__(192, 2)
   tc::tc_fence_after();
   const uint32_t tbase = *tslot;
   if (warp == 0) {
+    // ---------------- producer
     if (tc::elect_one()) {
-      const int row = p.sidx[s];
-      tc::mbar_expect_tx(full, F_A + F_B);
-      for (int kw = 0; kw < 5; ++kw)
-        tc::tma_load_4d(smem + kw * F_COPY, &mapX, full, 0, kw - 2, 16 * half - 2, row);
-      for (int kw = 0; kw < 5; ++kw)
-        for (int kh = 0; kh < 6; ++kh)  // tap 25..29 (kh = 5) is out of range -> zeros
-          tc::tma_load_4d(smem + F_A + (kw * 6 + kh) * 512, &mapW, full, 0, kh * 5 + kw, 0, a * p.wmul);
+      int it = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x) {
+        if (!valid(t)) continue;
+        const int a = t / (4 * p.B), s = t >> 2, vh = (t >> 1) & 1, ch = t & 1;
+        const int st = it % Q_NST, ph = (it / Q_NST) & 1;
+        ++it;
+        tc::mbar_wait(empty + st, ph ^ 1);
+        uint8_t* sa = smem + st * Q_STAGE;
+        tc::mbar_expect_tx(full + st, Q_STAGE);
+        const int row = p.sidx[s];
+        for (int kw = 0; kw < 5; ++kw)
+          tc::tma_load_3d(sa + kw * Q_COPY, &mapX, full + st, 4 * (16 * ch + kw - 2), 16 * vh - 2, row);
+        tc::bulk_load(sa + Q_A, p.wt + (int64_t)a * C1WT_FLOATS * p.wmul, Q_B, full + st);
+      }
     }
   } else if (warp == 1) {
+    // ---------------- MMA issuer
     if (tc::elect_one()) {
-      tc::mbar_wait(full, 0);
-      tc::tc_fence_after();
-      const uint32_t sa = tc::smem_u32(smem), sb = sa + F_A;
-      for (int j = 0; j < 4; ++j)
-        for (int kw = 0; kw < 5; ++kw)
-          for (int kp = 0; kp < 3; ++kp) {  // taps (2kp, kw) and (2kp+1, kw)
-            const uint64_t ad = tc::sdesc(sa + kw * F_COPY + (4 * j + 2 * kp) * ROWB, ROWB, 128, tc::kSWNONE);
-            const uint64_t bd = tc::sdesc(sb + (kw * 6 + 2 * kp) * 512, 512, 128, tc::kSWNONE);
-            tc::mma_tf32(tbase + j * C1, ad, bd, IDESC, (kw | kp) != 0);
-          }
-      tc::mma_commit(tfull);
+      int it = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x) {
+        if (!valid(t)) continue;
+        const int st = it % Q_NST, ph = (it / Q_NST) & 1, buf = it & 1, aph = (it >> 1) & 1;
+        ++it;
+        tc::mbar_wait(aempty + buf, aph ^ 1);
+        tc::mbar_wait(full + st, ph);
+        tc::tc_fence_after();
+        const uint32_t sa = tc::smem_u32(smem + st * Q_STAGE), sb = sa + Q_A;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int kw = 0; kw < 5; ++kw)
+#pragma unroll
+            for (int kp = 0; kp < 3; ++kp) {  // taps (2kp, kw) and (2kp+1, kw): LBO = one image row
+              const uint64_t ad = tc::sdesc(sa + kw * Q_COPY + (8 * j + 2 * kp) * Q_ROWB, Q_ROWB, 128, tc::kSWNONE);
+              const uint64_t bd = tc::sdesc(sb + (kw * 6 + 2 * kp) * 512, 512, 128, tc::kSWNONE);
+              tc::mma_tf32(tbase + buf * 64 + j * C1, ad, bd, IDESC, (kw | kp) != 0);
+            }
+        tc::mma_commit(empty + st);
+        tc::mma_commit(afull + buf);
+      }
     }
   } else {
+    // ---------------- epilogue: bias + ReLU + 2x2 max-pool (first maximum in row-major
+    // window order, reading A13) with shuffles; lanes (l & 17) == 0 own a pooled pixel.
     const int qd = warp & 3;
-    tc::mbar_wait(tfull, 0);
-    tc::tc_fence_after();
-    // bias + ReLU + 2x2 max-pool (first maximum in row-major window order, reading A13).
-    // Tile j holds image rows 16*half + 4j..+3, one row per warp; the vertical window partner is
-    // in the next warp, so each 16-channel chunk is exchanged through shared memory.
-    const float* bias = p.bias + (int64_t)a * p.bias_stride * p.wmul;
-    float* xb = reinterpret_cast<float*>(smem + F_XCH);  // [4 rows][32 w][16 c]
-    const int t = threadIdx.x - 64;                    // 0..127 over the epilogue warps
-    for (int j = 0; j < 4; ++j) {
-#pragma unroll 1
-      for (int n0 = 0; n0 < C1; n0 += 16) {
-        float v[16];
-        tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + j * C1 + n0, v);
-        float4* xr = reinterpret_cast<float4*>(xb + (qd * 32 + lane) * 16);
+    int it = 0;
+    for (int t = blockIdx.x; t < T; t += gridDim.x) {
+      if (!valid(t)) continue;
+      const int a = t / (4 * p.B), s = t >> 2, vh = (t >> 1) & 1, ch = t & 1;
+      const int buf = it & 1, aph = (it >> 1) & 1;
+      ++it;
+      tc::mbar_wait(afull + buf, aph);
+      tc::tc_fence_after();
+      const float* bias = p.bias + (int64_t)a * p.bias_stride * p.wmul;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          xr[i] = make_float4(v[4 * i] + bias[n0 + 4 * i], v[4 * i + 1] + bias[n0 + 4 * i + 1],
-                              v[4 * i + 2] + bias[n0 + 4 * i + 2], v[4 * i + 3] + bias[n0 + 4 * i + 3]);
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        // thread t -> pooled row (t >> 6), pooled column ((t >> 2) & 15), channels 4(t & 3)..+3
-        const int pr = t >> 6, pc = (t >> 2) & 15, c4 = t & 3;
-        const float* q00 = xb + ((2 * pr) * 32 + 2 * pc) * 16 + 4 * c4;
-        float4 r;
-        uint32_t am = 0;
+      for (int j = 0; j < 2; ++j) {
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const float x00 = q00[cc], x01 = q00[16 + cc], x10 = q00[32 * 16 + cc], x11 = q00[33 * 16 + cc];
-          float bv = x00;
-          uint32_t bi = 0;
-          if (x01 > bv) { bv = x01; bi = 1; }
-          if (x10 > bv) { bv = x10; bi = 2; }
-          if (x11 > bv) { bv = x11; bi = 3; }
-          reinterpret_cast<float*>(&r)[cc] = bv > 0.f ? bv : 0.f;
-          am |= bi << (8 * cc);
+        for (int n0 = 0; n0 < C1; n0 += 16) {
+          float v[16];
+          tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + buf * 64 + j * C1 + n0, v);
+          float pv[16];
+          uint8_t pa[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float x00 = v[q] + __ldg(bias + n0 + q);
+            const float x01 = __shfl_xor_sync(0xffffffffu, x00, 1);
+            const float x10 = __shfl_xor_sync(0xffffffffu, x00, 16);
+            const float x11 = __shfl_xor_sync(0xffffffffu, x00, 17);
+            float bv = x00;
+            int bi = 0;
+            if (x01 > bv) { bv = x01; bi = 1; }
+            if (x10 > bv) { bv = x10; bi = 2; }
+            if (x11 > bv) { bv = x11; bi = 3; }
+            pv[q] = bv > 0.f ? bv : 0.f;
+            pa[q] = (uint8_t)bi;
+          }
+          if ((lane & 17) == 0) {
+            const int prow = 8 * vh + 4 * j + qd, pcol = 8 * ch + ((lane & 15) >> 1);
+            const int64_t o = (((int64_t)s * 16 + prow) * 16 + pcol) * C1 + n0;
+            float4* dst = reinterpret_cast<float4*>(p.p1 + o);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dst[q] = make_float4(pv[4 * q], pv[4 * q + 1], pv[4 * q + 2], pv[4 * q + 3]);
+            uint32_t pk[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              pk[q] = pa[4 * q] | (pa[4 * q + 1] << 8) | (pa[4 * q + 2] << 16) | ((uint32_t)pa[4 * q + 3] << 24);
+            *reinterpret_cast<uint4*>(p.am1 + o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
         }
-        const int64_t o = (((int64_t)s * 16 + 8 * half + 2 * j + pr) * 16 + pc) * C1 + n0 + 4 * c4;
-        *reinterpret_cast<float4*>(p.p1 + o) = r;
-        *reinterpret_cast<uint32_t*>(p.am1 + o) = am;
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // buffer reused by the next chunk
       }
+      tc::tc_fence_before();
+      tc::mbar_arrive(aempty + buf);
     }
   }
   tc::tc_fence_before();
   __syncthreads();
   pdl_trigger();  // late trigger: a dependent kernel's CTAs park on SM resources until it runs
   if (warp == 0) tc::tmem_dealloc<128>(tbase);
+}
+
+// Tap-major copy of conv1 weights for the forward's B operand: out[(kw*6+kh)*32+o][c] =
+// w[o][kh*5+kw][c], zeros for the pad tap kh = 5.
+__global__ void k_c1wt_pack(const float* __restrict__ w, float* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= C1WT_FLOATS) return;
+  const int c = e & 3, o = (e >> 2) & 31, kk = e >> 7, kw = kk / 6, kh = kk % 6;
+  out[e] = kh < 5 ? w[(o * 25 + kh * 5 + kw) * 4 + c] : 0.f;
 }
 
 // ------------------------------------------------------------------ weight gradient
@@ -278,24 +334,29 @@ __global__ void __launch_bounds__(192, 1)
 }  // namespace
 
 // conv1 forward (+ bias) on tensor cores: packed input rows -> a1 (pre-activation).
-int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* xpack,
+int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, const float* wt, const float* xpack,
                  int64_t xrows, float* p1, uint8_t* am1, cudaStream_t st) {
-  CUtensorMap mx, mw;
-  uint64_t dx[4] = {4, W, H, (uint64_t)xrows};
-  uint64_t sx[3] = {16, 16 * W, 16 * W * H};
-  uint32_t bx[4] = {4, W, F_ROWS, 1};
-  uint64_t dw[4] = {4, 25, 32, (uint64_t)wclients};  // c1w[o][tap][4] of every client slot
-  uint64_t sw[3] = {16, 400, (uint64_t)L.P_pad * 4};
-  uint32_t bw[4] = {4, 1, 32, 1};
-  if (!tmap_encode(&mx, xpack, 4, dx, sx, bx, 0) || !tmap_encode(&mw, wbase + L.o_c1w, 4, dw, sw, bw, 0)) return -1;
+  CUtensorMap mx;
+  // a 16-pixel row segment (256 B) is the innermost box dimension; a one-pixel shift is a
+  // 16-byte-aligned start coordinate (a 16-byte inner box made TMA the bottleneck)
+  uint64_t dx[3] = {4 * W, H, (uint64_t)xrows};
+  uint64_t sx[2] = {16 * W, 16 * W * H};
+  uint32_t bx[3] = {64, Q_ROWS, 1};
+  if (!tmap_encode(&mx, xpack, 3, dx, sx, bx, 0)) return -1;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_conv1_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM);
+    cudaFuncSetAttribute(k_conv1_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_SMEM);
     attr = true;
   }
-  C1Args p{wa.sidx, wa.bs, wa.B, wa.first ? 0 : 1, wbase + L.o_c1b, L.P_pad, p1, am1};
-  launch_pdl(wa.pdl, k_conv1_fwd_tc, dim3(2 * wa.B, wa.A), 192, F_SMEM, st, mx, mw, p);
+  C1Args p{wa.sidx, wa.bs, wa.A, wa.B, wa.first ? 0 : 1, wt, wbase + L.o_c1b, L.P_pad, p1, am1};
+  const int tiles = wa.A * wa.B * 4;
+  launch_pdl(wa.pdl, k_conv1_fwd_tc, dim3(tiles < 148 ? tiles : 148), 192, Q_SMEM, st, mx, p);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+int c1wt_pack(const float* c1w, float* out, cudaStream_t st) {
+  k_c1wt_pack<<<(C1WT_FLOATS + 255) / 256, 256, 0, st>>>(c1w, out);
+  return 1;
 }
 
 // conv1 weight gradient on tensor cores: partials [A*nch][32][101] for k_dw_reduce_sgd.
