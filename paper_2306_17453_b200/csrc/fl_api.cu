@@ -209,7 +209,7 @@ struct fl_ctx {
   int64_t steps_cap = 0;
   int64_t* d_slot_off = nullptr;
   int64_t slot_off_cap = 0;
-  int64_t sidx_cap = 0, bs_cap = 0;
+  int64_t sidx_cap = 0, bs_cap = 0, bpre_cap = 0;
   WaveSched ws;
   CnnBufs cb;
   int64_t cb_slots_cap = 0, cb_part_cap = 0;
@@ -324,7 +324,7 @@ void fl_round_destroy(fl_ctx* c) {
   if (c->st) cudaStreamSynchronize(c->st);
   if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
   void* ptrs[] = {c->d_theta, c->d_canon_of, c->d_canon, c->d_slots, c->d_S, c->d_xpack, c->d_ypack, c->d_stage,
-                  c->d_ystage, c->d_src_row, c->d_n, c->d_steps, c->d_slot_off, c->ws.d_sidx, c->ws.d_bs,
+                  c->d_ystage, c->d_src_row, c->d_n, c->d_steps, c->d_slot_off, c->ws.d_sidx, c->ws.d_bs, c->ws.d_bpre,
                   c->cb.a1, c->cb.p1, c->cb.a2, c->cb.p2, c->cb.h, c->cb.dh, c->cb.am1, c->cb.am2, c->cb.dp2,
                   c->cb.dY2, c->cb.dp1, c->cb.dY1, c->cb.part1, c->cb.part2, c->cb.xplanar, c->cb.fc1_part, c->cb.c1wt, c->cb.c1wt_g,
                   c->cb.dz};
@@ -541,7 +541,8 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   ws.n_waves = (int64_t)ws.A.size();
   const int64_t n_sidx = ws.slot_off[(size_t)ws.n_waves], n_bs = ws.bs_off[(size_t)ws.n_waves];
   // pinned table layout: src_row[R] i64 | n[K] i64 | slot_off[W+1] i64 | sidx i32 | bs i32 | steps[K] i32
-  size_t need = sizeof(int64_t) * (size_t)(R + K + ws.n_waves + 1) + sizeof(int32_t) * (size_t)(n_sidx + n_bs + K) + 64;
+  size_t need = sizeof(int64_t) * (size_t)(R + K + ws.n_waves + 1) +
+                sizeof(int32_t) * (size_t)(n_sidx + n_bs + K + n_bs + ws.n_waves) + 64;
   if (c->tab_pending) {
     CK(cudaEventSynchronize(c->ev_tab));
     c->tab_pending = false;
@@ -558,6 +559,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   int32_t* h_sidx = (int32_t*)(h_soff + ws.n_waves + 1);
   int32_t* h_bs = h_sidx + n_sidx;
   int32_t* h_steps = h_bs + n_bs;
+  int32_t* h_bpre = h_steps + K;  // per wave: prefix sums of |b| over its A clients (A + 1 entries)
   for (int64_t e = 0; e < K; ++e) {
     int64_t id = c->local_ids[(size_t)c->exec[(size_t)e]];
     for (int64_t i = 0; i < c->n_exec[(size_t)e]; ++i) h_src[c->pseg[(size_t)e] + i] = c->pop_off[(size_t)id] + i;
@@ -594,6 +596,11 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       }
     }
   }
+  for (int64_t k = 0; k < ws.n_waves; ++k) {
+    int32_t* pre = h_bpre + ws.bs_off[(size_t)k] + k;
+    pre[0] = 0;
+    for (int32_t a = 0; a < ws.A[(size_t)k]; ++a) pre[a + 1] = pre[a] + h_bs[ws.bs_off[(size_t)k] + a];
+  }
   // device capacity (grow-only; allocation happens on the first round of a given size)
   CK(grow_dev(c->d_slots, c->slots_cap, std::max<int64_t>(K, 1) * L.P_pad));
   CK(grow_dev(c->d_xpack, c->xpack_cap, std::max<int64_t>(R, 1) * L.D_pack));
@@ -606,6 +613,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   CK(grow_dev(c->d_slot_off, c->slot_off_cap, ws.n_waves + 1));
   CK(grow_dev(ws.d_sidx, c->sidx_cap, n_sidx));
   CK(grow_dev(ws.d_bs, c->bs_cap, n_bs));
+  CK(grow_dev(ws.d_bpre, c->bpre_cap, n_bs + ws.n_waves));
   if (!c->pop_dev) {
     CK(grow_dev(c->d_stage, c->stage_cap, std::max<int64_t>(R, 1) * L.D_in));
     CK(grow_dev(c->d_ystage, c->ystage_cap, R));
@@ -680,9 +688,10 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   CK(cudaMemcpyAsync(ws.d_sidx, h_sidx, sizeof(int32_t) * n_sidx, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(ws.d_bs, h_bs, sizeof(int32_t) * n_bs, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(c->d_steps, h_steps, sizeof(int32_t) * K, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ws.d_bpre, h_bpre, sizeof(int32_t) * (n_bs + ws.n_waves), cudaMemcpyHostToDevice, st));
   CK(cudaEventRecord(c->ev_tab, st));
   c->tab_pending = true;
-  h2d += (int64_t)(sizeof(int64_t) * (R + K + ws.n_waves + 1) + sizeof(int32_t) * (n_sidx + n_bs + K));
+  h2d += (int64_t)(sizeof(int64_t) * (R + K + ws.n_waves + 1) + sizeof(int32_t) * (n_sidx + 2 * n_bs + K + ws.n_waves));
   // stage the cohort's samples: device population -> gather; host population -> H2D copies
   const float* xsrc = (const float*)c->x;
   const int32_t* ysrc = c->y;
@@ -740,7 +749,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
           for (int32_t a = 0; a < ws.A[(size_t)k]; ++a) sum_bs += h_bs[ws.bs_off[(size_t)k] + a];
           WaveArgs wa{ws.A[(size_t)k], (int)B, t == 0, ws.d_sidx + ws.slot_off[(size_t)k],
                       ws.d_bs + ws.bs_off[(size_t)k], c->cfg.lr, sum_bs, &c->prof, c->cfg.math == 0,
-                      ws.gn[(size_t)g], ws.A[(size_t)k] <= c->pdl_max_a};
+                      ws.gn[(size_t)g], ws.A[(size_t)k] <= c->pdl_max_a, ws.d_bpre + ws.bs_off[(size_t)k] + k};
           int nl = cnn_wave_simt(L, wa, c->d_xpack, c->d_ypack, c->d_theta, c->d_slots + base * L.P_pad,
                                  gv[(size_t)g], gst[(size_t)g]);
           if (nl < 0)

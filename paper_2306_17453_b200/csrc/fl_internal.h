@@ -81,6 +81,7 @@ struct WaveSched {
   std::vector<int64_t> bs_off;     // offset of the wave's [A_t] batch-size table
   int32_t* d_sidx = nullptr;       // device: packed sample row or -1
   int32_t* d_bs = nullptr;         // device: |b| of each active client
+  int32_t* d_bpre = nullptr;       // device: per wave, prefix sums of |b| (A + 1 entries at bs_off + wave)
   int ngroups = 1;
   std::vector<int64_t> gbase, gn, gw0, gnw;
   std::vector<int> gstream;        // stream index of each group
@@ -168,6 +169,7 @@ struct WaveArgs {
   bool use_tc;       // tensor-core (tcgen05) kernels where built for this geometry
   int64_t wclients;  // client slots allocated (weights tensor-map extent)
   bool pdl;          // launch this wave's kernels with programmatic dependent launch
+  const int32_t* bpre;  // [A + 1] prefix sums of bs (balanced split-K over the wave's samples)
 };
 
 // Kernel launchers (k_*.cu). All asynchronous on `st`. Return the number of launches.
@@ -180,9 +182,9 @@ bool tmap_encode(struct CUtensorMap_st* m, const void* base, int rank, const uin
 // tcgen05 kernels (k_conv_tc.cu, k_convdw_tc.cu)
 bool conv_tc_supported(const Layout& L);
 int conv2_dw_tc(const Layout& L, const WaveArgs& wa, const float* p1, const float* dY2, int64_t slots, float* part,
-                int64_t part_cap, int* nch_out, int* rpc_out, cudaStream_t st);
+                int64_t part_cap, int* g_out, cudaStream_t st);
 int conv2_dw_reduce_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wsrc_stride, float* dst,
-                       const float* part, int nch, int rpc, cudaStream_t st);
+                       const float* part, int G, cudaStream_t st);
 int64_t conv2_dw_tc_part_z(int64_t max_clients);
 int64_t conv2_dw_tc_z_floats();
 bool conv1_tc_supported(const Layout& L);
@@ -198,6 +200,9 @@ int fc1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t 
                int64_t slots, float* h, float* part, int64_t part_floats, cudaStream_t st, int* launches);
 int fc1_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dh,
               const float* p2, const uint8_t* am2, int64_t slots, float* dY2, cudaStream_t st);
+int fc1_bwd_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wclients_src, float* slots_w,
+               int64_t wclients_dst, const float* dh, const float* p2, const uint8_t* am2, int64_t slots, float* dY2,
+               cudaStream_t st);
 int fc1_dw_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wclients_src, float* slots_w,
               int64_t wclients_dst, const float* dh, const float* p2, int64_t slots, cudaStream_t st);
 int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p1,

@@ -540,28 +540,41 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
                                                           slots, L.P_pad, wa.lr), ++n;
   pf.end(K_HEAD, 3.0 * f_f2, 8.0 * A * d.NCLS * d.HID + 8.0 * S * d.HID, st);
   // ---- backward (each layer's dX reads W before its dW epilogue overwrites it)
-  pf.begin(st);
-  if (tcf) {  // fused: dp2 -> pool2/ReLU backward -> dY2 in the epilogue
-    if (fc1_dx_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, b.dh, b.p2, b.am2, b.slots, b.dY2, st) < 0) return -1;
-    ++n;
-    pf.end(K_FC1_DX, f_f1, wbytes + 4.0 * S * (d.F + d.HID) + S * hw1 * d.C2 * (9.0 / 4.0), st);
-  } else {
-    launch(FcDx{b.dh, wa.bs, B, d.F, d.HID, w, L.o_f1w, b.dp2}, B, d.F, A, st), ++n;
-    pf.end(K_FC1_DX, f_f1, wbytes + 4.0 * S * (d.F + d.HID), st);
+  static const bool fc1_fused = [] {
+    const char* e = getenv("FL_FC1_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  if (tcf && fc1_fused) {  // one W1 pass: dX (+ pool2/ReLU backward -> dY2), dW, SGD
     pf.begin(st);
-    k_unpool<<<dim3(4, A * B), 256, 0, st>>>(b.dp2, b.p2, b.am2, d.H1, d.W1, d.C2, B, wa.bs, b.dY2), ++n;
-    pf.end(K_UNPOOL2, 0, S * hw1 * d.C2 * (4.0 + 9.0 / 4.0), st);
-  }
-  pf.begin(st);
-  if (tcf) {
-    if (fc1_dw_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, slots, wa.wclients, b.dh, b.p2, b.slots, st) < 0)
+    if (fc1_bwd_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, slots, wa.wclients, b.dh, b.p2, b.am2, b.slots, b.dY2,
+                   st) < 0)
       return -1;
     ++n;
+    pf.end(K_FC1_DW, 2.0 * f_f1, 2.0 * wbytes + 4.0 * S * (d.F + d.HID) + S * hw1 * d.C2 * (9.0 / 4.0), st);
   } else {
-    launch(FcDwSgd{b.dh, b.p2, wa.bs, B, d.F, d.HID, w, slots, L.P_pad, L.o_f1w, L.o_f1b, wa.lr}, d.HID, d.F + 1, A,
-           st), ++n;
+    pf.begin(st);
+    if (tcf) {  // fused: dp2 -> pool2/ReLU backward -> dY2 in the epilogue
+      if (fc1_dx_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, b.dh, b.p2, b.am2, b.slots, b.dY2, st) < 0) return -1;
+      ++n;
+      pf.end(K_FC1_DX, f_f1, wbytes + 4.0 * S * (d.F + d.HID) + S * hw1 * d.C2 * (9.0 / 4.0), st);
+    } else {
+      launch(FcDx{b.dh, wa.bs, B, d.F, d.HID, w, L.o_f1w, b.dp2}, B, d.F, A, st), ++n;
+      pf.end(K_FC1_DX, f_f1, wbytes + 4.0 * S * (d.F + d.HID), st);
+      pf.begin(st);
+      k_unpool<<<dim3(4, A * B), 256, 0, st>>>(b.dp2, b.p2, b.am2, d.H1, d.W1, d.C2, B, wa.bs, b.dY2), ++n;
+      pf.end(K_UNPOOL2, 0, S * hw1 * d.C2 * (4.0 + 9.0 / 4.0), st);
+    }
+    pf.begin(st);
+    if (tcf) {
+      if (fc1_dw_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, slots, wa.wclients, b.dh, b.p2, b.slots, st) < 0)
+        return -1;
+      ++n;
+    } else {
+      launch(FcDwSgd{b.dh, b.p2, wa.bs, B, d.F, d.HID, w, slots, L.P_pad, L.o_f1w, L.o_f1b, wa.lr}, d.HID, d.F + 1, A,
+             st), ++n;
+    }
+    pf.end(K_FC1_DW, f_f1, 2.0 * wbytes + 4.0 * S * (d.F + d.HID), st);
   }
-  pf.end(K_FC1_DW, f_f1, 2.0 * wbytes + 4.0 * S * (d.F + d.HID), st);
   pf.begin(st);
   if (tc) {  // pool1/ReLU backward fused into the epilogue: writes dY1 directly
     if (conv2_dx_tc(L, wa, w.base, wcl, b.dY2, b.slots, b.p1, b.am1, b.dY1, st) < 0) return -1;
@@ -576,13 +589,13 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   }
   const int rpc = (B + b.nch - 1) / b.nch;
   if (tc) {  // tcgen05 dW with all 800 (tap, c) rows resident in TMEM; SGD in the reduction
-    int nch2 = 0, rpc2 = 0;
+    int g2 = 0;
     pf.begin(st);
-    if (conv2_dw_tc(L, wa, b.p1, b.dY2, b.slots, b.part2, b.part2_tc_cap, &nch2, &rpc2, st) < 0) return -1;
+    if (conv2_dw_tc(L, wa, b.p1, b.dY2, b.slots, b.part2, b.part2_tc_cap, &g2, st) < 0) return -1;
     ++n;
     pf.end(K_CONV2_DW, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
     pf.begin(st);
-    if (conv2_dw_reduce_tc(L, wa, w.base, w.stride, slots, b.part2, nch2, rpc2, st) < 0) return -1;
+    if (conv2_dw_reduce_tc(L, wa, w.base, w.stride, slots, b.part2, g2, st) < 0) return -1;
     ++n;
     pf.end(K_CONV2_DWR, 0, 8.0 * A * d.C2 * 25 * d.C1, st);
   } else {

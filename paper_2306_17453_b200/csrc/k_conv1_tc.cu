@@ -43,7 +43,9 @@ constexpr int Q_A = 5 * Q_COPY;                 // 26880
 constexpr int Q_B = C1WT_FLOATS * 4;            // 15360: [kw][kh = 0..5][32 o][4 c]
 constexpr int Q_STAGE = Q_A + Q_B;              // 42240
 constexpr int Q_NST = 4;
-constexpr int Q_BAR = Q_NST * Q_STAGE;
+constexpr int XPITCH = 20;                      // floats per staged row (16 + 4: conflict-free v4 stores)
+constexpr int Q_XCH = Q_NST * Q_STAGE;          // 8 epilogue warps x [32 rows][XPITCH]
+constexpr int Q_BAR = Q_XCH + 8 * 32 * XPITCH * 4;
 constexpr int Q_SMEM = Q_BAR + 128 + 1024;
 static_assert(Q_STAGE % 128 == 0, "TMA destinations stay 128-byte aligned");
 
@@ -58,7 +60,10 @@ struct C1Args {
   uint8_t* am1;       // [S][16][16][32] window argmax
 };
 
-__global__ void __launch_bounds__(192, 1)
+// 320 threads: warp 0 producer, warp 1 MMA, warps 2-9 epilogue (two per TMEM lane quarter,
+// one per 16-channel half: the epilogue is issue-bound, so it gets the most warps).
+constexpr int F_THREADS = 320;
+__global__ void __launch_bounds__(F_THREADS, 1)
     k_conv1_fwd_tc(const __grid_constant__ CUtensorMap mapX, C1Args p) {
   constexpr uint32_t IDESC = tc::idesc_tf32(128, C1, 0, 0);
   const int T = p.A * p.B * 4;
@@ -83,7 +88,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       for (int i = 0; i < 2; ++i) {
         tc::mbar_init(afull + i, 1);
-        tc::mbar_init(aempty + i, 128);
+        tc::mbar_init(aempty + i, F_THREADS - 64);
       }
       tc::fence_mbar_init();
     }
@@ -140,52 +145,56 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     // ---------------- epilogue: bias + ReLU + 2x2 max-pool (first maximum in row-major
-    // window order, reading A13) with shuffles; lanes (l & 17) == 0 own a pooled pixel.
-    const int qd = warp & 3;
+    // window order, reading A13). A warp's 32 accumulator rows are 2 image rows x 16 px, so
+    // every pool window lies inside the warp: stage (acc + bias) in a warp-private smem tile,
+    // __syncwarp, then lane L pools channels 4(L&3).. of pooled column L>>2 (4 vector loads).
+    const int qd = warp & 3, nh = (warp - 2) >> 2, n0 = nh * 16;
+    float* xw = reinterpret_cast<float*>(smem + Q_XCH) + (warp - 2) * (32 * XPITCH);
+    const int pc = lane >> 2, c4 = lane & 3;
     int it = 0;
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
       if (!valid(t)) continue;
       const int a = t / (4 * p.B), s = t >> 2, vh = (t >> 1) & 1, ch = t & 1;
       const int buf = it & 1, aph = (it >> 1) & 1;
       ++it;
+      const float* bias = p.bias + (int64_t)a * p.bias_stride * p.wmul + n0;
+      float bv[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) bv[q] = __ldg(bias + q);
       tc::mbar_wait(afull + buf, aph);
       tc::tc_fence_after();
-      const float* bias = p.bias + (int64_t)a * p.bias_stride * p.wmul;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
+        float v[16];
+        tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + buf * 64 + j * C1 + n0, v);
+        float4* xr = reinterpret_cast<float4*>(xw + lane * XPITCH);
 #pragma unroll
-        for (int n0 = 0; n0 < C1; n0 += 16) {
-          float v[16];
-          tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + buf * 64 + j * C1 + n0, v);
-          float pv[16];
-          uint8_t pa[16];
+        for (int q = 0; q < 4; ++q)
+          xr[q] = make_float4(v[4 * q] + bv[4 * q], v[4 * q + 1] + bv[4 * q + 1], v[4 * q + 2] + bv[4 * q + 2],
+                              v[4 * q + 3] + bv[4 * q + 3]);
+        __syncwarp();
+        const float4 x00 = *reinterpret_cast<const float4*>(xw + (2 * pc) * XPITCH + 4 * c4);
+        const float4 x01 = *reinterpret_cast<const float4*>(xw + (2 * pc + 1) * XPITCH + 4 * c4);
+        const float4 x10 = *reinterpret_cast<const float4*>(xw + (2 * pc + 16) * XPITCH + 4 * c4);
+        const float4 x11 = *reinterpret_cast<const float4*>(xw + (2 * pc + 17) * XPITCH + 4 * c4);
+        __syncwarp();  // the tile is rewritten by the next j
+        float r[4];
+        uint32_t am = 0;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float x00 = v[q] + __ldg(bias + n0 + q);
-            const float x01 = __shfl_xor_sync(0xffffffffu, x00, 1);
-            const float x10 = __shfl_xor_sync(0xffffffffu, x00, 16);
-            const float x11 = __shfl_xor_sync(0xffffffffu, x00, 17);
-            float bv = x00;
-            int bi = 0;
-            if (x01 > bv) { bv = x01; bi = 1; }
-            if (x10 > bv) { bv = x10; bi = 2; }
-            if (x11 > bv) { bv = x11; bi = 3; }
-            pv[q] = bv > 0.f ? bv : 0.f;
-            pa[q] = (uint8_t)bi;
-          }
-          if ((lane & 17) == 0) {
-            const int prow = 8 * vh + 4 * j + qd, pcol = 8 * ch + ((lane & 15) >> 1);
-            const int64_t o = (((int64_t)s * 16 + prow) * 16 + pcol) * C1 + n0;
-            float4* dst = reinterpret_cast<float4*>(p.p1 + o);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) dst[q] = make_float4(pv[4 * q], pv[4 * q + 1], pv[4 * q + 2], pv[4 * q + 3]);
-            uint32_t pk[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              pk[q] = pa[4 * q] | (pa[4 * q + 1] << 8) | (pa[4 * q + 2] << 16) | ((uint32_t)pa[4 * q + 3] << 24);
-            *reinterpret_cast<uint4*>(p.am1 + o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          }
+        for (int cc = 0; cc < 4; ++cc) {
+          const float a0 = (&x00.x)[cc], a1 = (&x01.x)[cc], a2 = (&x10.x)[cc], a3 = (&x11.x)[cc];
+          float m = a0;
+          uint32_t bi = 0;
+          if (a1 > m) { m = a1; bi = 1; }
+          if (a2 > m) { m = a2; bi = 2; }
+          if (a3 > m) { m = a3; bi = 3; }
+          r[cc] = m > 0.f ? m : 0.f;
+          am |= bi << (8 * cc);
         }
+        const int prow = 8 * vh + 4 * j + qd, pcol = 8 * ch + pc;
+        const int64_t o = (((int64_t)s * 16 + prow) * 16 + pcol) * C1 + n0 + 4 * c4;
+        *reinterpret_cast<float4*>(p.p1 + o) = make_float4(r[0], r[1], r[2], r[3]);
+        *reinterpret_cast<uint32_t*>(p.am1 + o) = am;
       }
       tc::tc_fence_before();
       tc::mbar_arrive(aempty + buf);
@@ -350,7 +359,7 @@ int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, const 
   }
   C1Args p{wa.sidx, wa.bs, wa.A, wa.B, wa.first ? 0 : 1, wt, wbase + L.o_c1b, L.P_pad, p1, am1};
   const int tiles = wa.A * wa.B * 4;
-  launch_pdl(wa.pdl, k_conv1_fwd_tc, dim3(tiles < 148 ? tiles : 148), 192, Q_SMEM, st, mx, p);
+  launch_pdl(wa.pdl, k_conv1_fwd_tc, dim3(tiles < 148 ? tiles : 148), F_THREADS, Q_SMEM, st, mx, p);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -17,6 +17,8 @@
 // The epilogue writes the chunk's partial [801][64]; k_dw2_reduce_sgd sums the chunks of a
 // client and applies W <- W − η·g (θ_g read on the first wave, slot init fused).
 #include <cuda.h>
+
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,29 +43,43 @@ constexpr int NROW = 801;                        // 800 (tap, c) rows + bias
 constexpr int NO = 64;
 
 struct DwArgs {
-  const int32_t* bs;
-  int B, nch, rpc;
-  float* part;  // [A*nch][801][64]
+  const int32_t* bpre;  // [A + 1] prefix sums of the wave's batch sizes
+  int A, B, G;          // G CTAs split the wave's U k-blocks (8 per sample) evenly
+  int64_t U;
+  float* part;          // [A + G][801][64]: partial of (CTA c, client a) at z = a + c
 };
 
+// Largest a in [0, A) with bpre[a] <= x (the client owning concatenated sample x).
+__device__ __forceinline__ int client_of(const int32_t* __restrict__ bpre, int A, int64_t x) {
+  int lo = 0, hi = A - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (bpre[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Balanced split-K: CTA c reduces k-blocks [c·U/G, (c+1)·U/G) of the wave's concatenated
+// (client, sample, 2-row block) sequence; each client segment of that range ends with its
+// partial written to z = a + c (unique: CTA ranges are monotone in a).  The TMEM
+// accumulators are reused across segments (tempty: the epilogue has drained them).
 __global__ void __launch_bounds__(192, 1)
     k_conv2_dw_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapD, DwArgs p) {
   constexpr uint32_t IDESC = tc::idesc_tf32(128, NO, 1, 1);  // A and B MN-major
-  const int ch = blockIdx.x, a = blockIdx.y, z = a * p.nch + ch;
-  const int r0 = ch * p.rpc;
-  const int r1 = min(p.bs[a], r0 + p.rpc);
-  if (r0 >= r1) return;
-  const int nkb = (r1 - r0) * 8;
-
+  const int c = blockIdx.x;
+  const int64_t u0 = (int64_t)c * p.U / p.G, u1 = (int64_t)(c + 1) * p.U / p.G;
   // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
   // would stall other streams' kernels) or touching anything it writes.
   pdl_wait();
+  const int a0 = client_of(p.bpre, p.A, u0 >> 3);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   float* ones = reinterpret_cast<float*>(smem + ONES_OFF);
@@ -78,6 +94,7 @@ __global__ void __launch_bounds__(192, 1)
         tc::mbar_init(empty + i, 1);
       }
       tc::mbar_init(tfull, 1);
+      tc::mbar_init(tempty, 128);
       tc::fence_mbar_init();
     }
     __syncwarp();
@@ -90,68 +107,90 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (tc::elect_one()) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int st = kb % NST, ph = (kb / NST) & 1;
-        const int s = a * p.B + r0 + kb / 8, h0 = 2 * (kb % 8);
-        tc::mbar_wait(empty + st, ph ^ 1);
-        uint8_t* sa = smem + st * STAGE;
-        tc::mbar_expect_tx(full + st, STAGE);
+      int it = 0;
+      for (int a = a0; a < p.A; ++a) {
+        const int64_t kb0 = 8 * (int64_t)p.bpre[a];
+        const int64_t ss = u0 > kb0 ? u0 : kb0, se = min(u1, 8 * (int64_t)p.bpre[a + 1]);
+        if (ss >= u1) break;
+        for (int64_t u = ss; u < se; ++u, ++it) {
+          const int st = it % NST, ph = (it / NST) & 1;
+          const int kk = (int)(u - kb0), s = a * p.B + (kk >> 3), h0 = 2 * (kk & 7);
+          tc::mbar_wait(empty + st, ph ^ 1);
+          uint8_t* sa = smem + st * STAGE;
+          tc::mbar_expect_tx(full + st, STAGE);
 #pragma unroll
-        for (int kw = 0; kw < 5; ++kw) tc::tma_load_4d(sa + kw * COPY_BYTES, &mapX, full + st, 0, kw - 2, h0 - 2, s);
-        tc::tma_load_4d(sa + A_BYTES, &mapD, full + st, 0, 0, h0, s);
-        tc::tma_load_4d(sa + A_BYTES + 4096, &mapD, full + st, 32, 0, h0, s);
+          for (int kw = 0; kw < 5; ++kw) tc::tma_load_4d(sa + kw * COPY_BYTES, &mapX, full + st, 0, kw - 2, h0 - 2, s);
+          tc::tma_load_4d(sa + A_BYTES, &mapD, full + st, 0, 0, h0, s);
+          tc::tma_load_4d(sa + A_BYTES + 4096, &mapD, full + st, 32, 0, h0, s);
+        }
       }
     }
   } else if (warp == 1) {
     if (tc::elect_one()) {
       const uint32_t ones_a = tc::smem_u32(ones);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int st = kb % NST, ph = (kb / NST) & 1;
-        tc::mbar_wait(full + st, ph);
+      int it = 0, si = 0;
+      for (int a = a0; a < p.A; ++a, ++si) {
+        const int64_t kb0 = 8 * (int64_t)p.bpre[a];
+        const int64_t ss = u0 > kb0 ? u0 : kb0, se = min(u1, 8 * (int64_t)p.bpre[a + 1]);
+        if (ss >= u1) break;
+        tc::mbar_wait(tempty, (si & 1) ^ 1);  // previous segment's accumulators drained
         tc::tc_fence_after();
-        const uint32_t sa = tc::smem_u32(smem + st * STAGE);
-        const uint32_t sb = sa + A_BYTES;
+        for (int64_t u = ss; u < se; ++u, ++it) {
+          const int st = it % NST, ph = (it / NST) & 1;
+          tc::mbar_wait(full + st, ph);
+          tc::tc_fence_after();
+          const uint32_t sa = tc::smem_u32(smem + st * STAGE);
+          const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {  // 8 pixels (K rows) per MMA
-          const uint32_t acc = (kb | k) != 0;
-          const uint64_t bd = tc::sdesc(sb + k * 1024, 4096, 512, tc::kSW128_32B);
+          for (int k = 0; k < 4; ++k) {  // 8 pixels (K rows) per MMA
+            const uint32_t acc = (u != ss || k != 0) ? 1u : 0u;
+            const uint64_t bd = tc::sdesc(sb + k * 1024, 4096, 512, tc::kSW128_32B);
 #pragma unroll
-          for (int kw = 0; kw < 5; ++kw)  // tiles 0-4: taps (kh = 0..3, kw)
-            tc::mma_tf32(tbase + kw * NO, tc::sdesc(sa + kw * COPY_BYTES + k * 1024, 2048, 512, tc::kSW128_32B), bd,
+            for (int kw = 0; kw < 5; ++kw)  // tiles 0-4: taps (kh = 0..3, kw)
+              tc::mma_tf32(tbase + kw * NO, tc::sdesc(sa + kw * COPY_BYTES + k * 1024, 2048, 512, tc::kSW128_32B),
+                           bd, IDESC, acc);
+            // tile 5: taps (kh = 4, kw = 0..3); tile 6: tap (4, 4); tile 7: bias (ones)
+            tc::mma_tf32(tbase + 5 * NO, tc::sdesc(sa + 4 * 2048 + k * 1024, COPY_BYTES, 512, tc::kSW128_32B), bd,
                          IDESC, acc);
-          // tile 5: taps (kh = 4, kw = 0..3); tile 6: tap (4, 4); tile 7: bias (ones)
-          tc::mma_tf32(tbase + 5 * NO, tc::sdesc(sa + 4 * 2048 + k * 1024, COPY_BYTES, 512, tc::kSW128_32B), bd,
-                       IDESC, acc);
-          tc::mma_tf32(tbase + 6 * NO,
-                       tc::sdesc(sa + 4 * COPY_BYTES + 4 * 2048 + k * 1024, 0, 512, tc::kSW128_32B), bd, IDESC, acc);
-          tc::mma_tf32(tbase + 7 * NO, tc::sdesc(ones_a + k * 1024, 0, 512, tc::kSW128_32B), bd, IDESC, acc);
+            tc::mma_tf32(tbase + 6 * NO,
+                         tc::sdesc(sa + 4 * COPY_BYTES + 4 * 2048 + k * 1024, 0, 512, tc::kSW128_32B), bd, IDESC,
+                         acc);
+            tc::mma_tf32(tbase + 7 * NO, tc::sdesc(ones_a + k * 1024, 0, 512, tc::kSW128_32B), bd, IDESC, acc);
+          }
+          tc::mma_commit(empty + st);
         }
-        tc::mma_commit(empty + st);
+        tc::mma_commit(tfull);
       }
-      tc::mma_commit(tfull);
     }
   } else {
     const int qd = warp & 3, i = qd * 32 + lane;  // accumulator row
-    tc::mbar_wait(tfull, 0);
-    tc::tc_fence_after();
-    float* out = p.part + (int64_t)z * NROW * NO;
+    int si = 0;
+    for (int a = a0; a < p.A; ++a, ++si) {
+      const int64_t kb0 = 8 * (int64_t)p.bpre[a];
+      if ((u0 > kb0 ? u0 : kb0) >= u1) break;
+      tc::mbar_wait(tfull, si & 1);
+      tc::tc_fence_after();
+      float* out = p.part + (int64_t)(a + c) * NROW * NO;
 #pragma unroll 1
-    for (int t = 0; t < 8; ++t) {
-      int row;  // partial row = tap*32 + c, or 800 for the bias
-      if (t < 5) row = ((i >> 5) * 5 + t) * 32 + (i & 31);
-      else if (t == 5) row = (20 + (i >> 5)) * 32 + (i & 31);
-      else if (t == 6) row = qd == 0 ? 24 * 32 + lane : -1;
-      else row = i == 0 ? 800 : -1;
+      for (int t = 0; t < 8; ++t) {
+        int row;  // partial row = tap*32 + c, or 800 for the bias
+        if (t < 5) row = ((i >> 5) * 5 + t) * 32 + (i & 31);
+        else if (t == 5) row = (20 + (i >> 5)) * 32 + (i & 31);
+        else if (t == 6) row = qd == 0 ? 24 * 32 + lane : -1;
+        else row = i == 0 ? 800 : -1;
 #pragma unroll
-      for (int n0 = 0; n0 < NO; n0 += 16) {
-        float v[16];
-        tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + t * NO + n0, v);  // warp-collective
-        if (row >= 0) {
-          float4* dst = reinterpret_cast<float4*>(out + (int64_t)row * NO + n0);
+        for (int n0 = 0; n0 < NO; n0 += 16) {
+          float v[16];
+          tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + t * NO + n0, v);  // warp-collective
+          if (row >= 0) {
+            float4* dst = reinterpret_cast<float4*>(out + (int64_t)row * NO + n0);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
         }
       }
+      tc::tc_fence_before();
+      tc::mbar_arrive(tempty);
     }
   }
   tc::tc_fence_before();
@@ -160,17 +199,17 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) tc::tmem_dealloc<512>(tbase);
 }
 
-// Σ of a client's chunk partials, then SGD on conv2.w / conv2.b (a7).
-__global__ void k_dw2_reduce_sgd(const float* __restrict__ part, int nch, int rpc, const int32_t* __restrict__ bs,
-                                 const float* wsrc, int64_t wstride, float* dst, int64_t P_pad, int64_t o_w,
-                                 int64_t o_b, float lr) {
+// Σ of a client's partials (CTAs c_first..c_last, in order), then SGD on conv2.w / conv2.b.
+__global__ void k_dw2_reduce_sgd(const float* __restrict__ part, const int32_t* __restrict__ bpre, int G,
+                                 int64_t U, const float* wsrc, int64_t wstride, float* dst, int64_t P_pad,
+                                 int64_t o_w, int64_t o_b, float lr) {
   pdl_wait();  // (PDL) previous kernel's writes visible; the implicit trigger is at exit
   const int a = blockIdx.y;
-  const int nvalid = (bs[a] + rpc - 1) / rpc;
-  const float* pa = part + (int64_t)a * nch * NROW * NO;
+  const int64_t v0 = 8 * (int64_t)bpre[a], v1 = 8 * (int64_t)bpre[a + 1] - 1;  // the client's k-blocks
+  const int c0 = (int)(((v0 + 1) * G + U - 1) / U) - 1, c1 = (int)(((v1 + 1) * G + U - 1) / U) - 1;
+  const float* pa = part + (int64_t)(a + c0) * NROW * NO;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < NROW * NO; e += gridDim.x * blockDim.x) {
-    float g = 0.f;
-    g = ordered_sum(pa + e, nvalid, (int64_t)NROW * NO);
+    const float g = ordered_sum(pa + e, c1 - c0 + 1, (int64_t)NROW * NO);
     const int row = e / NO, o = e - row * NO;
     const int64_t idx = row < 800 ? o_w + (int64_t)o * 800 + row : o_b + o;
     dst[(int64_t)a * P_pad + idx] = wsrc[(int64_t)a * wstride + idx] - lr * g;
@@ -190,31 +229,28 @@ bool make_maps(CUtensorMap* mx, CUtensorMap* md, const float* p1, const float* d
 }  // namespace
 
 int conv2_dw_tc(const Layout& L, const WaveArgs& wa, const float* p1, const float* dY2, int64_t slots, float* part,
-                int64_t part_cap, int* nch_out, int* rpc_out, cudaStream_t st) {
+                int64_t part_cap, int* g_out, cudaStream_t st) {
   CUtensorMap mx, md;
   if (!make_maps(&mx, &md, p1, dY2, slots)) return -1;
-  // split-K over sample chunks so the grid covers ~2 CTAs per SM
-  int nch = (2 * 148 + wa.A - 1) / wa.A;
-  nch = nch < 1 ? 1 : (nch > wa.B ? wa.B : nch);
-  const int rpc = (wa.B + nch - 1) / nch;
-  nch = (wa.B + rpc - 1) / rpc;
-  if ((int64_t)wa.A * nch > part_cap) return -1;
+  // one CTA per SM (512 TMEM columns each), every CTA at least one sample of work
+  const int64_t U = 8 * wa.sum_bs;
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(148, wa.sum_bs));
+  if ((int64_t)wa.A + G > part_cap) return -1;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_conv2_dw_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     attr = true;
   }
-  DwArgs p{wa.bs, wa.B, nch, rpc, part};
-  launch_pdl(wa.pdl, k_conv2_dw_tc, dim3(nch, wa.A), 192, SMEM, st, mx, md, p);
-  *nch_out = nch;
-  *rpc_out = rpc;
+  DwArgs p{wa.bpre, wa.A, wa.B, G, U, part};
+  launch_pdl(wa.pdl, k_conv2_dw_tc, dim3(G), 192, SMEM, st, mx, md, p);
+  *g_out = G;
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
 int conv2_dw_reduce_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wsrc_stride, float* dst,
-                       const float* part, int nch, int rpc, cudaStream_t st) {
-  launch_pdl(wa.pdl, k_dw2_reduce_sgd, dim3((NROW * NO + 255) / 256, wa.A), 256, 0, st, part, nch, rpc, wa.bs, wsrc, wsrc_stride,
-                                                                       dst, L.P_pad, L.o_c2w, L.o_c2b, wa.lr);
+                       const float* part, int G, cudaStream_t st) {
+  launch_pdl(wa.pdl, k_dw2_reduce_sgd, dim3((NROW * NO + 255) / 256, wa.A), 256, 0, st, part, wa.bpre, G,
+             (int64_t)8 * wa.sum_bs, wsrc, wsrc_stride, dst, L.P_pad, L.o_c2w, L.o_c2b, wa.lr);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

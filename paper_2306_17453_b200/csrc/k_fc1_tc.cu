@@ -361,6 +361,242 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) tc::tmem_dealloc<DW_N>(tbase);
 }
 
+// ------------------------------------------------------------------ fused dX + dW + SGD
+// Persistent over (client, 128-column k panel of W1) tiles; a panel is streamed in 4 chunks
+// of 128 rows (n).  Each chunk (64 KB, SWIZZLE_128B_ATOM_32B, so it is directly the MN-major
+// A operand of the dX MMA) is read from HBM once: the dX MMAs accumulate
+// dp2[k][r] += Σ_n W1[n][k] dh[r][n] from the OLD values, the dW MMAs produce
+// G[n][k] = Σ_r dh[r][n] p2[r][k] into a double-buffered TMEM tile, and only after both
+// complete does the epilogue apply W1 <- W1 − η·G in shared memory and TMA-store the chunk.
+// W1 is read once and written once per client step (separate dX / dW kernels read it
+// twice).  After a panel's last chunk the epilogue routes dp2 through pool2's argmax / ReLU'
+// into dY2.  The stage ring, the G buffers and the two dX accumulators run across tiles.
+constexpr int BW_W = 4 * 128 * 128;               // 4 k-chunks x [128 n][32 k]
+constexpr int BW_DH = 4 * NB * 128;               // dh, 4 boxes [32 r][32 n] (SW128: K-major B of dX)
+constexpr int BW_DHT = 4 * NB * 128;              // dhᵀ, 4 chunks [32 r][32 n] (ATOM_32B: MN-major A of dW)
+constexpr int BW_STAGE = BW_W + BW_DH + BW_DHT;   // 96 KB
+constexpr int BW_NST = 2;
+constexpr int BW_P2B = 4 * NB * 128;              // p2ᵀ panel, 4 chunks [32 r][32 k] (MN-major B of dW)
+constexpr int BW_P2 = BW_NST * BW_STAGE;          // two panels (double-buffered across tiles)
+constexpr int BW_BAR = BW_P2 + 2 * BW_P2B;
+constexpr int BW_SMEM = BW_BAR + 256 + 1024;
+constexpr uint32_t BW_TCOLS = 512;                // G [0,128) [128,256); dX [256,288) [288,320)
+
+struct BwArgs {
+  const int32_t* bs;
+  int A, B, HID, F, wmul;
+  int H2, W2, C2;
+  const float* p2;
+  const uint8_t* am2;
+  float* dY2;
+  const float* bsrc;   // client 0 bias (θ_g on the first wave); client a at + a*bstride
+  int64_t bstride;
+  float* bdst;         // slot 0 bias; client a at + a*P_pad
+  int64_t P_pad;
+  const float* dh;     // [S][HID]
+  float lr;
+};
+
+__global__ void __launch_bounds__(192, 1)
+    k_fc1_bwd_tc(const __grid_constant__ CUtensorMap mapWsrc, const __grid_constant__ CUtensorMap mapWdst,
+                 const __grid_constant__ CUtensorMap mapDh, const __grid_constant__ CUtensorMap mapDht,
+                 const __grid_constant__ CUtensorMap mapX, BwArgs p) {
+  constexpr uint32_t IDESC_DX = tc::idesc_tf32(128, NB, 1, 0);   // A (W1ᵀ) MN-major, B (dh) K-major
+  constexpr uint32_t IDESC_DW = tc::idesc_tf32(128, 128, 1, 1);  // A (dhᵀ), B (p2ᵀ) MN-major
+  const int KT = p.F / 128, T = p.A * KT, nch = p.HID / 128;
+  pdl_wait();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + BW_BAR);
+  uint64_t* empty = full + BW_NST;
+  uint64_t* gfull = empty + BW_NST;
+  uint64_t* gempty = gfull + 2;
+  uint64_t* p2full = gempty + 2;    // [2]
+  uint64_t* p2empty = p2full + 2;   // [2]
+  uint64_t* dxfull = p2empty + 2;   // [2]
+  uint64_t* dxempty = dxfull + 2;   // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dxempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::prefetch_tmap(&mapWsrc);
+      tc::prefetch_tmap(&mapWdst);
+      tc::prefetch_tmap(&mapDh);
+      tc::prefetch_tmap(&mapDht);
+      tc::prefetch_tmap(&mapX);
+      for (int i = 0; i < BW_NST; ++i) {
+        tc::mbar_init(full + i, 1);
+        tc::mbar_init(empty + i, 1);
+      }
+      for (int i = 0; i < 2; ++i) {
+        tc::mbar_init(gfull + i, 1);
+        tc::mbar_init(gempty + i, 128);
+        tc::mbar_init(p2full + i, 1);
+        tc::mbar_init(p2empty + i, 1);
+        tc::mbar_init(dxfull + i, 1);
+        tc::mbar_init(dxempty + i, 128);
+      }
+      tc::fence_mbar_init();
+    }
+    __syncwarp();
+    tc::tmem_alloc<BW_TCOLS>(tslot);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  if (warp == 0) {
+    // ---------------- producer
+    if (tc::elect_one()) {
+      int it = 0, ti = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x) {
+        const int a = t / KT, kt = t % KT;
+        if (p.bs[a] == 0) continue;
+        const int pb = ti & 1, pph = (ti >> 1) & 1;
+        ++ti;
+        tc::mbar_wait(p2empty + pb, pph ^ 1);
+        tc::mbar_expect_tx(p2full + pb, BW_P2B);
+        tc::tma_load_3d(smem + BW_P2 + pb * BW_P2B, &mapX, p2full + pb, 0, a * p.B, 4 * kt);
+        for (int c = 0; c < nch; ++c, ++it) {
+          const int st = it % BW_NST, ph = (it / BW_NST) & 1;
+          tc::mbar_wait(empty + st, ph ^ 1);
+          uint8_t* sw = smem + st * BW_STAGE;
+          tc::mbar_expect_tx(full + st, BW_STAGE);
+          for (int j = 0; j < 4; ++j)
+            tc::tma_load_3d(sw + j * 16384, &mapWsrc, full + st, 128 * kt + 32 * j, 128 * c, a * p.wmul);
+          for (int j = 0; j < 4; ++j)
+            tc::tma_load_3d(sw + BW_W + j * 4096, &mapDh, full + st, 128 * c + 32 * j, a * p.B, 0);
+          tc::tma_load_3d(sw + BW_W + BW_DH, &mapDht, full + st, 0, a * p.B, 4 * c);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (tc::elect_one()) {
+      int it = 0, ti = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x) {
+        const int a = t / KT;
+        if (p.bs[a] == 0) continue;
+        const int pb = ti & 1, pph = (ti >> 1) & 1;
+        ++ti;
+        tc::mbar_wait(p2full + pb, pph);
+        tc::mbar_wait(dxempty + pb, pph ^ 1);  // dX accumulator pb drained by the epilogue
+        const uint32_t up2 = tc::smem_u32(smem + BW_P2 + pb * BW_P2B);
+        const uint32_t tdx = tbase + 256 + pb * 32;
+        for (int c = 0; c < nch; ++c, ++it) {
+          const int st = it % BW_NST, ph = (it / BW_NST) & 1, buf = it & 1, gph = (it >> 1) & 1;
+          tc::mbar_wait(full + st, ph);
+          tc::mbar_wait(gempty + buf, gph ^ 1);
+          tc::tc_fence_after();
+          const uint32_t uw = tc::smem_u32(smem + st * BW_STAGE), udh = uw + BW_W, udht = udh + BW_DH;
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk)  // dX: K = this chunk's 128 n, 8 per MMA
+            tc::mma_tf32(tdx, tc::sdesc(uw + kk * 1024, 16384, 512, tc::kSW128_32B),
+                         tc::sdesc(udh + (kk >> 2) * 4096 + (kk & 3) * 32, 0, 1024, tc::kSW128), IDESC_DX,
+                         (c | kk) != 0);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)      // dW: K = 32 batch slots
+            tc::mma_tf32(tbase + buf * 128, tc::sdesc(udht + k * 1024, NB * 128, 512, tc::kSW128_32B),
+                         tc::sdesc(up2 + k * 1024, NB * 128, 512, tc::kSW128_32B), IDESC_DW, k != 0);
+          tc::mma_commit(gfull + buf);
+        }
+        tc::mma_commit(p2empty + pb);
+        tc::mma_commit(dxfull + pb);
+      }
+    }
+  } else {
+    // ---------------- epilogue (thread = n row of the chunk for G; = k row of the panel for dX)
+    const int qd = warp & 3, row = qd * 32 + lane;
+    int it = 0, ti = 0;
+    for (int t = blockIdx.x; t < T; t += gridDim.x) {
+      const int a = t / KT, kt = t % KT;
+      const int bs = p.bs[a];
+      if (bs == 0) continue;
+      const int pb = ti & 1, pph = (ti >> 1) & 1;
+      ++ti;
+      // pool2 state of this thread's dX row: independent of the MMAs, fetched up front
+      const int k = kt * 128 + row;
+      bool pos[NB];
+      uint8_t amr[NB];
+#pragma unroll
+      for (int r = 0; r < NB; ++r) {
+        const int64_t s = (int64_t)a * p.B + r;
+        pos[r] = r < bs ? p.p2[s * p.F + k] > 0.f : false;
+        amr[r] = r < bs ? p.am2[s * p.F + k] : 0;
+      }
+      for (int c = 0; c < nch; ++c, ++it) {
+        const int st = it % BW_NST, buf = it & 1, gph = (it >> 1) & 1;
+        uint8_t* sw = smem + st * BW_STAGE;
+        tc::mbar_wait(gfull + buf, gph);
+        tc::tc_fence_after();
+        for (int j = 0; j < 4; ++j) {
+          float v[32];
+          const uint32_t tg = tbase + ((uint32_t)(qd * 32) << 16) + buf * 128 + 32 * j;
+          tc::tmem_ld16(tg, *reinterpret_cast<float(*)[16]>(v));
+          tc::tmem_ld16(tg + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+          uint8_t* rowp = sw + j * 16384 + row * 128;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {  // 32-byte granule g of the row sits at g ^ (row % 4) (ATOM_32B)
+            float4* w4 = reinterpret_cast<float4*>(rowp + ((g ^ (row & 3)) << 5));
+#pragma unroll
+            for (int hq = 0; hq < 2; ++hq) {
+              float4 w = w4[hq];
+              w.x -= p.lr * v[8 * g + 4 * hq];
+              w.y -= p.lr * v[8 * g + 4 * hq + 1];
+              w.z -= p.lr * v[8 * g + 4 * hq + 2];
+              w.w -= p.lr * v[8 * g + 4 * hq + 3];
+              w4[hq] = w;
+            }
+          }
+        }
+        tc::tc_fence_before();
+        tc::mbar_arrive(gempty + buf);  // G buffer drained
+        if (kt == 0) {  // bias: b1[n] -= η Σ_r dh[r][n], from the stage's dhᵀ chunk (ATOM_32B)
+          const int n = 128 * c + row, nn = row & 31;
+          const uint8_t* dq = sw + BW_W + BW_DH + (row >> 5) * 4096 + (nn & 7) * 4;
+          float g = 0.f;
+          for (int r = 0; r < bs; ++r) g += *reinterpret_cast<const float*>(dq + r * 128 + (((nn >> 3) ^ (r & 3)) << 5));
+          p.bdst[(int64_t)a * p.P_pad + n] = p.bsrc[(int64_t)a * p.bstride * p.wmul + n] - p.lr * g;
+        }
+        tc::fence_async_smem();  // generic-proxy writes -> TMA store
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 2 && tc::elect_one()) {
+          for (int j = 0; j < 4; ++j) tc::tma_store_3d(&mapWdst, sw + j * 16384, 128 * kt + 32 * j, 128 * c, a);
+          tc::tma_store_commit_wait();  // the stage may be refilled once the store has read it
+          tc::mbar_arrive(empty + st);
+        }
+      }
+      // dX epilogue: dp2 -> pool2 / ReLU backward -> dY2 (every cell of the 2x2 window written)
+      tc::mbar_wait(dxfull + pb, pph);
+      tc::tc_fence_after();
+      float v[NB];
+      const uint32_t tdx = tbase + ((uint32_t)(qd * 32) << 16) + 256 + pb * 32;
+      tc::tmem_ld16(tdx, *reinterpret_cast<float(*)[16]>(v));
+      tc::tmem_ld16(tdx + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+      tc::tc_fence_before();
+      tc::mbar_arrive(dxempty + pb);
+      const int cc = k % p.C2, pw = (k / p.C2) % p.W2, ph = k / (p.C2 * p.W2);
+      const int W1 = 2 * p.W2, H1 = 2 * p.H2;
+#pragma unroll
+      for (int r = 0; r < NB; ++r) {
+        if (r >= bs) break;
+        const int64_t s = (int64_t)a * p.B + r;
+        const float g = pos[r] ? v[r] : 0.f;
+        const int am = amr[r];
+        float* d = p.dY2 + ((s * H1 + 2 * ph) * W1 + 2 * pw) * p.C2 + cc;
+        d[0] = am == 0 ? g : 0.f;
+        d[p.C2] = am == 1 ? g : 0.f;
+        d[(int64_t)W1 * p.C2] = am == 2 ? g : 0.f;
+        d[(int64_t)W1 * p.C2 + p.C2] = am == 3 ? g : 0.f;
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  pdl_trigger();
+  if (warp == 0) tc::tmem_dealloc<BW_TCOLS>(tbase);
+}
+
 template <class K>
 void set_smem(K k, int bytes, bool& done) {
   if (!done) {
@@ -457,6 +693,38 @@ int fc1_dw_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wc
   DwArgs p{wa.bs, wa.B, d.HID, d.F, ntiles, wa.first ? 0 : 1, wsrc + L.o_f1b, L.P_pad, slots_w + L.o_f1b,
            L.P_pad, dh, wa.lr};
   launch_pdl(wa.pdl, k_fc1_dw_tc, dim3(mtiles * ntiles, wa.A), 192, DW_SMEM, st, mh, mx, mws, mwd, p);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+// fused dX + dW + SGD (one W1 pass): dh -> dY2 (pool2 / ReLU backward), W1, b1 updated
+int fc1_bwd_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wclients_src, float* slots_w,
+               int64_t wclients_dst, const float* dh, const float* p2, const uint8_t* am2, int64_t slots, float* dY2,
+               cudaStream_t st) {
+  const CnnDims& d = L.d;
+  CUtensorMap mws, mwd, mdh, mdht, mx;
+  uint64_t dws[3] = {(uint64_t)d.F, (uint64_t)d.HID, (uint64_t)wclients_src};
+  uint64_t dwd[3] = {(uint64_t)d.F, (uint64_t)d.HID, (uint64_t)wclients_dst};
+  uint64_t sww[2] = {(uint64_t)d.F * 4, (uint64_t)L.P_pad * 4};
+  uint32_t bww[3] = {32, 128, 1};
+  uint64_t dd[3] = {(uint64_t)d.HID, (uint64_t)slots, 1};
+  uint64_t sd[2] = {(uint64_t)d.HID * 4, (uint64_t)d.HID * 4 * slots};
+  uint32_t bd[3] = {32, NB, 1};
+  uint64_t dh3[3] = {32, (uint64_t)slots, (uint64_t)d.HID / 32};
+  uint64_t sh3[2] = {(uint64_t)d.HID * 4, 128};
+  uint32_t bh3[3] = {32, NB, 4};
+  uint64_t dx3[3] = {32, (uint64_t)slots, (uint64_t)d.F / 32};
+  uint64_t sx3[2] = {(uint64_t)d.F * 4, 128};
+  uint32_t bx3[3] = {32, NB, 4};
+  if (!tmap_encode(&mws, wsrc + L.o_f1w, 3, dws, sww, bww, 2) || !tmap_encode(&mwd, slots_w + L.o_f1w, 3, dwd, sww, bww, 2) ||
+      !tmap_encode(&mdh, dh, 3, dd, sd, bd, 1) || !tmap_encode(&mdht, dh, 3, dh3, sh3, bh3, 2) ||
+      !tmap_encode(&mx, p2, 3, dx3, sx3, bx3, 2))
+    return -1;
+  static bool attr = false;
+  set_smem(k_fc1_bwd_tc, BW_SMEM, attr);
+  BwArgs p{wa.bs, wa.A, wa.B, d.HID, d.F, wa.first ? 0 : 1, d.H2, d.W2, d.C2, p2, am2, dY2,
+           wsrc + L.o_f1b, L.P_pad, slots_w + L.o_f1b, L.P_pad, dh, wa.lr};
+  const int tiles = wa.A * (d.F / 128);
+  launch_pdl(wa.pdl, k_fc1_bwd_tc, dim3(tiles < 148 ? tiles : 148), 192, BW_SMEM, st, mws, mwd, mdh, mdht, mx, p);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
