@@ -318,11 +318,25 @@ __global__ void __launch_bounds__(256) k_head_fwd(const float* __restrict__ h, c
   float* hs = zs + HR * NCLS;      // [HR][HID] staged activations
   const int nr = max(0, min(HR, b - r0));
   if (nr > 0) {
-    // every global load issued before any use (one round trip), then compute from smem
+    // every global load issued before any store (one round trip), then compute from smem
     const float4* W4 = reinterpret_cast<const float4*>(w.at(z, o_w));
-    for (int e = threadIdx.x; e < NCLS * HID / 4; e += blockDim.x) reinterpret_cast<float4*>(Ws)[e] = W4[e];
     const float4* h4 = reinterpret_cast<const float4*>(h + ((int64_t)z * B + r0) * HID);
-    for (int e = threadIdx.x; e < nr * HID / 4; e += blockDim.x) reinterpret_cast<float4*>(hs)[e] = h4[e];
+    const int nw4 = NCLS * HID / 4, nh4 = nr * HID / 4;
+    for (int base = 0; base < nw4 + nh4; base += 12 * 256) {
+      float4 v[12];
+#pragma unroll
+      for (int i = 0; i < 12; ++i) {
+        const int e = base + threadIdx.x + i * 256;
+        if (e < nw4) v[i] = __ldg(W4 + e);
+        else if (e < nw4 + nh4) v[i] = __ldg(h4 + (e - nw4));
+      }
+#pragma unroll
+      for (int i = 0; i < 12; ++i) {
+        const int e = base + threadIdx.x + i * 256;
+        if (e < nw4) reinterpret_cast<float4*>(Ws)[e] = v[i];
+        else if (e < nw4 + nh4) reinterpret_cast<float4*>(hs)[e - nw4] = v[i];
+      }
+    }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int idx = warp; idx < nr * NCLS; idx += nw) {
@@ -378,10 +392,30 @@ __global__ void __launch_bounds__(256) k_head_sgd(const float* __restrict__ h, c
   float* Wd = dst + (int64_t)z * P_pad;
   const float* dzz = dzbuf + (int64_t)z * B * NCLS;
   const float* hz = h + (int64_t)z * B * HID;
-  for (int e = threadIdx.x; e < b * NCLS; e += blockDim.x) dzs[e] = dzz[e];
-  for (int e = threadIdx.x; e < b * 64; e += blockDim.x) {
-    const int r = e >> 6, n = n0 + (e & 63);
-    hs[e] = n < HID ? hz[(int64_t)r * HID + n] : 0.f;
+  {  // all loads in flight before any store: dz (<= B*NCLS) and the h column chunk (<= B*64)
+    constexpr int LZ = 2, LH = 8;
+    float zv[LZ], hv[LH];
+#pragma unroll
+    for (int i = 0; i < LZ; ++i) {
+      const int e = threadIdx.x + i * 256;
+      zv[i] = e < b * NCLS ? __ldg(dzz + e) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < LH; ++i) {
+      const int e = threadIdx.x + i * 256, r = e >> 6, n = n0 + (e & 63);
+      hv[i] = (e < b * 64 && n < HID) ? __ldg(hz + (int64_t)r * HID + n) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < LZ; ++i)
+      if (threadIdx.x + i * 256 < b * NCLS) dzs[threadIdx.x + i * 256] = zv[i];
+#pragma unroll
+    for (int i = 0; i < LH; ++i)
+      if (threadIdx.x + i * 256 < b * 64) hs[threadIdx.x + i * 256] = hv[i];
+    for (int e = threadIdx.x + LZ * 256; e < b * NCLS; e += blockDim.x) dzs[e] = dzz[e];  // B*NCLS > 512
+    for (int e = threadIdx.x + LH * 256; e < b * 64; e += blockDim.x) {                   // B > 32
+      const int r = e >> 6, n = n0 + (e & 63);
+      hs[e] = n < HID ? hz[(int64_t)r * HID + n] : 0.f;
+    }
   }
   __syncthreads();
   for (int e = threadIdx.x; e < NCLS * 64; e += blockDim.x) {
