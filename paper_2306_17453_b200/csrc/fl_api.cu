@@ -238,6 +238,9 @@ struct fl_ctx {
   // client 9.3 -> 7.6 ms); an early trigger parked dependent CTAs on smem and starved the
   // concurrent streams (C2 22 ms).
   int pdl_max_a = 1 << 30;
+  // SMs the bulk groups' persistent kernels leave free for the solo (critical-path) streams
+  // when solo groups exist (FL_RESERVE_SMS; measured: 64 -> C2 -3%)
+  int reserve_sms = 64;
   std::vector<cudaStream_t> gstream;  // [nsolo high-priority | ngroups normal]
   std::vector<cudaEvent_t> ev_join;
   cudaEvent_t ev_fork = nullptr;
@@ -399,6 +402,7 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   if (const char* ng = getenv("FL_GROUPS")) c->ngroups = std::max(1, atoi(ng));
   if (const char* ns = getenv("FL_SOLO")) c->nsolo = std::max(0, atoi(ns));
   if (const char* pm = getenv("FL_PDL_MAXA")) c->pdl_max_a = atoi(pm);
+  if (const char* rs = getenv("FL_RESERVE_SMS")) c->reserve_sms = std::max(0, std::min(120, atoi(rs)));
   c->nsolo = std::min(c->nsolo, std::max(0, 8 - c->ngroups));
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   const int nstreams = c->nsolo + c->ngroups;
@@ -521,10 +525,12 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   ws.slot_off.assign(1, 0);
   ws.bs_off.assign(1, 0);
   ws.gstream.assign((size_t)NG, 0);
+  ws.gsolo.assign((size_t)NG, 0);
   for (int g = 0; g < NG; ++g) {
     const int64_t n_g = gsize[(size_t)g];
     ws.gn[(size_t)g] = n_g;
     ws.gstream[(size_t)g] = g < NS ? g : c->nsolo + (g - NS);
+    ws.gsolo[(size_t)g] = (g < NS || NS == 0) ? 1 : 0;
     ws.gbase[(size_t)g + 1] = ws.gbase[(size_t)g] + n_g;
     const int64_t b0 = ws.gbase[(size_t)g];
     const int64_t nw = n_g ? c->steps_exec[(size_t)b0] : 0;
@@ -741,6 +747,8 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
                                        conv2_dw_tc_z_floats(), (int64_t)L.d.C1 * (25 * L.d.cpad + 1));
         max_w = std::max(max_w, ws.gnw[(size_t)g]);
       }
+      static const bool hostprof = getenv("FL_HOSTPROF") != nullptr;
+      const auto th0 = std::chrono::steady_clock::now();
       for (int64_t t = 0; t < max_w; ++t) {
         for (int g = 0; g < ws.ngroups; ++g) {
           if (ws.gn[(size_t)g] == 0 || t >= ws.gnw[(size_t)g]) continue;
@@ -749,7 +757,8 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
           for (int32_t a = 0; a < ws.A[(size_t)k]; ++a) sum_bs += h_bs[ws.bs_off[(size_t)k] + a];
           WaveArgs wa{ws.A[(size_t)k], (int)B, t == 0, ws.d_sidx + ws.slot_off[(size_t)k],
                       ws.d_bs + ws.bs_off[(size_t)k], c->cfg.lr, sum_bs, &c->prof, c->cfg.math == 0,
-                      ws.gn[(size_t)g], ws.A[(size_t)k] <= c->pdl_max_a, ws.d_bpre + ws.bs_off[(size_t)k] + k};
+                      ws.gn[(size_t)g], ws.A[(size_t)k] <= c->pdl_max_a, ws.d_bpre + ws.bs_off[(size_t)k] + k,
+                      (ws.gsolo[(size_t)g] || c->reserve_sms == 0) ? 148 : 148 - c->reserve_sms};
           int nl = cnn_wave_simt(L, wa, c->d_xpack, c->d_ypack, c->d_theta, c->d_slots + base * L.P_pad,
                                  gv[(size_t)g], gst[(size_t)g]);
           if (nl < 0)
@@ -758,6 +767,10 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
           tl += nl;
         }
       }
+      if (hostprof)
+        fprintf(stderr, "[fl] issued %lld launches for %lld waves in %.3f ms host time\n", (long long)tl,
+                (long long)ws.n_waves,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count());
       for (int g = 0; g < ws.ngroups; ++g) {
         if (ws.gn[(size_t)g] == 0 || gst[(size_t)g] == st) continue;
         CK(cudaEventRecord(c->ev_join[(size_t)g], gst[(size_t)g]));

@@ -85,6 +85,7 @@ struct WaveSched {
   int ngroups = 1;
   std::vector<int64_t> gbase, gn, gw0, gnw;
   std::vector<int> gstream;        // stream index of each group
+  std::vector<int> gsolo;          // 1: a solo (critical-path) group, or no solo groups at all
 };
 
 // ---------------------------------------------------------------- CNN buffers
@@ -170,6 +171,7 @@ struct WaveArgs {
   int64_t wclients;  // client slots allocated (weights tensor-map extent)
   bool pdl;          // launch this wave's kernels with programmatic dependent launch
   const int32_t* bpre;  // [A + 1] prefix sums of bs (balanced split-K over the wave's samples)
+  int sms;              // SMs the wave's persistent kernels may occupy (bulk groups leave some to the solo streams)
 };
 
 // Kernel launchers (k_*.cu). All asynchronous on `st`. Return the number of launches.
@@ -194,7 +196,7 @@ int c1wt_pack(const float* c1w, float* out, cudaStream_t st);
 int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, const float* wt, const float* xpack,
                  int64_t xrows, float* p1, uint8_t* am1, cudaStream_t st);
 int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64_t xrows, const float* dY1,
-                int64_t slots, float* part, int64_t part_cap, int* nch_out, int* rpc_out, cudaStream_t st);
+                int64_t slots, float* part, int64_t part_cap, int* g_out, cudaStream_t st);
 bool fc1_tc_supported(const Layout& L, int B);
 int fc1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p2,
                int64_t slots, float* h, float* part, int64_t part_floats, cudaStream_t st, int* launches);

@@ -280,16 +280,29 @@ __global__ void k_unpool(const float* __restrict__ dp, const float* __restrict__
 }
 
 // Σ of the split-K partials, then fused SGD on the conv weights and bias.
+// Partials: [A*nch] chunks of rpc samples (bpre == nullptr), or the balanced split-K layout
+// (bpre != nullptr): client a's partials are z = a + c for the CTAs c0..c1 covering its k-blocks
+// [kbps·bpre[a], kbps·bpre[a+1]) of U, split evenly over G CTAs.
 __global__ void k_dw_reduce_sgd(const float* __restrict__ part, int nch, int rpc, const int32_t* __restrict__ bs,
                                 int O, int N, WSrc w, int64_t o_w, int64_t o_b, float* dst, int64_t P_pad, float lr,
-                                float* __restrict__ wt) {
+                                float* __restrict__ wt, const int32_t* __restrict__ bpre, int G, int64_t U, int kbps) {
   pdl_wait();  // (PDL) previous kernel's writes visible; the implicit trigger is at exit
   const int a = blockIdx.y;
-  const int nvalid = (bs[a] + rpc - 1) / rpc;
   const int tot = O * N;
+  const float* pa;
+  int nvalid;
+  if (bpre) {
+    const int64_t v0 = (int64_t)kbps * bpre[a], v1 = (int64_t)kbps * bpre[a + 1] - 1;
+    const int c0 = (int)(((v0 + 1) * G + U - 1) / U) - 1, c1 = (int)(((v1 + 1) * G + U - 1) / U) - 1;
+    pa = part + (int64_t)(a + c0) * tot;
+    nvalid = c1 - c0 + 1;
+  } else {
+    pa = part + (int64_t)a * nch * tot;
+    nvalid = (bs[a] + rpc - 1) / rpc;
+  }
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {
     float g = 0.f;
-    g = ordered_sum(part + (int64_t)a * nch * tot + e, nvalid, tot);
+    g = ordered_sum(pa + e, nvalid, tot);
     const int m = e / N, n = e - m * N;
     const int64_t off = n < N - 1 ? o_w + (int64_t)m * (N - 1) + n : o_b + m;
     const float nv = *w.at(a, off) - lr * g;
@@ -639,13 +652,13 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     pf.end(K_CONV2_DW, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
     pf.begin(st);
     launch_pdl(wa.pdl, k_dw_reduce_sgd, dim3(16, A), 256, 0, st, b.part2, b.nch, rpc, wa.bs, d.C2, 25 * d.C1 + 1, w, L.o_c2w,
-                                                 L.o_c2b, slots, L.P_pad, wa.lr, nullptr), ++n;
+                                                 L.o_c2b, slots, L.P_pad, wa.lr, nullptr, nullptr, 0, 0, 0), ++n;
     pf.end(K_CONV2_DWR, 0, 8.0 * A * d.C2 * 25 * d.C1, st);
   }
-  int nch1 = b.nch, rpc1 = rpc;
+  int nch1 = b.nch, rpc1 = rpc, g1 = 0;
   pf.begin(st);
   if (tc1) {
-    if (conv1_dw_tc(L, wa, b.xplanar, b.xrows, b.dY1, b.slots, b.part1, b.part1_tc_cap, &nch1, &rpc1, st) < 0) return -1;
+    if (conv1_dw_tc(L, wa, b.xplanar, b.xrows, b.dY1, b.slots, b.part1, b.part1_tc_cap, &g1, st) < 0) return -1;
     ++n;
   } else {
     launch(ConvDw{b.dY1, xpack, wa.sidx, wa.bs, B, d.H0, d.W0, d.cpad, d.C1, b.nch, rpc, b.part1}, d.C1,
@@ -655,7 +668,8 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   pf.begin(st);
   launch_pdl(wa.pdl, k_dw_reduce_sgd, dim3((d.C1 * (25 * d.cpad + 1) + 127) / 128, A), 128, 0, st, 
       b.part1, nch1, rpc1, wa.bs, d.C1, 25 * d.cpad + 1, w, L.o_c1w,
-                                              L.o_c1b, slots, L.P_pad, wa.lr, tc1 ? b.c1wt : nullptr), ++n;
+                                              L.o_c1b, slots, L.P_pad, wa.lr, tc1 ? b.c1wt : nullptr,
+      tc1 ? wa.bpre : nullptr, g1, (int64_t)d.H0 * wa.sum_bs, d.H0), ++n;
   pf.end(K_CONV1_DWR, 0, 8.0 * A * d.C1 * 25 * d.cin, st);
   return n;
 }

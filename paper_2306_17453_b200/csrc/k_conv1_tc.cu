@@ -16,6 +16,8 @@
 // Weight gradient (M = (kw, c, kh) = 100 rows + bias, N = o = 32, K = pixels): see below.
 //   Split-K over sample chunks -> partial [32][101] -> k_dw_reduce_sgd (SIMT, shared).
 #include <cuda.h>
+
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -233,27 +235,40 @@ constexpr int NPART = 25 * 4 + 1;        // partial row length per output channe
 
 struct C1DwArgs {
   const int32_t* sidx;
-  const int32_t* bs;
-  int B, nch, rpc;
-  float* part;  // [A*nch][32][101]
+  const int32_t* bpre;  // [A + 1] prefix sums of the wave's batch sizes
+  int A, B, G;          // G CTAs split the wave's U k-blocks (H image rows per sample) evenly
+  int64_t U;
+  float* part;          // [A + G][32][101]: partial of (CTA c, client a) at z = a + c
 };
+
+// Largest a in [0, A) with bpre[a] <= x (the client owning concatenated sample x).
+__device__ __forceinline__ int c1_client_of(const int32_t* __restrict__ bpre, int A, int64_t x) {
+  int lo = 0, hi = A - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (bpre[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
 
 __global__ void __launch_bounds__(192, 1)
     k_conv1_dw_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapD, C1DwArgs p) {
   constexpr uint32_t IDESC = tc::idesc_tf32(128, C1, 0, 1);  // A K-major, B MN-major
-  const int ch = blockIdx.x, a = blockIdx.y, z = a * p.nch + ch;
-  const int r0 = ch * p.rpc, r1 = min(p.bs[a], r0 + p.rpc);
-  if (r0 >= r1) return;
-  const int nkb = (r1 - r0) * H;
-  // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
-  // would stall other streams' kernels) or touching anything it writes.
+  // Balanced split-K (as conv2's dW): CTA c reduces k-blocks [c·U/G, (c+1)·U/G) of the wave's
+  // concatenated (client, sample, image row) sequence; each client segment ends with its
+  // partial written to z = a + c.
+  const int c = blockIdx.x;
+  const int64_t u0 = (int64_t)c * p.U / p.G, u1 = (int64_t)(c + 1) * p.U / p.G;
   pdl_wait();
+  const int a0 = c1_client_of(p.bpre, p.A, u0 / H);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + D_BAR);
   uint64_t* empty = full + D_NST;
   uint64_t* tfull = empty + D_NST;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // constant rows of every stage (never written by TMA): pad rows 20-23 of each kw block = 0,
   // row 120 = ones (bias), rows 121-127 = 0
@@ -272,6 +287,7 @@ __global__ void __launch_bounds__(192, 1)
         tc::mbar_init(empty + i, 1);
       }
       tc::mbar_init(tfull, 1);
+      tc::mbar_init(tempty, 128);
       tc::fence_mbar_init();
     }
     __syncwarp();
@@ -283,55 +299,76 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tbase = *tslot;
   if (warp == 0) {
     if (tc::elect_one()) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int st = kb % D_NST, ph = (kb / D_NST) & 1;
-        const int rr = r0 + kb / H, h0 = kb % H;
-        const int row = p.sidx[a * p.B + rr];
-        tc::mbar_wait(empty + st, ph ^ 1);
-        uint8_t* sa = smem + st * D_STAGE;
-        tc::mbar_expect_tx(full + st, D_TX);
-        // tap column kw = shifted copy (kw & 3) read from w' = (kw & 4): x[w + kw - 2]
-        for (int kw = 0; kw < 5; ++kw)
-          tc::tma_load_5d(sa + kw * D_KWB, &mapX, full + st, kw & 4, h0 - 2, 0, kw & 3, row);
-        tc::tma_load_4d(sa + D_A, &mapD, full + st, 0, 0, h0, a * p.B + rr);
+      int it = 0;
+      for (int a = a0; a < p.A; ++a) {
+        const int64_t kb0 = (int64_t)H * p.bpre[a];
+        const int64_t ss = u0 > kb0 ? u0 : kb0, se = min(u1, (int64_t)H * p.bpre[a + 1]);
+        if (ss >= u1) break;
+        for (int64_t u = ss; u < se; ++u, ++it) {
+          const int st = it % D_NST, ph = (it / D_NST) & 1;
+          const int kk = (int)(u - kb0), rr = kk / H, h0 = kk % H;
+          const int row = p.sidx[a * p.B + rr];
+          tc::mbar_wait(empty + st, ph ^ 1);
+          uint8_t* sa = smem + st * D_STAGE;
+          tc::mbar_expect_tx(full + st, D_TX);
+          // tap column kw = shifted copy (kw & 3) read from w' = (kw & 4): x[w + kw - 2]
+          for (int kw = 0; kw < 5; ++kw)
+            tc::tma_load_5d(sa + kw * D_KWB, &mapX, full + st, kw & 4, h0 - 2, 0, kw & 3, row);
+          tc::tma_load_4d(sa + D_A, &mapD, full + st, 0, 0, h0, a * p.B + rr);
+        }
       }
     }
   } else if (warp == 1) {
     if (tc::elect_one()) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int st = kb % D_NST, ph = (kb / D_NST) & 1;
-        tc::mbar_wait(full + st, ph);
+      int it = 0, si = 0;
+      for (int a = a0; a < p.A; ++a, ++si) {
+        const int64_t kb0 = (int64_t)H * p.bpre[a];
+        const int64_t ss = u0 > kb0 ? u0 : kb0, se = min(u1, (int64_t)H * p.bpre[a + 1]);
+        if (ss >= u1) break;
+        tc::mbar_wait(tempty, (si & 1) ^ 1);  // previous segment's accumulator drained
         tc::tc_fence_after();
-        const uint32_t sa = tc::smem_u32(smem + st * D_STAGE), sb = sa + D_A;
+        for (int64_t u = ss; u < se; ++u, ++it) {
+          const int st = it % D_NST, ph = (it / D_NST) & 1;
+          tc::mbar_wait(full + st, ph);
+          tc::tc_fence_after();
+          const uint32_t sa = tc::smem_u32(smem + st * D_STAGE), sb = sa + D_A;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {  // 8 pixels per MMA
-          const uint64_t ad = tc::sdesc(sa + k * 32, 0, 1024, tc::kSW128);
-          const uint64_t bd = tc::sdesc(sb + k * 1024, 4096, 512, tc::kSW128_32B);
-          tc::mma_tf32(tbase, ad, bd, IDESC, (kb | k) != 0);
+          for (int k = 0; k < 4; ++k) {  // 8 pixels per MMA
+            const uint64_t ad = tc::sdesc(sa + k * 32, 0, 1024, tc::kSW128);
+            const uint64_t bd = tc::sdesc(sb + k * 1024, 4096, 512, tc::kSW128_32B);
+            tc::mma_tf32(tbase, ad, bd, IDESC, (u != ss || k != 0) ? 1u : 0u);
+          }
+          tc::mma_commit(empty + st);
         }
-        tc::mma_commit(empty + st);
+        tc::mma_commit(tfull);
       }
-      tc::mma_commit(tfull);
     }
   } else {
     const int qd = warp & 3, m = qd * 32 + lane;  // row = kw*24 + c*5 + kh; 120 = bias
-    tc::mbar_wait(tfull, 0);
-    tc::tc_fence_after();
     int n = -1;
     if (m < 120 && (m % 24) < 20) {
-      const int kw = m / 24, c = (m % 24) / 5, kh = (m % 24) % 5;
-      n = (kh * 5 + kw) * 4 + c;
+      const int kw = m / 24, cc = (m % 24) / 5, kh = (m % 24) % 5;
+      n = (kh * 5 + kw) * 4 + cc;
     } else if (m == 120) {
       n = 100;
     }
-    float* out = p.part + (int64_t)z * C1 * NPART;
+    int si = 0;
+    for (int a = a0; a < p.A; ++a, ++si) {
+      const int64_t kb0 = (int64_t)H * p.bpre[a];
+      if ((u0 > kb0 ? u0 : kb0) >= u1) break;
+      tc::mbar_wait(tfull, si & 1);
+      tc::tc_fence_after();
+      float* out = p.part + (int64_t)(a + c) * C1 * NPART;
 #pragma unroll
-    for (int n0 = 0; n0 < C1; n0 += 16) {
-      float v[16];
-      tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + n0, v);
-      if (n >= 0)
+      for (int n0 = 0; n0 < C1; n0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + n0, v);
+        if (n >= 0)
 #pragma unroll
-        for (int j = 0; j < 16; ++j) out[(n0 + j) * NPART + n] = v[j];
+          for (int j = 0; j < 16; ++j) out[(n0 + j) * NPART + n] = v[j];
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(tempty);
     }
   }
   tc::tc_fence_before();
@@ -359,7 +396,7 @@ int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, const 
   }
   C1Args p{wa.sidx, wa.bs, wa.A, wa.B, wa.first ? 0 : 1, wt, wbase + L.o_c1b, L.P_pad, p1, am1};
   const int tiles = wa.A * wa.B * 4;
-  launch_pdl(wa.pdl, k_conv1_fwd_tc, dim3(tiles < 148 ? tiles : 148), F_THREADS, Q_SMEM, st, mx, p);
+  launch_pdl(wa.pdl, k_conv1_fwd_tc, dim3(tiles < wa.sms ? tiles : wa.sms), F_THREADS, Q_SMEM, st, mx, p);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -370,7 +407,7 @@ int c1wt_pack(const float* c1w, float* out, cudaStream_t st) {
 
 // conv1 weight gradient on tensor cores: partials [A*nch][32][101] for k_dw_reduce_sgd.
 int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64_t xrows, const float* dY1,
-                int64_t slots, float* part, int64_t part_cap, int* nch_out, int* rpc_out, cudaStream_t st) {
+                int64_t slots, float* part, int64_t part_cap, int* g_out, cudaStream_t st) {
   CUtensorMap mx, md;
   constexpr int WP = W + 4;  // shifted planar copies [r][s][c][h][W+4]
   uint64_t dx[5] = {WP, H, 4, 4, (uint64_t)xrows};
@@ -380,20 +417,18 @@ int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64
   uint64_t sd[3] = {128, 128 * W, 128 * W * H};
   uint32_t bd[4] = {32, W, 1, 1};
   if (!tmap_encode(&mx, xplanar, 5, dx, sx, bx, 1) || !tmap_encode(&md, dY1, 4, dd, sd, bd, 2)) return -1;
-  int nch = (2 * 148 + wa.A - 1) / wa.A;
-  nch = nch < 1 ? 1 : (nch > wa.B ? wa.B : nch);
-  const int rpc = (wa.B + nch - 1) / nch;
-  nch = (wa.B + rpc - 1) / rpc;
-  if ((int64_t)wa.A * nch > part_cap) return -1;
+  // two CTAs per SM; at least half a sample (16 image rows) of work per CTA
+  const int64_t U = (int64_t)H * wa.sum_bs;
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(2 * wa.sms, U / 16));
+  if ((int64_t)wa.A + G > part_cap) return -1;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_conv1_dw_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, D_SMEM);
     attr = true;
   }
-  C1DwArgs p{wa.sidx, wa.bs, wa.B, nch, rpc, part};
-  launch_pdl(wa.pdl, k_conv1_dw_tc, dim3(nch, wa.A), 192, D_SMEM, st, mx, md, p);
-  *nch_out = nch;
-  *rpc_out = rpc;
+  C1DwArgs p{wa.sidx, wa.bpre, wa.A, wa.B, G, U, part};
+  launch_pdl(wa.pdl, k_conv1_dw_tc, dim3(G), 192, D_SMEM, st, mx, md, p);
+  *g_out = G;
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

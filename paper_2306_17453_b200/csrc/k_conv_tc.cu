@@ -22,6 +22,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
+
+#include <unordered_map>
 
 #include "fl_internal.h"
 #include "tc_common.cuh"
@@ -33,8 +36,53 @@ static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
 // swz: 0 none, 1 128B (16-B granules, K-major operands), 2 128B with 32-B atoms (32-bit
 // MN-major operands: matches the SWIZZLE_128B_BASE32B descriptor layout, Swizzle<2,5,2>).
+// Encoding a tensor map costs microseconds of host time and a round issues thousands of
+// launches whose maps repeat (same buffers, extents and boxes every wave and every round), so
+// encoded maps are memoised per host thread, keyed by every encode input.
+namespace {
+struct TmapKey {
+  const void* base;
+  int rank, swz;
+  uint64_t dims[5], strides[4];
+  uint32_t box[5];
+  bool operator==(const TmapKey& o) const { return memcmp(this, &o, sizeof *this) == 0; }
+};
+struct TmapKeyHash {
+  size_t operator()(const TmapKey& k) const {
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(&k);
+    uint64_t h = 1469598103934665603ull;
+    for (size_t i = 0; i < sizeof k / 8; ++i) h = (h ^ w[i]) * 1099511628211ull;
+    return (size_t)h;
+  }
+};
+}  // namespace
+
+static bool tmap_encode_uncached(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+                                 const uint64_t* strides_b, const uint32_t* box, int swz);
+
 bool tmap_encode(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_b,
                  const uint32_t* box, int swz) {
+  static thread_local std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash> cache;
+  TmapKey k;
+  memset(&k, 0, sizeof k);
+  k.base = base;
+  k.rank = rank;
+  k.swz = swz;
+  for (int i = 0; i < rank; ++i) k.dims[i] = dims[i], k.box[i] = box[i];
+  for (int i = 0; i + 1 < rank; ++i) k.strides[i] = strides_b[i];
+  auto it = cache.find(k);
+  if (it != cache.end()) {
+    *m = it->second;
+    return true;
+  }
+  if (!tmap_encode_uncached(m, base, rank, dims, strides_b, box, swz)) return false;
+  if (cache.size() > 4096) cache.clear();  // bounded: buffers are grow-only, so maps rarely churn
+  cache.emplace(k, *m);
+  return true;
+}
+
+static bool tmap_encode_uncached(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+                                 const uint64_t* strides_b, const uint32_t* box, int swz) {
   if (!g_encode) {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
@@ -286,7 +334,8 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 template <int N, int CH, int BMN, int FLIP, int POOL>
-cudaError_t launch_conv5(const CUtensorMap& mx, const CUtensorMap& mw, const ConvTcArgs& p, int A, bool pdl, cudaStream_t st) {
+cudaError_t launch_conv5(const CUtensorMap& mx, const CUtensorMap& mw, const ConvTcArgs& p, int A, bool pdl, int sms,
+                         cudaStream_t st) {
   constexpr int NB = BMN ? 32 : N;
   const int smem = ConvSmem<N, NB>::TOTAL;
   auto kfn = k_conv5_tc<N, CH, BMN, FLIP, POOL>;
@@ -296,7 +345,7 @@ cudaError_t launch_conv5(const CUtensorMap& mx, const CUtensorMap& mw, const Con
     attr = true;
   }
   const int tiles = A * p.B;
-  launch_pdl(pdl, kfn, dim3(tiles < 148 ? tiles : 148), 192, smem, st, mx, mw, p);
+  launch_pdl(pdl, kfn, dim3(tiles < sms ? tiles : sms), 192, smem, st, mx, mw, p);
   return cudaGetLastError();
 }
 
@@ -330,7 +379,7 @@ int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_
   CUtensorMap mx, mw;
   if (!make_plane_map(&mx, p1, 32, slots) || !make_w2_map(&mw, L, wbase, wclients, 64, 1)) return -1;
   ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, wbase + L.o_c2b, L.P_pad, p2, am2};
-  return launch_conv5<64, 1, 0, 0, 1>(mx, mw, p, wa.A, wa.pdl, st) == cudaSuccess ? 1 : -1;
+  return launch_conv5<64, 1, 0, 0, 1>(mx, mw, p, wa.A, wa.pdl, wa.sms, st) == cudaSuccess ? 1 : -1;
 }
 
 // conv2 dX (transposed conv) on tensor cores: dY2 -> dp1.
@@ -339,7 +388,7 @@ int conv2_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t
   CUtensorMap mx, mw;
   if (!make_plane_map(&mx, dY2, 64, slots) || !make_w2_map(&mw, L, wbase, wclients, 32, 2)) return -1;
   ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, nullptr, 0, dY1, nullptr, p1, am1};
-  return launch_conv5<32, 2, 1, 1, 0>(mx, mw, p, wa.A, wa.pdl, st) == cudaSuccess ? 1 : -1;
+  return launch_conv5<32, 2, 1, 1, 0>(mx, mw, p, wa.A, wa.pdl, wa.sms, st) == cudaSuccess ? 1 : -1;
 }
 
 }  // namespace flb

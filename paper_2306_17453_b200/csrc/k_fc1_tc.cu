@@ -724,7 +724,7 @@ int fc1_bwd_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t w
   BwArgs p{wa.bs, wa.A, wa.B, d.HID, d.F, wa.first ? 0 : 1, d.H2, d.W2, d.C2, p2, am2, dY2,
            wsrc + L.o_f1b, L.P_pad, slots_w + L.o_f1b, L.P_pad, dh, wa.lr};
   const int tiles = wa.A * (d.F / 128);
-  launch_pdl(wa.pdl, k_fc1_bwd_tc, dim3(tiles < 148 ? tiles : 148), 192, BW_SMEM, st, mws, mwd, mdh, mdht, mx, p);
+  launch_pdl(wa.pdl, k_fc1_bwd_tc, dim3(tiles < wa.sms ? tiles : wa.sms), 192, BW_SMEM, st, mws, mwd, mdh, mdht, mx, p);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
