@@ -195,8 +195,9 @@ constexpr int C1WT_FLOATS = 30 * 32 * 4;
 int c1wt_pack(const float* c1w, float* out, cudaStream_t st);
 int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, const float* wt, const float* xpack,
                  int64_t xrows, float* p1, uint8_t* am1, cudaStream_t st);
-int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64_t xrows, const float* dY1,
-                int64_t slots, float* part, int64_t part_cap, int* g_out, cudaStream_t st);
+// conv1 dW partials; dY1 is expanded on chip from dp1m and pool1's argmax am1
+int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64_t xrows, const float* dp1m,
+                const uint8_t* am1, int64_t slots, float* part, int64_t part_cap, int* g_out, cudaStream_t st);
 bool fc1_tc_supported(const Layout& L, int B);
 int fc1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p2,
                int64_t slots, float* h, float* part, int64_t part_floats, cudaStream_t st, int* launches);
@@ -209,8 +210,9 @@ int fc1_dw_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wc
               int64_t wclients_dst, const float* dh, const float* p2, int64_t slots, cudaStream_t st);
 int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p1,
                  int64_t slots, float* p2, uint8_t* am2, cudaStream_t st);
+// conv2 dX + ReLU' of pool1 -> dp1m [S][16][16][32] (the pool1 routing is fused into conv1's dW)
 int conv2_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dY2,
-                int64_t slots, const float* p1, const uint8_t* am1, float* dY1, cudaStream_t st);
+                int64_t slots, const float* p1, float* dp1m, cudaStream_t st);
 int logreg_train(const Layout& L, const WaveSched& ws, int n_local, int B, float lr, const float* xpack,
                  const int32_t* ypack, const float* theta_g, float* slots, const int32_t* steps_dev,
                  const int64_t* wave_slot_off_dev, cudaStream_t st);

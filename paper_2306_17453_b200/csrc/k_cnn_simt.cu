@@ -624,9 +624,9 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   }
   pf.begin(st);
   if (tc) {  // pool1/ReLU backward fused into the epilogue: writes dY1 directly
-    if (conv2_dx_tc(L, wa, w.base, wcl, b.dY2, b.slots, b.p1, b.am1, b.dY1, st) < 0) return -1;
+    if (conv2_dx_tc(L, wa, w.base, wcl, b.dY2, b.slots, b.p1, b.dp1, st) < 0) return -1;
     ++n;
-    pf.end(K_CONV2_DX, f_c2, 4.0 * S * hw1 * d.C2 + S * hw0 * d.C1 * 4.0 + S * hw1 * d.C1 * 5.0, st);  // dY2, p1+am1 in; dY1 out
+    pf.end(K_CONV2_DX, f_c2, 4.0 * S * hw1 * (d.C2 + 2.0 * d.C1), st);  // dY2, p1 in; dp1m out
   } else {
     launch(ConvDx{b.dY2, wa.bs, B, d.H1, d.W1, d.C1, d.C2, w, L.o_c2w, b.dp1}, B * d.H1 * d.W1, d.C1, A, st), ++n;
     pf.end(K_CONV2_DX, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
@@ -658,13 +658,14 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   int nch1 = b.nch, rpc1 = rpc, g1 = 0;
   pf.begin(st);
   if (tc1) {
-    if (conv1_dw_tc(L, wa, b.xplanar, b.xrows, b.dY1, b.slots, b.part1, b.part1_tc_cap, &g1, st) < 0) return -1;
+    if (conv1_dw_tc(L, wa, b.xplanar, b.xrows, b.dp1, b.am1, b.slots, b.part1, b.part1_tc_cap, &g1, st) < 0)
+      return -1;
     ++n;
   } else {
     launch(ConvDw{b.dY1, xpack, wa.sidx, wa.bs, B, d.H0, d.W0, d.cpad, d.C1, b.nch, rpc, b.part1}, d.C1,
            25 * d.cpad + 1, A * b.nch, st), ++n;
   }
-  pf.end(K_CONV1_DW, f_c1, 4.0 * S * hw0 * (d.cin + d.C1), st);
+  pf.end(K_CONV1_DW, f_c1, tc1 ? 4.0 * S * hw0 * d.cin + 5.0 * S * hw1 * d.C1 : 4.0 * S * hw0 * (d.cin + d.C1), st);
   pf.begin(st);
   launch_pdl(wa.pdl, k_dw_reduce_sgd, dim3((d.C1 * (25 * d.cpad + 1) + 127) / 128, A), 128, 0, st, 
       b.part1, nch1, rpc1, wa.bs, d.C1, 25 * d.cpad + 1, w, L.o_c1w,

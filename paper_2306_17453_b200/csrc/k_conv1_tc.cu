@@ -222,15 +222,20 @@ __global__ void k_c1wt_pack(const float* __restrict__ w, float* __restrict__ out
 // K-major SW128: row (kw, c, kh) = 32 consecutive pixels of input channel c, row h0+kh-2,
 // shifted by kw-2 — one TMA box {32 w, 5 h, 4 c} of the planar (c, h, w) input per kw lands
 // as 20 such rows.  Each kw block is padded to 24 rows (3 SW128 atoms); rows 120-127 hold a
-// constant ones row (bias) and zeros.  B = dY1 row (32 px x 32 ch), MN-major BASE32B.
+// constant ones row (bias) and zeros.  B = dY1 row (32 px x 32 ch), MN-major BASE32B, is
+// never read from HBM: TMA brings the pooled row h0/2 of dp1m and pool1's argmax, and the
+// four epilogue warps expand it (pool1 backward: dY1 = dp1m at the window's argmax, else 0)
+// into the stage's B tile before the MMA consumes it.
 constexpr int D_KWB = 24 * 128;          // 3072 B per kw block (20 rows + 4 zero rows)
 constexpr int D_A = 128 * 128;           // 16384: 5 kw blocks + constant rows 120..127
 constexpr int D_B = 32 * 128;            // 4096
-constexpr int D_STAGE = D_A + D_B;       // 20480
+constexpr int D_RAW = 16 * 32 * 4 + 16 * 32;  // pooled-row dp1m (16 px x 32 ch fp32) + its argmax bytes
+constexpr int D_STAGE = 23 * 1024;       // A + B + raw, 1024-aligned (SW128 operands)
 constexpr int D_NST = 4;
 constexpr int D_BAR = D_NST * D_STAGE;
 constexpr int D_SMEM = D_BAR + 128 + 1024;
-constexpr int D_TX = 5 * 20 * 128 + D_B; // bytes TMA writes per stage
+constexpr int D_TX = 5 * 20 * 128 + D_RAW;  // bytes TMA writes per stage (B is built by the expander warps)
+static_assert(D_A + D_B + D_RAW <= D_STAGE, "stage layout");
 constexpr int NPART = 25 * 4 + 1;        // partial row length per output channel (k_dw_reduce_sgd layout)
 
 struct C1DwArgs {
@@ -253,7 +258,8 @@ __device__ __forceinline__ int c1_client_of(const int32_t* __restrict__ bpre, in
 }
 
 __global__ void __launch_bounds__(192, 1)
-    k_conv1_dw_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapD, C1DwArgs p) {
+    k_conv1_dw_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapD,
+                  const __grid_constant__ CUtensorMap mapA, C1DwArgs p) {
   constexpr uint32_t IDESC = tc::idesc_tf32(128, C1, 0, 1);  // A K-major, B MN-major
   // Balanced split-K (as conv2's dW): CTA c reduces k-blocks [c·U/G, (c+1)·U/G) of the wave's
   // concatenated (client, sample, image row) sequence; each client segment ends with its
@@ -266,7 +272,8 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + D_BAR);
   uint64_t* empty = full + D_NST;
-  uint64_t* tfull = empty + D_NST;
+  uint64_t* bready = empty + D_NST;  // B tile expanded (128 arrivals)
+  uint64_t* tfull = bready + D_NST;
   uint64_t* tempty = tfull + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -282,9 +289,11 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       tc::prefetch_tmap(&mapX);
       tc::prefetch_tmap(&mapD);
+      tc::prefetch_tmap(&mapA);
       for (int i = 0; i < D_NST; ++i) {
         tc::mbar_init(full + i, 1);
         tc::mbar_init(empty + i, 1);
+        tc::mbar_init(bready + i, 128);
       }
       tc::mbar_init(tfull, 1);
       tc::mbar_init(tempty, 128);
@@ -314,7 +323,8 @@ __global__ void __launch_bounds__(192, 1)
           // tap column kw = shifted copy (kw & 3) read from w' = (kw & 4): x[w + kw - 2]
           for (int kw = 0; kw < 5; ++kw)
             tc::tma_load_5d(sa + kw * D_KWB, &mapX, full + st, kw & 4, h0 - 2, 0, kw & 3, row);
-          tc::tma_load_4d(sa + D_A, &mapD, full + st, 0, 0, h0, a * p.B + rr);
+          tc::tma_load_4d(sa + D_A + D_B, &mapD, full + st, 0, 0, h0 >> 1, a * p.B + rr);        // dp1m row
+          tc::tma_load_4d(sa + D_A + D_B + 2048, &mapA, full + st, 0, 0, h0 >> 1, a * p.B + rr);  // am1 row
         }
       }
     }
@@ -329,7 +339,7 @@ __global__ void __launch_bounds__(192, 1)
         tc::tc_fence_after();
         for (int64_t u = ss; u < se; ++u, ++it) {
           const int st = it % D_NST, ph = (it / D_NST) & 1;
-          tc::mbar_wait(full + st, ph);
+          tc::mbar_wait(bready + st, ph);  // A landed (the expanders waited on full) and B built
           tc::tc_fence_after();
           const uint32_t sa = tc::smem_u32(smem + st * D_STAGE), sb = sa + D_A;
 #pragma unroll
@@ -352,10 +362,32 @@ __global__ void __launch_bounds__(192, 1)
     } else if (m == 120) {
       n = 100;
     }
-    int si = 0;
+    int si = 0, it = 0;
+    const int t = threadIdx.x - 64, w = t >> 2, q = t & 3;  // B row (pixel) w, channels 8q..8q+7
     for (int a = a0; a < p.A; ++a, ++si) {
       const int64_t kb0 = (int64_t)H * p.bpre[a];
-      if ((u0 > kb0 ? u0 : kb0) >= u1) break;
+      const int64_t ss = u0 > kb0 ? u0 : kb0, se = min(u1, (int64_t)H * p.bpre[a + 1]);
+      if (ss >= u1) break;
+      for (int64_t u = ss; u < se; ++u, ++it) {  // pool1 backward into the stage's B tile
+        const int st = it % D_NST, ph = (it / D_NST) & 1;
+        const int h0 = (int)((u - kb0) % H);
+        tc::mbar_wait(full + st, ph);
+        uint8_t* stage = smem + st * D_STAGE;
+        const float* dp = reinterpret_cast<const float*>(stage + D_A + D_B) + (w >> 1) * 32 + 8 * q;
+        const uint2 am = *reinterpret_cast<const uint2*>(stage + D_A + D_B + 2048 + (w >> 1) * 32 + 8 * q);
+        const uint32_t code = (uint32_t)(((h0 & 1) << 1) | (w & 1));
+        const float4 g0 = *reinterpret_cast<const float4*>(dp), g1 = *reinterpret_cast<const float4*>(dp + 4);
+        const float4 o0 = make_float4((am.x & 0xff) == code ? g0.x : 0.f, ((am.x >> 8) & 0xff) == code ? g0.y : 0.f,
+                                      ((am.x >> 16) & 0xff) == code ? g0.z : 0.f, (am.x >> 24) == code ? g0.w : 0.f);
+        const float4 o1 = make_float4((am.y & 0xff) == code ? g1.x : 0.f, ((am.y >> 8) & 0xff) == code ? g1.y : 0.f,
+                                      ((am.y >> 16) & 0xff) == code ? g1.z : 0.f, (am.y >> 24) == code ? g1.w : 0.f);
+        // B row w (128 B = 32 channels), 32-byte granule q stored at q ^ (w % 4) (ATOM_32B)
+        float4* bw = reinterpret_cast<float4*>(stage + D_A + w * 128 + ((q ^ (w & 3)) << 5));
+        bw[0] = o0;
+        bw[1] = o1;
+        tc::fence_async_smem();  // generic-proxy writes -> tensor-core reads
+        tc::mbar_arrive(bready + st);
+      }
       tc::mbar_wait(tfull, si & 1);
       tc::tc_fence_after();
       float* out = p.part + (int64_t)(a + c) * C1 * NPART;
@@ -406,17 +438,23 @@ int c1wt_pack(const float* c1w, float* out, cudaStream_t st) {
 }
 
 // conv1 weight gradient on tensor cores: partials [A*nch][32][101] for k_dw_reduce_sgd.
-int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64_t xrows, const float* dY1,
-                int64_t slots, float* part, int64_t part_cap, int* g_out, cudaStream_t st) {
-  CUtensorMap mx, md;
+int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64_t xrows, const float* dp1m,
+                const uint8_t* am1, int64_t slots, float* part, int64_t part_cap, int* g_out, cudaStream_t st) {
+  CUtensorMap mx, md, ma;
   constexpr int WP = W + 4;  // shifted planar copies [r][s][c][h][W+4]
   uint64_t dx[5] = {WP, H, 4, 4, (uint64_t)xrows};
   uint64_t sx[4] = {4 * WP, 4 * WP * H, 4 * WP * H * 4, 4 * WP * H * 16};
   uint32_t bx[5] = {W, 5, 4, 1, 1};
-  uint64_t dd[4] = {32, W, H, (uint64_t)slots};
-  uint64_t sd[3] = {128, 128 * W, 128 * W * H};
-  uint32_t bd[4] = {32, W, 1, 1};
-  if (!tmap_encode(&mx, xplanar, 5, dx, sx, bx, 1) || !tmap_encode(&md, dY1, 4, dd, sd, bd, 2)) return -1;
+  // pooled rows of dp1m [S][16][16][32] fp32 and of am1 (u8, viewed as 8 x 4-byte words per pixel)
+  uint64_t dd[4] = {32, W / 2, H / 2, (uint64_t)slots};
+  uint64_t sd[3] = {128, 128 * (W / 2), 128 * (W / 2) * (H / 2)};
+  uint32_t bd[4] = {32, W / 2, 1, 1};
+  uint64_t da[4] = {8, W / 2, H / 2, (uint64_t)slots};
+  uint64_t sa[3] = {32, 32 * (W / 2), 32 * (W / 2) * (H / 2)};
+  uint32_t ba[4] = {8, W / 2, 1, 1};
+  if (!tmap_encode(&mx, xplanar, 5, dx, sx, bx, 1) || !tmap_encode(&md, dp1m, 4, dd, sd, bd, 0) ||
+      !tmap_encode(&ma, am1, 4, da, sa, ba, 0))
+    return -1;
   // two CTAs per SM; at least half a sample (16 image rows) of work per CTA
   const int64_t U = (int64_t)H * wa.sum_bs;
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>(2 * wa.sms, U / 16));
@@ -427,7 +465,7 @@ int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64
     attr = true;
   }
   C1DwArgs p{wa.sidx, wa.bpre, wa.A, wa.B, G, U, part};
-  launch_pdl(wa.pdl, k_conv1_dw_tc, dim3(G), 192, D_SMEM, st, mx, md, p);
+  launch_pdl(wa.pdl, k_conv1_dw_tc, dim3(G), 192, D_SMEM, st, mx, md, ma, p);
   *g_out = G;
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }

@@ -127,7 +127,7 @@ struct ConvTcArgs {
   int wmul;               // 0: every client reads θ_g (first wave), 1: client slot
   const float* bias;      // bias of client 0; client a at bias + a*bias_stride
   int64_t bias_stride;
-  float* out;             // fwd: p2 [S][8][8][N]; dx: dY1 [S][32][32][N] (pool1 backward fused)
+  float* out;             // fwd: p2 [S][8][8][N]; dx: dp1m [S][16][16][N] (ReLU'-masked pooled gradient)
   uint8_t* am;            // fwd: argmax [S][8][8][N]
   const float* p1;        // dx: pooled conv1 output [S][16][16][N] (ReLU' of the window max)
   const uint8_t* am1;     // dx: pool1 argmax [S][16][16][N]
@@ -293,32 +293,16 @@ __global__ void __launch_bounds__(192, 1)
             *reinterpret_cast<uint4*>(p.am + o) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
           }
         } else {
-          // pool1 backward fused: dY1 at the 2x2 window of (h, w) = dp1 routed to the
-          // window's argmax when the pooled (ReLU'd) value is > 0, zero elsewhere.
+          // ReLU' of pool1 fused: dp1m = dp1 where the pooled value is > 0, else 0.  The
+          // routing to the window's argmax (pool1 backward) happens where dY1 is consumed
+          // (conv1's dW expands it into its B operand), so dY1 is never written to HBM.
           const int64_t o = (((int64_t)s * HH + h) * WW + w) * N + n0;
-          float g[16];
-          uint8_t am[16];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const float4 pv = *reinterpret_cast<const float4*>(p.p1 + o + 4 * j);
-            const uint32_t aw = *reinterpret_cast<const uint32_t*>(p.am1 + o + 4 * j);
-            g[4 * j] = pv.x > 0.f ? v[4 * j] : 0.f;
-            g[4 * j + 1] = pv.y > 0.f ? v[4 * j + 1] : 0.f;
-            g[4 * j + 2] = pv.z > 0.f ? v[4 * j + 2] : 0.f;
-            g[4 * j + 3] = pv.w > 0.f ? v[4 * j + 3] : 0.f;
-            am[4 * j] = aw & 0xff;
-            am[4 * j + 1] = (aw >> 8) & 0xff;
-            am[4 * j + 2] = (aw >> 16) & 0xff;
-            am[4 * j + 3] = aw >> 24;
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            float4* dst = reinterpret_cast<float4*>(
-                p.out + ((((int64_t)s * 2 * HH + 2 * h + (u >> 1)) * 2 * WW + 2 * w + (u & 1)) * N + n0));
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              dst[j] = make_float4(am[4 * j] == u ? g[4 * j] : 0.f, am[4 * j + 1] == u ? g[4 * j + 1] : 0.f,
-                                   am[4 * j + 2] == u ? g[4 * j + 2] : 0.f, am[4 * j + 3] == u ? g[4 * j + 3] : 0.f);
+            *reinterpret_cast<float4*>(p.out + o + 4 * j) =
+                make_float4(pv.x > 0.f ? v[4 * j] : 0.f, pv.y > 0.f ? v[4 * j + 1] : 0.f,
+                            pv.z > 0.f ? v[4 * j + 2] : 0.f, pv.w > 0.f ? v[4 * j + 3] : 0.f);
           }
         }
       }
@@ -384,10 +368,10 @@ int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_
 
 // conv2 dX (transposed conv) on tensor cores: dY2 -> dp1.
 int conv2_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dY2,
-                int64_t slots, const float* p1, const uint8_t* am1, float* dY1, cudaStream_t st) {
+                int64_t slots, const float* p1, float* dp1m, cudaStream_t st) {
   CUtensorMap mx, mw;
   if (!make_plane_map(&mx, dY2, 64, slots) || !make_w2_map(&mw, L, wbase, wclients, 32, 2)) return -1;
-  ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, nullptr, 0, dY1, nullptr, p1, am1};
+  ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, nullptr, 0, dp1m, nullptr, p1, nullptr};
   return launch_conv5<32, 2, 1, 1, 0>(mx, mw, p, wa.A, wa.pdl, wa.sms, st) == cudaSuccess ? 1 : -1;
 }
 

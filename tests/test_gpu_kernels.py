@@ -88,17 +88,16 @@ def unpool_ref(dp, p, am):
 
 
 @pytest.mark.parametrize("sizes", SIZES)
-def test_conv2_dx_pool1_backward_tc(sizes):
+def test_conv2_dx_pool1_relu_tc(sizes):
     ctx, theta = one_wave(sizes)
     S = len(sizes) * B
     dY2 = ctx.fl_debug_read("dY2", (S, 16, 16, 64))
     p1 = ctx.fl_debug_read("p1", (S, 16, 16, 32))
-    am1 = ctx.fl_debug_read("am1", (S, 16, 16, 32), np.uint8)
-    dY1 = ctx.fl_debug_read("dY1", (S, 32, 32, 32))
+    dp1m = ctx.fl_debug_read("dp1", (S, 16, 16, 32))  # conv2 dX with pool1's ReLU' (routing is in conv1 dW)
     P = params(theta)
     valid = np.concatenate([np.arange(a * B, a * B + int(n)) for a, n in enumerate(sizes)])
     dp1 = F.conv_transpose2d(nchw(dY2[valid]), P["conv2.w"], padding=2).permute(0, 2, 3, 1).numpy()
-    assert rel(dY1[valid], unpool_ref(dp1, p1[valid], am1[valid])) < TOL
+    assert rel(dp1m[valid], np.where(p1[valid] > 0, dp1, 0.0)) < TOL
 
 
 def _grad_from_update(ctx, theta, client, lr):
@@ -145,7 +144,12 @@ def test_conv1_forward_tc(sizes):
 def test_conv1_dw_tc(sizes):
     ctx, theta = one_wave(sizes)
     S = len(sizes) * B
-    dY1 = ctx.fl_debug_read("dY1", (S, 32, 32, 32))
+    # dY1 never reaches HBM: the kernel expands it from dp1m and pool1's argmax on chip, so the
+    # reference expands the same inputs with the plain pool-backward definition
+    p1 = ctx.fl_debug_read("p1", (S, 16, 16, 32))
+    am1 = ctx.fl_debug_read("am1", (S, 16, 16, 32), np.uint8)
+    dp1m = ctx.fl_debug_read("dp1", (S, 16, 16, 32))
+    dY1 = unpool_ref(dp1m, p1, am1)
     lr = synth.preset("C2").lr
     for a, xa in enumerate(client_x(sizes)):
         g = _grad_from_update(ctx, theta, a, lr)
