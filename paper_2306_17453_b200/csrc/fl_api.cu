@@ -411,7 +411,8 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   int prio_lo = 0, prio_hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   for (int g = 0; g < nstreams; ++g) {
-    CK(cudaStreamCreateWithPriority(&c->gstream[(size_t)g], cudaStreamNonBlocking, g < c->nsolo ? prio_hi : prio_lo));
+    const bool hi = (g < c->nsolo) != (getenv("FL_BULK_PRIO") != nullptr);  // FL_BULK_PRIO: bulk groups high instead
+    CK(cudaStreamCreateWithPriority(&c->gstream[(size_t)g], cudaStreamNonBlocking, hi ? prio_hi : prio_lo));
     CK(cudaEventCreateWithFlags(&c->ev_join[(size_t)g], cudaEventDisableTiming));
   }
   if (!c->pop_dev) {

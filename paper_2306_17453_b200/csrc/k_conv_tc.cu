@@ -125,6 +125,7 @@ struct ConvTcArgs {
   int A;                  // active clients (tiles = A·B (client, sample) pairs)
   int B;
   int wmul;               // 0: every client reads θ_g (first wave), 1: client slot
+  int msplit;             // tiles per sample: 1 (both M-halves) or 2 (one M-half each, small waves)
   const float* bias;      // bias of client 0; client a at bias + a*bias_stride
   int64_t bias_stride;
   float* out;             // fwd: p2 [S][8][8][N]; dx: dp1m [S][16][16][N] (ReLU'-masked pooled gradient)
@@ -149,8 +150,13 @@ __global__ void __launch_bounds__(192, 1)
   // (samples past a client's |b| are skipped identically by every role).  The smem stage
   // ring runs across tiles and the TMEM accumulators are double-buffered, so the loads of
   // tile i+1 and the epilogue of tile i-1 overlap the MMAs of tile i.
-  const int T = p.A * p.B;
-  auto valid = [&](int t) { return (t % p.B) < p.bs[t / p.B]; };
+  // Tile t = slot (t / msplit) and, when msplit = 2, only its M-half (t & 1): small waves
+  // spread a sample's MMAs and epilogue over two SMs (the loads are the same either way).
+  const int T = p.A * p.B * p.msplit;
+  auto valid = [&](int t) {
+    const int sl = t / p.msplit;
+    return (sl % p.B) < p.bs[sl / p.B];
+  };
 
   // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
   // would stall other streams' kernels) or touching anything it writes.
@@ -192,7 +198,7 @@ __global__ void __launch_bounds__(192, 1)
       int it = 0;
       for (int t = blockIdx.x; t < T; t += gridDim.x) {
         if (!valid(t)) continue;
-        const int a = t / p.B, s = t;  // slot index = a*B + r = t
+        const int s = t / p.msplit, a = s / p.B;  // slot index s = a*B + r
         for (int kb = 0; kb < NKB; ++kb, ++it) {
           const int st = it % NSTAGE, ph = (it / NSTAGE) & 1;
           const int kw = kb / CH, q = kb % CH;
@@ -214,6 +220,7 @@ __global__ void __launch_bounds__(192, 1)
       int it = 0, tc_ = 0;
       for (int t = blockIdx.x; t < T; t += gridDim.x) {
         if (!valid(t)) continue;
+        const int mh0 = p.msplit == 2 ? (t & 1) : 0, mh1 = p.msplit == 2 ? mh0 + 1 : 2;
         const int buf = tc_ & 1, aph = (tc_ >> 1) & 1;
         tc::mbar_wait(aempty + buf, aph ^ 1);  // epilogue finished reading this buffer
         tc::tc_fence_after();
@@ -232,6 +239,7 @@ __global__ void __launch_bounds__(192, 1)
                                       : tc::sdesc(sb + kh * S::B_TAP + k * 32, 0, 1024, tc::kSW128);
 #pragma unroll
               for (int mh = 0; mh < 2; ++mh) {
+                if (mh < mh0 || mh >= mh1) continue;
                 const uint64_t ad = tc::sdesc(sa + (mh * 8 + kh) * WW * 128 + k * 32, 0, 1024, tc::kSW128);
                 tc::mma_tf32(acc0 + mh * N, ad, bd, IDESC, (kb | kh | k) != 0);
               }
@@ -249,7 +257,8 @@ __global__ void __launch_bounds__(192, 1)
     int tc_ = 0;
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
     if (!valid(t)) continue;
-    const int a = t / p.B, s = t;
+    const int s = t / p.msplit, a = s / p.B;
+    const int mh0 = p.msplit == 2 ? (t & 1) : 0, mh1 = p.msplit == 2 ? mh0 + 1 : 2;
     const int buf = tc_ & 1, aph = (tc_ >> 1) & 1;
     ++tc_;
     tc::mbar_wait(afull + buf, aph);
@@ -258,6 +267,7 @@ __global__ void __launch_bounds__(192, 1)
     const float* bias = p.bias + (int64_t)a * p.bias_stride * p.wmul;
 #pragma unroll
     for (int mh = 0; mh < 2; ++mh) {
+      if (mh < mh0 || mh >= mh1) continue;
       const int h = mh * 8 + (i >> 4), w = i & 15;
 #pragma unroll
       for (int n0 = 0; n0 < N; n0 += 16) {
@@ -317,6 +327,17 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) tc::tmem_dealloc<TMEM_COLS>(tbase);
 }
 
+// One M-half per tile when the doubled tile count still fits on the wave's SMs.  Opt-in
+// (FL_MSPLIT=1): it shortens a lone client's step (2000 samples: 7.2 -> 6.7 ms) but costs
+// throughput when the critical-path streams share the GPU with the bulk (C2 16.6 -> 17.1 ms).
+int msplit_for(const WaveArgs& wa) {
+  static const bool on = [] {
+    const char* e = getenv("FL_MSPLIT");
+    return e && e[0] == '1';
+  }();
+  return (on && 2 * wa.sum_bs <= wa.sms) ? 2 : 1;
+}
+
 template <int N, int CH, int BMN, int FLIP, int POOL>
 cudaError_t launch_conv5(const CUtensorMap& mx, const CUtensorMap& mw, const ConvTcArgs& p, int A, bool pdl, int sms,
                          cudaStream_t st) {
@@ -328,7 +349,7 @@ cudaError_t launch_conv5(const CUtensorMap& mx, const CUtensorMap& mw, const Con
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  const int tiles = A * p.B;
+  const int tiles = A * p.B * p.msplit;
   launch_pdl(pdl, kfn, dim3(tiles < sms ? tiles : sms), 192, smem, st, mx, mw, p);
   return cudaGetLastError();
 }
@@ -362,7 +383,7 @@ int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_
                  int64_t slots, float* p2, uint8_t* am2, cudaStream_t st) {
   CUtensorMap mx, mw;
   if (!make_plane_map(&mx, p1, 32, slots) || !make_w2_map(&mw, L, wbase, wclients, 64, 1)) return -1;
-  ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, wbase + L.o_c2b, L.P_pad, p2, am2};
+  ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, msplit_for(wa), wbase + L.o_c2b, L.P_pad, p2, am2};
   return launch_conv5<64, 1, 0, 0, 1>(mx, mw, p, wa.A, wa.pdl, wa.sms, st) == cudaSuccess ? 1 : -1;
 }
 
@@ -371,7 +392,7 @@ int conv2_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t
                 int64_t slots, const float* p1, float* dp1m, cudaStream_t st) {
   CUtensorMap mx, mw;
   if (!make_plane_map(&mx, dY2, 64, slots) || !make_w2_map(&mw, L, wbase, wclients, 32, 2)) return -1;
-  ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, nullptr, 0, dp1m, nullptr, p1, nullptr};
+  ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, msplit_for(wa), nullptr, 0, dp1m, nullptr, p1, nullptr};
   return launch_conv5<32, 2, 1, 1, 0>(mx, mw, p, wa.A, wa.pdl, wa.sms, st) == cudaSuccess ? 1 : -1;
 }
 
