@@ -46,7 +46,7 @@ struct DwArgs {
   const int32_t* bpre;  // [A + 1] prefix sums of the wave's batch sizes
   int A, B, G;          // G CTAs split the wave's U k-blocks (8 per sample) evenly
   int64_t U;
-  float* part;          // [A + G][801][64]: partial of (CTA c, client a) at z = a + c
+  float* part;          // [A + G][64 o][801]: partial of (CTA c, client a) at z = a + c
 };
 
 // Largest a in [0, A) with bpre[a] <= x (the client owning concatenated sample x).
@@ -182,11 +182,9 @@ __global__ void __launch_bounds__(192, 1)
         for (int n0 = 0; n0 < NO; n0 += 16) {
           float v[16];
           tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + t * NO + n0, v);  // warp-collective
-          if (row >= 0) {
-            float4* dst = reinterpret_cast<float4*>(out + (int64_t)row * NO + n0);
+          if (row >= 0)  // partial layout [o][row]: a warp's 32 rows are consecutive -> coalesced
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          }
+            for (int j = 0; j < 16; ++j) out[(int64_t)(n0 + j) * NROW + row] = v[j];
         }
       }
       tc::tc_fence_before();
@@ -210,7 +208,7 @@ __global__ void k_dw2_reduce_sgd(const float* __restrict__ part, const int32_t* 
   const float* pa = part + (int64_t)(a + c0) * NROW * NO;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < NROW * NO; e += gridDim.x * blockDim.x) {
     const float g = ordered_sum(pa + e, c1 - c0 + 1, (int64_t)NROW * NO);
-    const int row = e / NO, o = e - row * NO;
+    const int o = e / NROW, row = e - o * NROW;  // [o][row]: consecutive e -> consecutive W[o][tap][c]
     const int64_t idx = row < 800 ? o_w + (int64_t)o * 800 + row : o_b + o;
     dst[(int64_t)a * P_pad + idx] = wsrc[(int64_t)a * wstride + idx] - lr * g;
   }
