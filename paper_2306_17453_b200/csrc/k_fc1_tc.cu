@@ -372,13 +372,16 @@ __global__ void __launch_bounds__(192, 1)
 // twice).  After a panel's last chunk the epilogue routes dp2 through pool2's argmax / ReLU'
 // into dY2.  The stage ring, the G buffers and the two dX accumulators run across tiles.
 constexpr int BW_W = 4 * 128 * 128;               // 4 k-chunks x [128 n][32 k]
-constexpr int BW_DH = 4 * NB * 128;               // dh, 4 boxes [32 r][32 n] (SW128: K-major B of dX)
-constexpr int BW_DHT = 4 * NB * 128;              // dhᵀ, 4 chunks [32 r][32 n] (ATOM_32B: MN-major A of dW)
-constexpr int BW_STAGE = BW_W + BW_DH + BW_DHT;   // 96 KB
+// dh, 4 chunks [32 r][32 n] in the SWIZZLE_128B_ATOM_32B layout, used twice: as the MN-major A
+// of dW (n contiguous) and as the K-major B of dX (descriptor layout BASE32B, SBO = 512 —
+// probed in scripts/tc_probe.cu), so one copy serves both MMAs
+constexpr int BW_DHT = 4 * NB * 128;
+constexpr int BW_STAGE = BW_W + BW_DHT;           // 80 KB
 constexpr int BW_NST = 2;
 constexpr int BW_P2B = 4 * NB * 128;              // p2ᵀ panel, 4 chunks [32 r][32 k] (MN-major B of dW)
 constexpr int BW_P2 = BW_NST * BW_STAGE;          // two panels (double-buffered across tiles)
-constexpr int BW_BAR = BW_P2 + 2 * BW_P2B;
+constexpr int BW_OUT = BW_P2 + 2 * BW_P2B;        // 2 x 16 KB store buffers: a stage is released as
+constexpr int BW_BAR = BW_OUT + 2 * 16384;        // soon as the epilogue has read it, not when stored
 constexpr int BW_SMEM = BW_BAR + 256 + 1024;
 constexpr uint32_t BW_TCOLS = 512;                // G [0,128) [128,256); dX [256,288) [288,320)
 
@@ -399,8 +402,7 @@ struct BwArgs {
 
 __global__ void __launch_bounds__(192, 1)
     k_fc1_bwd_tc(const __grid_constant__ CUtensorMap mapWsrc, const __grid_constant__ CUtensorMap mapWdst,
-                 const __grid_constant__ CUtensorMap mapDh, const __grid_constant__ CUtensorMap mapDht,
-                 const __grid_constant__ CUtensorMap mapX, BwArgs p) {
+                 const __grid_constant__ CUtensorMap mapDht, const __grid_constant__ CUtensorMap mapX, BwArgs p) {
   constexpr uint32_t IDESC_DX = tc::idesc_tf32(128, NB, 1, 0);   // A (W1ᵀ) MN-major, B (dh) K-major
   constexpr uint32_t IDESC_DW = tc::idesc_tf32(128, 128, 1, 1);  // A (dhᵀ), B (p2ᵀ) MN-major
   const int KT = p.F / 128, T = p.A * KT, nch = p.HID / 128;
@@ -421,12 +423,11 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       tc::prefetch_tmap(&mapWsrc);
       tc::prefetch_tmap(&mapWdst);
-      tc::prefetch_tmap(&mapDh);
       tc::prefetch_tmap(&mapDht);
       tc::prefetch_tmap(&mapX);
       for (int i = 0; i < BW_NST; ++i) {
         tc::mbar_init(full + i, 1);
-        tc::mbar_init(empty + i, 1);
+        tc::mbar_init(empty + i, 128);  // every epilogue thread, after its last read of the stage
       }
       for (int i = 0; i < 2; ++i) {
         tc::mbar_init(gfull + i, 1);
@@ -464,9 +465,7 @@ __global__ void __launch_bounds__(192, 1)
           tc::mbar_expect_tx(full + st, BW_STAGE);
           for (int j = 0; j < 4; ++j)
             tc::tma_load_3d(sw + j * 16384, &mapWsrc, full + st, 128 * kt + 32 * j, 128 * c, a * p.wmul);
-          for (int j = 0; j < 4; ++j)
-            tc::tma_load_3d(sw + BW_W + j * 4096, &mapDh, full + st, 128 * c + 32 * j, a * p.B, 0);
-          tc::tma_load_3d(sw + BW_W + BW_DH, &mapDht, full + st, 0, a * p.B, 4 * c);
+          tc::tma_load_3d(sw + BW_W, &mapDht, full + st, 0, a * p.B, 4 * c);
         }
       }
     }
@@ -488,11 +487,11 @@ __global__ void __launch_bounds__(192, 1)
           tc::mbar_wait(full + st, ph);
           tc::mbar_wait(gempty + buf, gph ^ 1);
           tc::tc_fence_after();
-          const uint32_t uw = tc::smem_u32(smem + st * BW_STAGE), udh = uw + BW_W, udht = udh + BW_DH;
+          const uint32_t uw = tc::smem_u32(smem + st * BW_STAGE), udht = uw + BW_W;
 #pragma unroll
-          for (int kk = 0; kk < 16; ++kk)  // dX: K = this chunk's 128 n, 8 per MMA
+          for (int kk = 0; kk < 16; ++kk)  // dX: K = this chunk's 128 n, 8 per MMA (B = dh, K-major BASE32B)
             tc::mma_tf32(tdx, tc::sdesc(uw + kk * 1024, 16384, 512, tc::kSW128_32B),
-                         tc::sdesc(udh + (kk >> 2) * 4096 + (kk & 3) * 32, 0, 1024, tc::kSW128), IDESC_DX,
+                         tc::sdesc(udht + (kk >> 2) * 4096 + (kk & 3) * 32, 0, 512, tc::kSW128_32B), IDESC_DX,
                          (c | kk) != 0);
 #pragma unroll
           for (int k = 0; k < 4; ++k)      // dW: K = 32 batch slots
@@ -507,64 +506,77 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     // ---------------- epilogue (thread = n row of the chunk for G; = k row of the panel for dX)
     const int qd = warp & 3, row = qd * 32 + lane;
-    int it = 0, ti = 0;
+    const bool storer = (warp == 2 && lane == 0);  // issues and retires the W stores (bulk groups are per thread)
+    int it = 0, ti = 0, oi = 0;
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
       const int a = t / KT, kt = t % KT;
       const int bs = p.bs[a];
       if (bs == 0) continue;
       const int pb = ti & 1, pph = (ti >> 1) & 1;
       ++ti;
-      // pool2 state of this thread's dX row: independent of the MMAs, fetched up front
+      // pool2 state of this thread's dX row: independent of the MMAs, loaded up front and only
+      // inspected in the dX epilogue, so the loads stay in flight during the chunk loop
       const int k = kt * 128 + row;
-      bool pos[NB];
-      uint8_t amr[NB];
+      float p2v[NB];
+      uint32_t amw[NB / 4];
 #pragma unroll
-      for (int r = 0; r < NB; ++r) {
-        const int64_t s = (int64_t)a * p.B + r;
-        pos[r] = r < bs ? p.p2[s * p.F + k] > 0.f : false;
-        amr[r] = r < bs ? p.am2[s * p.F + k] : 0;
+      for (int r = 0; r < NB; ++r) p2v[r] = r < bs ? __ldg(p.p2 + ((int64_t)a * p.B + r) * p.F + k) : 0.f;
+#pragma unroll
+      for (int r4 = 0; r4 < NB / 4; ++r4) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = 4 * r4 + u;
+          const uint32_t b8 = r < bs ? __ldg(p.am2 + ((int64_t)a * p.B + r) * p.F + k) : 0u;
+          w |= b8 << (8 * u);
+        }
+        amw[r4] = w;
       }
       for (int c = 0; c < nch; ++c, ++it) {
         const int st = it % BW_NST, buf = it & 1, gph = (it >> 1) & 1;
         uint8_t* sw = smem + st * BW_STAGE;
         tc::mbar_wait(gfull + buf, gph);
         tc::tc_fence_after();
-        for (int j = 0; j < 4; ++j) {
-          float v[32];
-          const uint32_t tg = tbase + ((uint32_t)(qd * 32) << 16) + buf * 128 + 32 * j;
-          tc::tmem_ld16(tg, *reinterpret_cast<float(*)[16]>(v));
-          tc::tmem_ld16(tg + 16, *reinterpret_cast<float(*)[16]>(v + 16));
-          uint8_t* rowp = sw + j * 16384 + row * 128;
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {  // 32-byte granule g of the row sits at g ^ (row % 4) (ATOM_32B)
-            float4* w4 = reinterpret_cast<float4*>(rowp + ((g ^ (row & 3)) << 5));
-#pragma unroll
-            for (int hq = 0; hq < 2; ++hq) {
-              float4 w = w4[hq];
-              w.x -= p.lr * v[8 * g + 4 * hq];
-              w.y -= p.lr * v[8 * g + 4 * hq + 1];
-              w.z -= p.lr * v[8 * g + 4 * hq + 2];
-              w.w -= p.lr * v[8 * g + 4 * hq + 3];
-              w4[hq] = w;
-            }
-          }
-        }
-        tc::tc_fence_before();
-        tc::mbar_arrive(gempty + buf);  // G buffer drained
-        if (kt == 0) {  // bias: b1[n] -= η Σ_r dh[r][n], from the stage's dhᵀ chunk (ATOM_32B)
+        if (kt == 0) {  // bias: b1[n] -= η Σ_r dh[r][n], from the stage's dh chunk (ATOM_32B)
           const int n = 128 * c + row, nn = row & 31;
-          const uint8_t* dq = sw + BW_W + BW_DH + (row >> 5) * 4096 + (nn & 7) * 4;
+          const uint8_t* dq = sw + BW_W + (row >> 5) * 4096 + (nn & 7) * 4;
           float g = 0.f;
           for (int r = 0; r < bs; ++r) g += *reinterpret_cast<const float*>(dq + r * 128 + (((nn >> 3) ^ (r & 3)) << 5));
           p.bdst[(int64_t)a * p.P_pad + n] = p.bsrc[(int64_t)a * p.bstride * p.wmul + n] - p.lr * g;
         }
-        tc::fence_async_smem();  // generic-proxy writes -> TMA store
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == 2 && tc::elect_one()) {
-          for (int j = 0; j < 4; ++j) tc::tma_store_3d(&mapWdst, sw + j * 16384, 128 * kt + 32 * j, 128 * c, a);
-          tc::tma_store_commit_wait();  // the stage may be refilled once the store has read it
-          tc::mbar_arrive(empty + st);
+        for (int j = 0; j < 4; ++j, ++oi) {
+          uint8_t* ob = smem + BW_OUT + (oi & 1) * 16384;
+          if (storer) tc::bulk_wait_read<1>();  // the store issued from this buffer two sub-chunks ago has read it
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          float v[32];
+          const uint32_t tg = tbase + ((uint32_t)(qd * 32) << 16) + buf * 128 + 32 * j;
+          tc::tmem_ld16(tg, *reinterpret_cast<float(*)[16]>(v));
+          tc::tmem_ld16(tg + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+          const uint8_t* rowp = sw + j * 16384 + row * 128;
+          uint8_t* orow = ob + row * 128;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {  // 32-byte granule g of the row sits at g ^ (row % 4) (ATOM_32B)
+            const int off = (g ^ (row & 3)) << 5;
+#pragma unroll
+            for (int hq = 0; hq < 2; ++hq) {
+              float4 w = reinterpret_cast<const float4*>(rowp + off)[hq];
+              w.x -= p.lr * v[8 * g + 4 * hq];
+              w.y -= p.lr * v[8 * g + 4 * hq + 1];
+              w.z -= p.lr * v[8 * g + 4 * hq + 2];
+              w.w -= p.lr * v[8 * g + 4 * hq + 3];
+              reinterpret_cast<float4*>(orow + off)[hq] = w;
+            }
+          }
+          tc::fence_async_smem();  // generic-proxy writes -> TMA store
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (storer) {
+            tc::tma_store_3d(&mapWdst, ob, 128 * kt + 32 * j, 128 * c, a);
+            tc::bulk_commit();
+          }
         }
+        tc::tc_fence_before();
+        tc::mbar_arrive(gempty + buf);  // G buffer drained
+        tc::mbar_arrive(empty + st);    // this thread is done reading the stage
       }
       // dX epilogue: dp2 -> pool2 / ReLU backward -> dY2 (every cell of the 2x2 window written)
       tc::mbar_wait(dxfull + pb, pph);
@@ -581,8 +593,8 @@ __global__ void __launch_bounds__(192, 1)
       for (int r = 0; r < NB; ++r) {
         if (r >= bs) break;
         const int64_t s = (int64_t)a * p.B + r;
-        const float g = pos[r] ? v[r] : 0.f;
-        const int am = amr[r];
+        const float g = p2v[r] > 0.f ? v[r] : 0.f;
+        const int am = (amw[r >> 2] >> (8 * (r & 3))) & 0xff;
         float* d = p.dY2 + ((s * H1 + 2 * ph) * W1 + 2 * pw) * p.C2 + cc;
         d[0] = am == 0 ? g : 0.f;
         d[p.C2] = am == 1 ? g : 0.f;
@@ -591,6 +603,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   }
+  if (warp == 2 && lane == 0) tc::bulk_wait_all();  // smem must outlive the last stores
   tc::tc_fence_before();
   __syncthreads();
   pdl_trigger();
@@ -701,14 +714,11 @@ int fc1_bwd_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t w
                int64_t wclients_dst, const float* dh, const float* p2, const uint8_t* am2, int64_t slots, float* dY2,
                cudaStream_t st) {
   const CnnDims& d = L.d;
-  CUtensorMap mws, mwd, mdh, mdht, mx;
+  CUtensorMap mws, mwd, mdht, mx;
   uint64_t dws[3] = {(uint64_t)d.F, (uint64_t)d.HID, (uint64_t)wclients_src};
   uint64_t dwd[3] = {(uint64_t)d.F, (uint64_t)d.HID, (uint64_t)wclients_dst};
   uint64_t sww[2] = {(uint64_t)d.F * 4, (uint64_t)L.P_pad * 4};
   uint32_t bww[3] = {32, 128, 1};
-  uint64_t dd[3] = {(uint64_t)d.HID, (uint64_t)slots, 1};
-  uint64_t sd[2] = {(uint64_t)d.HID * 4, (uint64_t)d.HID * 4 * slots};
-  uint32_t bd[3] = {32, NB, 1};
   uint64_t dh3[3] = {32, (uint64_t)slots, (uint64_t)d.HID / 32};
   uint64_t sh3[2] = {(uint64_t)d.HID * 4, 128};
   uint32_t bh3[3] = {32, NB, 4};
@@ -716,7 +726,7 @@ int fc1_bwd_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t w
   uint64_t sx3[2] = {(uint64_t)d.F * 4, 128};
   uint32_t bx3[3] = {32, NB, 4};
   if (!tmap_encode(&mws, wsrc + L.o_f1w, 3, dws, sww, bww, 2) || !tmap_encode(&mwd, slots_w + L.o_f1w, 3, dwd, sww, bww, 2) ||
-      !tmap_encode(&mdh, dh, 3, dd, sd, bd, 1) || !tmap_encode(&mdht, dh, 3, dh3, sh3, bh3, 2) ||
+      !tmap_encode(&mdht, dh, 3, dh3, sh3, bh3, 2) ||
       !tmap_encode(&mx, p2, 3, dx3, sx3, bx3, 2))
     return -1;
   static bool attr = false;
@@ -724,7 +734,7 @@ int fc1_bwd_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t w
   BwArgs p{wa.bs, wa.A, wa.B, d.HID, d.F, wa.first ? 0 : 1, d.H2, d.W2, d.C2, p2, am2, dY2,
            wsrc + L.o_f1b, L.P_pad, slots_w + L.o_f1b, L.P_pad, dh, wa.lr};
   const int tiles = wa.A * (d.F / 128);
-  launch_pdl(wa.pdl, k_fc1_bwd_tc, dim3(tiles < wa.sms ? tiles : wa.sms), 192, BW_SMEM, st, mws, mwd, mdh, mdht, mx, p);
+  launch_pdl(wa.pdl, k_fc1_bwd_tc, dim3(tiles < wa.sms ? tiles : wa.sms), 192, BW_SMEM, st, mws, mwd, mdht, mx, p);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -31,7 +31,8 @@ __global__ void probe(const float* A, const float* Bm, float* D, uint32_t lbo, u
   for (int e = t; e < N * 32; e += blockDim.x) {
     int n = e / 32, k = e % 32;   // B(n,k)
     float v = Bm[n * 32 + k];
-    if (!BMN) *(float*)(sb + sw128(n, k / 4) + (k % 4) * 4) = v;
+    if (BMN == 0) *(float*)(sb + sw128(n, k / 4) + (k % 4) * 4) = v;
+    else if (BMN == 2) *(float*)(sb + sw128_32b(n, k * 4)) = v;  // K-major rows in the BASE32B pattern
     else {
       int chunk = n / 32, nn = n % 32;  // MN chunk of 32 elements
       *(float*)(sb + chunk * lbo + sw128_32b(k, nn * 4)) = v;
@@ -48,11 +49,12 @@ __global__ void probe(const float* A, const float* Bm, float* D, uint32_t lbo, u
   tc::tc_fence_after();
   uint32_t tb = tslot;
   if (t == 0) {
-    constexpr uint32_t ID = tc::idesc_tf32(128, N, 0, BMN);
+    constexpr uint32_t ID = tc::idesc_tf32(128, N, 0, BMN == 1 ? 1 : 0);
     for (int k = 0; k < 4; ++k) {
       uint64_t ad = tc::sdesc(tc::smem_u32(sa) + k * 32, 0, 1024, tc::kSW128);
-      uint64_t bd = BMN ? tc::sdesc(tc::smem_u32(sb) + k * 1024, lbo, sbo, 1)
-                        : tc::sdesc(tc::smem_u32(sb) + k * 32, 0, 1024, tc::kSW128);
+      uint64_t bd = BMN == 1 ? tc::sdesc(tc::smem_u32(sb) + k * 1024, lbo, sbo, 1)
+                  : BMN == 2 ? tc::sdesc(tc::smem_u32(sb) + k * 32, lbo, sbo, 1)
+                             : tc::sdesc(tc::smem_u32(sb) + k * 32, 0, 1024, tc::kSW128);
       tc::mma_tf32(tb, ad, bd, ID, k > 0);
     }
     tc::mma_commit(&bar);
@@ -74,7 +76,7 @@ __global__ void probe(const float* A, const float* Bm, float* D, uint32_t lbo, u
 template <int N, int BMN>
 void run(uint32_t lbo, uint32_t sbo) {
   float *A, *Bm, *D;
-  cudaMallocManaged(&A, 128 * 32 * 4);
+  if (cudaMallocManaged(&A, 128 * 32 * 4) != cudaSuccess) { printf("context dead\n"); exit(1); }
   cudaMallocManaged(&Bm, N * 32 * 4);
   cudaMallocManaged(&D, 128 * N * 4);
   for (int i = 0; i < 128 * 32; ++i) A[i] = (float)((i * 37 % 17) - 8) / 8.f;
@@ -95,7 +97,13 @@ void run(uint32_t lbo, uint32_t sbo) {
   cudaFree(A); cudaFree(Bm); cudaFree(D);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  setvbuf(stdout, nullptr, _IONBF, 0);
+  if (argc > 1) {  // one K-major BASE32B variant per process (a bad descriptor faults the context)
+    cudaFuncSetAttribute(probe<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    run<32, 2>((uint32_t)atoi(argv[1]), (uint32_t)atoi(argv[2]));
+    return 0;
+  }
   cudaFuncSetAttribute(probe<64, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   cudaFuncSetAttribute(probe<32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   cudaFuncSetAttribute(probe<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
