@@ -29,7 +29,7 @@ namespace flb {
 const char* const kKindName[K_NKINDS] = {
     "pack", "conv1_fwd", "pool1", "conv2_fwd", "pool2", "fc1_fwd", "head_fc2_ce", "fc1_dx", "unpool2",
     "fc1_dw_sgd", "conv2_dx", "unpool1", "conv2_dw", "conv2_dw_reduce_sgd", "conv1_dw", "conv1_dw_reduce_sgd",
-    "logreg_client", "fedavg_accum"};
+    "logreg_client", "fedavg_accum", "lstm_step"};
 
 // ---------------------------------------------------------------- layouts
 static int64_t up32(int64_t x) { return (x + 31) / 32 * 32; }
@@ -46,6 +46,7 @@ bool make_layout(int model, Layout* L) {
     for (int64_t i = 0; i < 7850; ++i) L->canon_of[(size_t)i] = i;
     return true;
   }
+  if (model == FL_MODEL_CHAR_LSTM) return lstm_layout(L);
   if (model != FL_MODEL_CNN_CIFAR && model != FL_MODEL_CNN_SPEECH) return false;
   CnnDims& d = L->d;
   if (model == FL_MODEL_CNN_CIFAR) { d.cin = 3; d.H0 = 32; d.W0 = 32; d.HID = 512; d.NCLS = 10; }
@@ -212,6 +213,7 @@ struct fl_ctx {
   int64_t sidx_cap = 0, bs_cap = 0, bpre_cap = 0;
   WaveSched ws;
   CnnBufs cb;
+  LstmBufs lb;
   int64_t cb_slots_cap = 0, cb_part_cap = 0;
 
   // pinned host staging of the per-round tables
@@ -276,7 +278,7 @@ static fl_status set_err(fl_ctx* c, fl_status s, const char* fmt, ...) {
   } while (0)
 
 static bool model_supported(int m) {
-  return m == FL_MODEL_LOGREG || m == FL_MODEL_CNN_CIFAR || m == FL_MODEL_CNN_SPEECH;
+  return m == FL_MODEL_LOGREG || m == FL_MODEL_CNN_CIFAR || m == FL_MODEL_CNN_SPEECH || m == FL_MODEL_CHAR_LSTM;
 }
 
 extern "C" {
@@ -330,7 +332,8 @@ void fl_round_destroy(fl_ctx* c) {
                   c->d_ystage, c->d_src_row, c->d_n, c->d_steps, c->d_slot_off, c->ws.d_sidx, c->ws.d_bs, c->ws.d_bpre,
                   c->cb.a1, c->cb.p1, c->cb.a2, c->cb.p2, c->cb.h, c->cb.dh, c->cb.am1, c->cb.am2, c->cb.dp2,
                   c->cb.dY2, c->cb.dp1, c->cb.dY1, c->cb.part1, c->cb.part2, c->cb.xplanar, c->cb.fc1_part, c->cb.c1wt, c->cb.c1wt_g,
-                  c->cb.dz};
+                  c->cb.dz, c->lb.xp, c->lb.G0, c->lb.G1, c->lb.dpre, c->lb.C0, c->lb.C1, c->lb.H0, c->lb.H1,
+                  c->lb.dX, c->lb.E, c->lb.dE, c->lb.dhT};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_tab) cudaFreeHost(c->h_tab);
@@ -364,7 +367,9 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   fl_ctx* c = new fl_ctx();
   c->cfg = *cfg;
   make_layout(cfg->model, &c->L);
-  if (pop->feature_dim != c->L.D_in) {
+  // the LSTM's 80 one-byte characters travel as 20 four-byte words
+  if (pop->feature_dim != (c->L.model == FL_MODEL_CHAR_LSTM ? 4 * c->L.D_in : c->L.D_in) ||
+      (c->L.model == FL_MODEL_CHAR_LSTM && cfg->batch_size != 4)) {
     delete c;
     return FL_ERR_INVALID;
   }
@@ -626,6 +631,18 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
     CK(grow_dev(c->d_ystage, c->ystage_cap, R));
   }
   const bool cnn = (L.model == FL_MODEL_CNN_CIFAR || L.model == FL_MODEL_CNN_SPEECH);
+  const bool lstm = L.model == FL_MODEL_CHAR_LSTM;
+  if (lstm && K * B > c->lb.slots) {  // wave 0 has every local client active
+    LstmBufs& b = c->lb;
+    float** bufs[] = {&b.xp, &b.G0, &b.G1, &b.dpre, &b.C0, &b.C1, &b.H0, &b.H1, &b.dX, &b.E, &b.dE, &b.dhT};
+    const int kind[] = {0, 0, 0, 0, 1, 1, 1, 1, 2, 3, 3, 4};
+    for (int i = 0; i < 12; ++i) {
+      if (*bufs[i]) cudaFree(*bufs[i]);
+      *bufs[i] = nullptr;
+      CK(cudaMalloc(bufs[i], sizeof(float) * lstm_act_floats(K * B, kind[i])));
+    }
+    b.slots = K * B;
+  }
   if (cnn && K > 0) {
     CnnBufs& b = c->cb;
     const CnnDims& d = L.d;
@@ -776,6 +793,19 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
         if (ws.gn[(size_t)g] == 0 || gst[(size_t)g] == st) continue;
         CK(cudaEventRecord(c->ev_join[(size_t)g], gst[(size_t)g]));
         CK(cudaStreamWaitEvent(st, c->ev_join[(size_t)g], 0));
+      }
+    } else if (lstm) {
+      for (int64_t k = 0; k < ws.n_waves; ++k) {
+        int64_t sum_bs = 0;
+        for (int32_t a = 0; a < ws.A[(size_t)k]; ++a) sum_bs += h_bs[ws.bs_off[(size_t)k] + a];
+        WaveArgs wa{ws.A[(size_t)k], (int)B, k == 0, ws.d_sidx + ws.slot_off[(size_t)k], ws.d_bs + ws.bs_off[(size_t)k],
+                    c->cfg.lr, sum_bs, &c->prof, true, K, true, ws.d_bpre + ws.bs_off[(size_t)k] + k, 148};
+        c->prof.begin(st);
+        const int nl = lstm_wave(L, wa, reinterpret_cast<const uint8_t*>(c->d_xpack), c->d_ypack, c->d_theta,
+                                 c->d_slots, c->lb, st);
+        if (nl < 0) return set_err(c, FL_ERR_CUDA, "lstm wave %lld launch failed", (long long)k);
+        c->prof.end(K_LSTM, 381.5e6 * (double)sum_bs, 2.0 * 4.0 * ws.A[(size_t)k] * L.P_pad, st);
+        tl += nl;
       }
     } else {
       c->prof.begin(st);

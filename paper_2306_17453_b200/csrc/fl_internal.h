@@ -10,6 +10,8 @@
 #include <utility>
 #include <vector>
 
+#include "../../include/fl.h"
+
 namespace flb {
 
 // Programmatic dependent launch: the kernel may begin while its stream predecessor drains;
@@ -54,6 +56,11 @@ struct CnnDims {
 //   c1w [C1][5][5][cpad]  c1b [C1]  c2w [C2][5][5][C1]  c2b [C2]
 //   f1w [HID][H2][W2][C2] f1b [HID] f2w [NCLS][HID]     f2b [NCLS]
 // logreg: w [10][784] b [10].   LSTM: canonical order (see lstm kernels).
+// char-LSTM parameter offsets (canonical torch order, every tensor 128-byte aligned)
+struct LstmOff {
+  int64_t emb = 0, wih[2] = {0, 0}, whh[2] = {0, 0}, bih[2] = {0, 0}, bhh[2] = {0, 0}, wfc = 0, bfc = 0;
+};
+
 struct Layout {
   int model = -1;
   int64_t P = 0;      // canonical parameter count
@@ -62,6 +69,7 @@ struct Layout {
   int D_pack = 0;     // packed per-sample floats (NHWC4 for CNN)
   CnnDims d{};
   int64_t o_c1w = 0, o_c1b = 0, o_c2w = 0, o_c2b = 0, o_f1w = 0, o_f1b = 0, o_f2w = 0, o_f2b = 0;
+  LstmOff lo;
   std::vector<int64_t> canon_of;  // [P_pad]: canonical index of each internal slot, -1 = padding
 };
 
@@ -121,7 +129,7 @@ CnnBufs cnn_group_view(const CnnBufs& b, const CnnDims& d, int B, int64_t base_c
 // tagged with its kernel class and the algorithmic FLOPs / bytes of that launch.
 enum KKind {
   K_PACK = 0, K_CONV1_FWD, K_POOL1, K_CONV2_FWD, K_POOL2, K_FC1_FWD, K_HEAD, K_FC1_DX, K_UNPOOL2, K_FC1_DW,
-  K_CONV2_DX, K_UNPOOL1, K_CONV2_DW, K_CONV2_DWR, K_CONV1_DW, K_CONV1_DWR, K_LOGREG, K_FEDAVG, K_NKINDS
+  K_CONV2_DX, K_UNPOOL1, K_CONV2_DW, K_CONV2_DWR, K_CONV1_DW, K_CONV1_DWR, K_LOGREG, K_FEDAVG, K_LSTM, K_NKINDS
 };
 extern const char* const kKindName[K_NKINDS];
 struct KRec {
@@ -232,5 +240,19 @@ int fedavg_accum_partial(const float* slots, int64_t stride, const int64_t* n, i
                          const float* theta_g, double* S, cudaStream_t st);
 int fedavg_finalize(const double* S, int64_t P, const float* theta_g, const double* Ndev, float* out,
                     cudaStream_t st);
+
+// ---------------------------------------------------------------- char-LSTM (k_lstm.cu)
+// Per-slot activations of one wave (slot s = a*B + r; B must be 4): input projections xp,
+// post-activation gates G0/G1, cell/hidden states C/H [T+1] (index 0 = zero state), gate
+// pre-activation gradients dpre, layer-1 input gradient dX, embeddings E, dE, dL/dh_T.
+struct LstmBufs {
+  int64_t slots = 0;
+  float *xp = nullptr, *G0 = nullptr, *G1 = nullptr, *C0 = nullptr, *C1 = nullptr, *H0 = nullptr, *H1 = nullptr;
+  float *dpre = nullptr, *dX = nullptr, *E = nullptr, *dE = nullptr, *dhT = nullptr;
+};
+bool lstm_layout(Layout* L);
+int64_t lstm_act_floats(int64_t S, int which);  // 0: [S][T][G] 1: [S][T+1][H] 2: [S][T][H] 3: [S][T][E] 4: [S][H]
+int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const int32_t* ypack, const float* theta_g,
+              float* slots, LstmBufs& b, cudaStream_t st);
 
 }  // namespace flb

@@ -1,0 +1,548 @@
+// k_lstm.cu — local SGD of the LEAF char-LSTM (reading A10):
+// embed 80 -> 8, LSTM 8 -> 256, LSTM 256 -> 256 over T = 80 characters, fc 256 -> 80 on h_T,
+// softmax-CE (mean over |b|), BPTT, SGD (a7) — one wave = one step of every active client.
+//
+// The recurrences are the critical path (T dependent phases per layer, forward and
+// backward), so they run as thread-block CLUSTERS of 8 CTAs per client: each CTA keeps its
+// 128-row slice of W_hh (the i, f, g, o rows of 32 hidden units, padded k-major so the
+// forward and the transposed backward products are both bank-conflict free) resident in
+// shared memory for all T steps, owns those 32 units' cell state, and exchanges h_t (forward)
+// or the partial W_hhᵀ·dpre sums (backward, reduce-scatter) through distributed shared memory
+// with one cluster barrier per time step.  Everything that is not on the recurrence — the
+// input projections, dX of layer 2, every weight gradient (K = |b|·T) with the SGD step in its
+// epilogue, the embedding and the fc head — is batched per client outside the time loop.
+// Deterministic: every sum has a fixed order.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "dev_util.cuh"
+#include "fl_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace flb {
+namespace {
+
+constexpr int LT = 80, LH = 256, LG = 1024, LE = 8, LV = 80;
+constexpr int CL = 8;              // CTAs per client cluster
+constexpr int UPC = LH / CL;       // 32 hidden units per CTA
+constexpr int RPC = 4 * UPC;       // 128 gate rows per CTA
+constexpr int WP = RPC + 1;        // padded pitch of the k-major W_hh slice
+constexpr int REC_SMEM = (LH * WP + 2 * 4 * LH + 4 * RPC + 2 * CL * 4 * UPC) * 4;
+
+__device__ __forceinline__ float sigm(float v) { return 1.f / (1.f + __expf(-v)); }
+
+// global gate row of local row rl of cluster rank c: gate rl/32 (i, f, g, o), unit 32c + rl%32
+__device__ __forceinline__ int grow_of(int rl, int c) { return (rl >> 5) * LH + UPC * c + (rl & 31); }
+
+struct RecArgs {
+  const float* wsrc;   // client a's parameters at wsrc + a*wstride (θ_g on the first wave: stride 0)
+  int64_t wstride;
+  int64_t o_whh;       // W_hh [LG][LH]
+  int B;               // slots per client (batch)
+  const float* xp;     // fwd: [S][T][LG] input projection + both biases
+  float* G;            // [S][T][LG] post-activation gates (fwd writes, bwd reads)
+  float* C;            // [S][T+1][LH] cell states, C[., 0] = 0
+  float* H;            // [S][T+1][LH] hidden states, H[., 0] = 0
+  const float* ext;    // bwd: external dL/dh — ext_mode 0: [S][LH] at t = T-1 only; 1: [S][T][LH]
+  int ext_mode;
+  float* dpre;         // bwd: [S][T][LG] gradient of the gate pre-activations
+};
+
+__device__ void load_whh_slice(float* Wt, const float* W, int c) {
+  for (int e = threadIdx.x; e < RPC * LH; e += blockDim.x) {
+    const int rl = e / LH, k = e - rl * LH;
+    Wt[k * WP + rl] = W[(int64_t)grow_of(rl, c) * LH + k];
+  }
+}
+
+// Forward recurrence of one layer for one client (cluster of 8 CTAs, 256 threads each).
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 1) k_lstm_fwd(RecArgs p) {
+  pdl_wait();
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank(), a = blockIdx.x / CL, tid = threadIdx.x;
+  extern __shared__ float sm[];
+  float* Wt = sm;                  // [LH][WP]
+  float* hb = Wt + LH * WP;        // [2][4][LH] h_{t-1} of the 4 batch rows (ping-pong)
+  float* gs = hb + 2 * 4 * LH;     // [4][RPC] activated gates of this CTA's rows
+  load_whh_slice(Wt, p.wsrc + (int64_t)a * p.wstride + p.o_whh, c);
+  for (int e = tid; e < 2 * 4 * LH; e += 256) hb[e] = 0.f;
+  const int cb = tid >> 5, cu = tid & 31, unit = UPC * c + cu;  // cell owned by threads < 128
+  const int64_t cs = (int64_t)a * p.B + cb;
+  float cst = 0.f;
+  if (tid < 128) {
+    p.C[cs * (LT + 1) * LH + unit] = 0.f;
+    p.H[cs * (LT + 1) * LH + unit] = 0.f;
+  }
+  cl.sync();
+  const int rl = tid >> 1, b0 = (tid & 1) * 2, gr = grow_of(rl, c);
+  const int64_t s0 = (int64_t)a * p.B + b0;
+  for (int t = 0; t < LT; ++t) {
+    const int cur = t & 1, nxt = cur ^ 1;
+    const float* h0 = hb + (cur * 4 + b0) * LH;
+    const float* h1 = h0 + LH;
+    float acc0 = p.xp[(s0 * LT + t) * LG + gr], acc1 = p.xp[((s0 + 1) * LT + t) * LG + gr];
+#pragma unroll 8
+    for (int k = 0; k < LH; ++k) {
+      const float w = Wt[k * WP + rl];
+      acc0 = fmaf(w, h0[k], acc0);
+      acc1 = fmaf(w, h1[k], acc1);
+    }
+    const bool tg = (rl >> 5) == 2;  // the cell-candidate gate uses tanh
+    gs[b0 * RPC + rl] = tg ? tanhf(acc0) : sigm(acc0);
+    gs[(b0 + 1) * RPC + rl] = tg ? tanhf(acc1) : sigm(acc1);
+    __syncthreads();
+    if (tid < 128) {
+      const float ig = gs[cb * RPC + cu], fg = gs[cb * RPC + 32 + cu], gg = gs[cb * RPC + 64 + cu],
+                  og = gs[cb * RPC + 96 + cu];
+      cst = fg * cst + ig * gg;                 // c_t = f c_{t-1} + i g
+      const float h = og * tanhf(cst);          // h_t = o tanh(c_t)
+      p.C[(cs * (LT + 1) + t + 1) * LH + unit] = cst;
+      p.H[(cs * (LT + 1) + t + 1) * LH + unit] = h;
+      float* g = p.G + (cs * LT + t) * LG + unit;
+      g[0] = ig;
+      g[LH] = fg;
+      g[2 * LH] = gg;
+      g[3 * LH] = og;
+#pragma unroll
+      for (int r = 0; r < CL; ++r) cl.map_shared_rank(hb, r)[(nxt * 4 + cb) * LH + unit] = h;
+    }
+    cl.sync();  // h_t visible in every CTA; every CTA done reading h_{t-1}
+  }
+}
+
+// Backward (BPTT) recurrence of one layer for one client.
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 1) k_lstm_bwd(RecArgs p) {
+  pdl_wait();
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank(), a = blockIdx.x / CL, tid = threadIdx.x;
+  extern __shared__ float sm[];
+  float* Wt = sm;                           // [LH][WP]
+  float* ds = Wt + LH * WP + 2 * 4 * LH;    // [4][RPC] dpre of this CTA's rows
+  float* part = ds + 4 * RPC;               // [2][CL src][4][UPC] partial W_hhᵀ·dpre for this CTA's units
+  load_whh_slice(Wt, p.wsrc + (int64_t)a * p.wstride + p.o_whh, c);
+  const int cb = tid >> 5, cu = tid & 31, unit = UPC * c + cu;
+  const int64_t cs = (int64_t)a * p.B + cb;
+  float dcs = 0.f, dhr = 0.f;  // carried dL/dc_t and the recurrent dL/dh_t of this cell
+  cl.sync();
+  for (int t = LT - 1; t >= 0; --t) {
+    const int pb = t & 1;
+    if (tid < 128) {
+      float dh = dhr;
+      if (p.ext_mode == 0) dh += (t == LT - 1) ? p.ext[cs * LH + unit] : 0.f;
+      else dh += p.ext[(cs * LT + t) * LH + unit];
+      const float* g = p.G + (cs * LT + t) * LG + unit;
+      const float ig = g[0], fg = g[LH], gg = g[2 * LH], og = g[3 * LH];
+      const float ct = p.C[(cs * (LT + 1) + t + 1) * LH + unit], cp = p.C[(cs * (LT + 1) + t) * LH + unit];
+      const float tc = tanhf(ct);
+      const float dct = dcs + dh * og * (1.f - tc * tc);
+      const float di = dct * gg * ig * (1.f - ig), df = dct * cp * fg * (1.f - fg),
+                  dg = dct * ig * (1.f - gg * gg), dob = dh * tc * og * (1.f - og);
+      dcs = dct * fg;
+      ds[cb * RPC + cu] = di;
+      ds[cb * RPC + 32 + cu] = df;
+      ds[cb * RPC + 64 + cu] = dg;
+      ds[cb * RPC + 96 + cu] = dob;
+      float* d = p.dpre + (cs * LT + t) * LG + unit;
+      d[0] = di;
+      d[LH] = df;
+      d[2 * LH] = dg;
+      d[3 * LH] = dob;
+    }
+    __syncthreads();
+    {  // partial dL/dh_{t-1}[b][k] over this CTA's 128 rows, scattered to the unit's owner CTA
+      const int k = tid;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+      for (int r = 0; r < RPC; ++r) {
+        const float w = Wt[k * WP + r];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[b] = fmaf(w, ds[b * RPC + r], acc[b]);
+      }
+      float* dst = cl.map_shared_rank(part, k / UPC) + ((pb * CL + c) * 4) * UPC + (k % UPC);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) dst[b * UPC] = acc[b];
+    }
+    cl.sync();
+    if (tid < 128) {  // fixed source order
+      float s = 0.f;
+#pragma unroll
+      for (int src = 0; src < CL; ++src) s += part[((pb * CL + src) * 4 + cb) * UPC + cu];
+      dhr = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- batched per-client GEMM
+// C(a, i, j) = Σ_kk A(a, i, kk) · Bm(a, j, kk); an operand element (a, x, y) lives at
+// base + a·sa + (x / Tx)·sxr + (x % Tx)·sxt + (y / Ty)·syr + (y % Ty)·syt (Tx / Ty decompose
+// a (batch row, time) index; INT32_MAX = plain affine).  Epilogue: store (+ up to two bias
+// vectors over j) or SGD (dst = src − η·C).  64 x 64 tiles, 256 threads, fp32 FFMA.
+struct Opnd {
+  const float* base;
+  int64_t sa, sxr, sxt, syr, syt;
+  int Tx, Ty;
+  __device__ __forceinline__ float at(int a, int x, int y) const {
+    return base[a * sa + (int64_t)(x / Tx) * sxr + (int64_t)(x % Tx) * sxt + (int64_t)(y / Ty) * syr +
+                (int64_t)(y % Ty) * syt];
+  }
+};
+struct GemmArgs {
+  Opnd A, Bm;
+  int M, N, K;
+  int mode;                // 0: out = C + bias0 + bias1; 1: SGD
+  float* out;              // element (a, i, j) at out + a*o_sa + (i/To)*o_r + (i%To)*o_t + j*o_j
+  int64_t o_sa, o_r, o_t, o_j;
+  int To;
+  const float* bias0;      // mode 0: bias vectors over j of client a at bias + a*b_sa (may be null)
+  const float* bias1;
+  int64_t b_sa;
+  const float* src;        // mode 1: client a's current W at src + a*src_sa (same indexing as out)
+  int64_t src_sa;
+  float lr;
+};
+
+__global__ void __launch_bounds__(256) k_lstm_gemm(GemmArgs p) {
+  pdl_wait();
+  __shared__ float As[16][65], Bs[16][65];
+  const int a = blockIdx.z, i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < p.K; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int kk = e >> 6, x = e & 63;
+      As[kk][x] = (i0 + x < p.M && k0 + kk < p.K) ? p.A.at(a, i0 + x, k0 + kk) : 0.f;
+      Bs[kk][x] = (j0 + x < p.N && k0 + kk < p.K) ? p.Bm.at(a, j0 + x, k0 + kk) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) av[u] = As[kk][ty + 16 * u], bv[u] = Bs[kk][tx + 16 * u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(av[u], bv[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int i = i0 + ty + 16 * u, j = j0 + tx + 16 * v;
+      if (i >= p.M || j >= p.N) continue;
+      const int64_t o = (int64_t)(i / p.To) * p.o_r + (int64_t)(i % p.To) * p.o_t + (int64_t)j * p.o_j;
+      if (p.mode == 0) {
+        float r = acc[u][v];
+        if (p.bias0) r += p.bias0[a * p.b_sa + j];
+        if (p.bias1) r += p.bias1[a * p.b_sa + j];
+        p.out[a * p.o_sa + o] = r;
+      } else {
+        p.out[a * p.o_sa + o] = p.src[a * p.src_sa + o] - p.lr * acc[u][v];
+      }
+    }
+}
+
+// ---------------------------------------------------------------- embedding, layer-0 input
+// E[s][t][j] = emb[x_t][j]; Xp0[s][t][n] = W_ih0[n]·E[s][t] + b_ih0[n] + b_hh0[n].  One CTA per slot.
+struct EmbArgs {
+  const uint8_t* xpack;   // [R][LT] characters
+  const int32_t* sidx;    // slot -> packed row or -1
+  const float* wsrc;
+  int64_t wstride;
+  int64_t o_emb, o_wih0, o_bih0, o_bhh0;
+  int B;
+  float* E;               // [S][LT][LE]
+  float* xp;              // [S][LT][LG]
+};
+__global__ void __launch_bounds__(256) k_lstm_embed(EmbArgs p) {
+  pdl_wait();
+  __shared__ float Ws[LG * LE], bsum[LG], es[LT * LE];
+  const int s = blockIdx.x, a = s / p.B;
+  const float* w = p.wsrc + (int64_t)a * p.wstride;
+  for (int e = threadIdx.x; e < LG * LE; e += 256) Ws[e] = w[p.o_wih0 + e];
+  for (int e = threadIdx.x; e < LG; e += 256) bsum[e] = w[p.o_bih0 + e] + w[p.o_bhh0 + e];
+  const int row = p.sidx[s];
+  for (int e = threadIdx.x; e < LT * LE; e += 256) {
+    const int t = e / LE, j = e - t * LE;
+    const int ch = row >= 0 ? p.xpack[(int64_t)row * LT + t] : 0;  // padding rows: char 0 (dz = 0 there)
+    es[e] = w[p.o_emb + ch * LE + j];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < LT * LE; e += 256) p.E[(int64_t)s * LT * LE + e] = es[e];
+  for (int e = threadIdx.x; e < LT * LG; e += 256) {
+    const int t = e / LG, n = e - t * LG;
+    float acc = bsum[n];
+#pragma unroll
+    for (int j = 0; j < LE; ++j) acc = fmaf(Ws[n * LE + j], es[t * LE + j], acc);
+    p.xp[(int64_t)s * LT * LG + e] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- fc head + CE + fc SGD
+// One CTA per client: z = W_fc h2_T + b_fc, dz = (softmax − onehot)/|b| (0 past |b|),
+// dh2_T = W_fcᵀ dz, W_fc -= η Σ_r dz ⊗ h2_T, b_fc -= η Σ_r dz.
+struct HeadArgs {
+  const float* H1;        // [S][T+1][LH] layer-2 hidden states
+  const int32_t* ypack;
+  const int32_t* sidx;
+  const int32_t* bs;
+  const float* wsrc;
+  int64_t wstride;
+  float* dst;
+  int64_t P_pad, o_wfc, o_bfc;
+  int B;
+  float lr;
+  float* dhT;             // [S][LH]
+};
+__global__ void __launch_bounds__(256) k_lstm_head(HeadArgs p) {
+  pdl_wait();
+  __shared__ float hT[4][LH], dz[4][LV];
+  extern __shared__ float Wf[];  // [LV][LH] (80 KB, dynamic)
+  const int a = blockIdx.x, b = p.bs[a], tid = threadIdx.x;
+  const float* w = p.wsrc + (int64_t)a * p.wstride;
+  for (int e = tid; e < LV * LH; e += 256) Wf[e] = w[p.o_wfc + e];
+  for (int e = tid; e < 4 * LH; e += 256) {
+    const int r = e / LH, k = e - r * LH;
+    hT[r][k] = r < p.B ? p.H1[(((int64_t)a * p.B + r) * (LT + 1) + LT) * LH + k] : 0.f;
+  }
+  __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int idx = warp; idx < 4 * LV; idx += 8) {
+    const int r = idx / LV, q = idx - r * LV;
+    float s = 0.f;
+    for (int k = lane; k < LH; k += 32) s = fmaf(Wf[q * LH + k], hT[r][k], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) dz[r][q] = s + w[p.o_bfc + q];
+  }
+  __syncthreads();
+  if (tid < 4) {
+    const int r = tid;
+    if (r < b) {
+      const int y = p.ypack[p.sidx[a * p.B + r]];
+      float mx = dz[r][0];
+      for (int q = 1; q < LV; ++q) mx = fmaxf(mx, dz[r][q]);
+      float s = 0.f;
+      for (int q = 0; q < LV; ++q) s += expf(dz[r][q] - mx);
+      const float inv = 1.f / (float)b;
+      for (int q = 0; q < LV; ++q) dz[r][q] = (expf(dz[r][q] - mx) / s - (q == y ? 1.f : 0.f)) * inv;
+    } else {
+      for (int q = 0; q < LV; ++q) dz[r][q] = 0.f;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < p.B * LH; e += 256) {
+    const int r = e / LH, k = e - r * LH;
+    float s = 0.f;
+    if (r < 4)
+      for (int q = 0; q < LV; ++q) s = fmaf(Wf[q * LH + k], dz[r][q], s);
+    p.dhT[((int64_t)a * p.B + r) * LH + k] = s;
+  }
+  float* d = p.dst + (int64_t)a * p.P_pad;
+  for (int e = tid; e < LV * LH; e += 256) {
+    const int q = e / LH, k = e - q * LH;
+    float g = 0.f;
+    for (int r = 0; r < 4; ++r) g = fmaf(dz[r][q], hT[r][k], g);
+    d[p.o_wfc + e] = Wf[e] - p.lr * g;
+  }
+  if (tid < LV) {
+    float g = 0.f;
+    for (int r = 0; r < 4; ++r) g += dz[r][tid];
+    d[p.o_bfc + tid] = w[p.o_bfc + tid] - p.lr * g;
+  }
+}
+
+// ---------------------------------------------------------------- biases and embedding SGD
+// b_ih, b_hh -= η Σ_{r,t} dpre (both receive the same gradient).  grid (LG/256, A).
+__global__ void k_lstm_bias_sgd(const float* __restrict__ dpre, int B, const float* wsrc, int64_t wstride,
+                                float* dst, int64_t P_pad, int64_t o_bih, int64_t o_bhh, float lr) {
+  pdl_wait();
+  const int a = blockIdx.y, n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= LG) return;
+  float g = 0.f;
+  for (int r = 0; r < B; ++r) {
+    const float* d = dpre + (((int64_t)a * B + r) * LT) * LG + n;
+    for (int t = 0; t < LT; ++t) g += d[(int64_t)t * LG];
+  }
+  const float* w = wsrc + (int64_t)a * wstride;
+  float* o = dst + (int64_t)a * P_pad;
+  o[o_bih + n] = w[o_bih + n] - lr * g;
+  o[o_bhh + n] = w[o_bhh + n] - lr * g;
+}
+
+// emb[c][j] -= η Σ_{(r,t): x_{r,t} = c} dE[r][t][j], dE = dpre0 · W_ih0 (old).  One CTA per client.
+__global__ void k_lstm_emb_sgd(const float* __restrict__ dE, const uint8_t* __restrict__ xpack,
+                               const int32_t* __restrict__ sidx, int B, const float* wsrc, int64_t wstride,
+                               float* dst, int64_t P_pad, int64_t o_emb, float lr) {
+  pdl_wait();
+  const int a = blockIdx.x;
+  const float* w = wsrc + (int64_t)a * wstride;
+  float* o = dst + (int64_t)a * P_pad;
+  for (int e = threadIdx.x; e < LV * LE; e += blockDim.x) {
+    const int ch = e / LE, j = e - ch * LE;
+    float g = 0.f;
+    for (int r = 0; r < B; ++r) {
+      const int row = sidx[a * B + r];
+      const float* de = dE + (((int64_t)a * B + r) * LT) * LE + j;
+      for (int t = 0; t < LT; ++t) {
+        const int c = row >= 0 ? xpack[(int64_t)row * LT + t] : 0;
+        if (c == ch) g += de[t * LE];
+      }
+    }
+    o[o_emb + e] = w[o_emb + e] - lr * g;
+  }
+}
+
+Opnd affine(const float* base, int64_t sa, int64_t sx, int64_t sy) {
+  return Opnd{base, sa, 0, sx, 0, sy, 0x7fffffff, 0x7fffffff};
+}
+
+}  // namespace
+
+bool lstm_layout(Layout* L) {
+  L->model = FL_MODEL_CHAR_LSTM;
+  LstmOff& q = L->lo;
+  auto up32 = [](int64_t x) { return (x + 31) / 32 * 32; };
+  // canonical torch order: emb, wih0, whh0, bih0, bhh0, wih1, whh1, bih1, bhh1, wfc, bfc
+  const int64_t sz[11] = {LV * LE, LG * LE, LG * LH, LG, LG, LG * LH, LG * LH, LG, LG, LV * LH, LV};
+  int64_t* dst[11] = {&q.emb, &q.wih[0], &q.whh[0], &q.bih[0], &q.bhh[0], &q.wih[1], &q.whh[1],
+                      &q.bih[1], &q.bhh[1], &q.wfc, &q.bfc};
+  int64_t o = 0, c = 0;
+  L->canon_of.clear();
+  std::vector<int64_t> m;
+  for (int i = 0; i < 11; ++i) {
+    *dst[i] = o;
+    m.resize((size_t)up32(o + sz[i]), -1);
+    for (int64_t e = 0; e < sz[i]; ++e) m[(size_t)(o + e)] = c + e;
+    c += sz[i];
+    o = up32(o + sz[i]);
+  }
+  L->P = c;  // 819,920
+  L->P_pad = o;
+  L->canon_of = m;
+  L->D_in = LT / 4;   // 80 one-byte characters per sample, moved as 20 four-byte words
+  L->D_pack = LT / 4;
+  return true;
+}
+
+// One wave of local SGD for the char-LSTM (all active clients of the wave, one step each).
+int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const int32_t* ypack, const float* theta_g,
+              float* slots, LstmBufs& b, cudaStream_t st) {
+  const LstmOff& q = L.lo;
+  const int A = wa.A, B = wa.B;
+  const float* wbase = wa.first ? theta_g : slots;
+  const int64_t wstride = wa.first ? 0 : L.P_pad;
+  const float lr = wa.lr;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_lstm_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, REC_SMEM);
+    cudaFuncSetAttribute(k_lstm_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, REC_SMEM);
+    cudaFuncSetAttribute(k_lstm_head, cudaFuncAttributeMaxDynamicSharedMemorySize, LV * LH * 4);
+    attr = true;
+  }
+  const int64_t S_T1 = (int64_t)(LT + 1) * LH;  // per-slot stride of H / C
+  int n = 0;
+  auto gemm = [&](const GemmArgs& g) {
+    launch_pdl(wa.pdl, k_lstm_gemm, dim3((g.N + 63) / 64, (g.M + 63) / 64, A), 256, 0, st, g);
+    ++n;
+  };
+  const int M = B * LT;  // (batch row, time) rows per client
+  // ---- forward: embedding + layer-0 input projection, layer-0 recurrence
+  EmbArgs ea{xpack, wa.sidx, wbase, wstride, q.emb, q.wih[0], q.bih[0], q.bhh[0], B, b.E, b.xp};
+  launch_pdl(wa.pdl, k_lstm_embed, dim3(A * B), 256, 0, st, ea), ++n;
+  RecArgs r0{wbase, wstride, q.whh[0], B, b.xp, b.G0, b.C0, b.H0, nullptr, 0, nullptr};
+  launch_pdl(wa.pdl, k_lstm_fwd, dim3(A * CL), 256, REC_SMEM, st, r0), ++n;
+  // layer-1 input projection: xp[s][t] = W_ih1 · H0[s][t+1] + b_ih1 + b_hh1
+  {
+    GemmArgs g{};
+    g.A = Opnd{b.H0 + LH, (int64_t)B * S_T1, S_T1, LH, 0, 1, LT, 0x7fffffff};
+    g.Bm = affine(wbase + q.wih[1], wstride, LH, 1);
+    g.M = M, g.N = LG, g.K = LH, g.mode = 0;
+    g.out = b.xp, g.o_sa = (int64_t)M * LG, g.o_r = (int64_t)LT * LG, g.o_t = LG, g.o_j = 1, g.To = LT;
+    g.bias0 = wbase + q.bih[1], g.bias1 = wbase + q.bhh[1], g.b_sa = wstride;
+    gemm(g);
+  }
+  RecArgs r1{wbase, wstride, q.whh[1], B, b.xp, b.G1, b.C1, b.H1, nullptr, 0, nullptr};
+  launch_pdl(wa.pdl, k_lstm_fwd, dim3(A * CL), 256, REC_SMEM, st, r1), ++n;
+  // ---- head (fc SGD) and layer-1 BPTT
+  HeadArgs ha{b.H1, ypack, wa.sidx, wa.bs, wbase, wstride, slots, L.P_pad, q.wfc, q.bfc, B, lr, b.dhT};
+  launch_pdl(wa.pdl, k_lstm_head, dim3(A), 256, LV * LH * 4, st, ha), ++n;
+  RecArgs rb1{wbase, wstride, q.whh[1], B, nullptr, b.G1, b.C1, b.H1, b.dhT, 0, b.dpre};
+  launch_pdl(wa.pdl, k_lstm_bwd, dim3(A * CL), 256, REC_SMEM, st, rb1), ++n;
+  // dX of layer 1 (old W_ih1): dX[s][t][k] = Σ_n dpre[s][t][n] W_ih1[n][k]
+  {
+    GemmArgs g{};
+    g.A = affine(b.dpre, (int64_t)M * LG, LG, 1);
+    g.Bm = affine(wbase + q.wih[1], wstride, 1, LH);
+    g.M = M, g.N = LH, g.K = LG, g.mode = 0;
+    g.out = b.dX, g.o_sa = (int64_t)M * LH, g.o_r = (int64_t)LT * LH, g.o_t = LH, g.o_j = 1, g.To = LT;
+    gemm(g);
+  }
+  // layer-1 weight gradients + SGD: W_hh1 -= η Σ dpreᵀ H1[t], W_ih1 -= η Σ dpreᵀ H0[t+1]
+  for (int which = 0; which < 2; ++which) {
+    GemmArgs g{};
+    g.A = Opnd{b.dpre, (int64_t)M * LG, 0, 1, (int64_t)LT * LG, LG, 0x7fffffff, LT};  // (n, m = (r, t))
+    const float* hsrc = which == 0 ? b.H1 : b.H0 + LH;
+    g.Bm = Opnd{hsrc, (int64_t)B * S_T1, 0, 1, S_T1, LH, 0x7fffffff, LT};            // (k, m)
+    g.M = LG, g.N = LH, g.K = M, g.mode = 1;
+    const int64_t ow = which == 0 ? q.whh[1] : q.wih[1];
+    g.out = slots + ow, g.o_sa = L.P_pad, g.o_r = 0, g.o_t = LH, g.o_j = 1, g.To = 0x7fffffff;
+    g.src = wbase + ow, g.src_sa = wstride, g.lr = lr;
+    gemm(g);
+  }
+  launch_pdl(wa.pdl, k_lstm_bias_sgd, dim3(LG / 256, A), 256, 0, st, (const float*)b.dpre, B, wbase, wstride, slots,
+             L.P_pad, q.bih[1], q.bhh[1], lr), ++n;
+  // ---- layer-0 BPTT with the external gradient dX, then its gradients
+  RecArgs rb0{wbase, wstride, q.whh[0], B, nullptr, b.G0, b.C0, b.H0, b.dX, 1, b.dpre};
+  launch_pdl(wa.pdl, k_lstm_bwd, dim3(A * CL), 256, REC_SMEM, st, rb0), ++n;
+  {  // dE = dpre0 · W_ih0 (old), before W_ih0 is updated
+    GemmArgs g{};
+    g.A = affine(b.dpre, (int64_t)M * LG, LG, 1);
+    g.Bm = affine(wbase + q.wih[0], wstride, 1, LE);
+    g.M = M, g.N = LE, g.K = LG, g.mode = 0;
+    g.out = b.dE, g.o_sa = (int64_t)M * LE, g.o_r = (int64_t)LT * LE, g.o_t = LE, g.o_j = 1, g.To = LT;
+    gemm(g);
+  }
+  {  // W_hh0 -= η Σ dpre0ᵀ H0[t]
+    GemmArgs g{};
+    g.A = Opnd{b.dpre, (int64_t)M * LG, 0, 1, (int64_t)LT * LG, LG, 0x7fffffff, LT};
+    g.Bm = Opnd{b.H0, (int64_t)B * S_T1, 0, 1, S_T1, LH, 0x7fffffff, LT};
+    g.M = LG, g.N = LH, g.K = M, g.mode = 1;
+    g.out = slots + q.whh[0], g.o_sa = L.P_pad, g.o_r = 0, g.o_t = LH, g.o_j = 1, g.To = 0x7fffffff;
+    g.src = wbase + q.whh[0], g.src_sa = wstride, g.lr = lr;
+    gemm(g);
+  }
+  {  // W_ih0 -= η Σ dpre0ᵀ E
+    GemmArgs g{};
+    g.A = Opnd{b.dpre, (int64_t)M * LG, 0, 1, (int64_t)LT * LG, LG, 0x7fffffff, LT};
+    g.Bm = Opnd{b.E, (int64_t)M * LE, 0, 1, (int64_t)LT * LE, LE, 0x7fffffff, LT};
+    g.M = LG, g.N = LE, g.K = M, g.mode = 1;
+    g.out = slots + q.wih[0], g.o_sa = L.P_pad, g.o_r = 0, g.o_t = LE, g.o_j = 1, g.To = 0x7fffffff;
+    g.src = wbase + q.wih[0], g.src_sa = wstride, g.lr = lr;
+    gemm(g);
+  }
+  launch_pdl(wa.pdl, k_lstm_bias_sgd, dim3(LG / 256, A), 256, 0, st, (const float*)b.dpre, B, wbase, wstride, slots,
+             L.P_pad, q.bih[0], q.bhh[0], lr), ++n;
+  launch_pdl(wa.pdl, k_lstm_emb_sgd, dim3(A), 256, 0, st, (const float*)b.dE, xpack, wa.sidx, B, wbase, wstride, slots,
+             L.P_pad, q.emb, lr), ++n;
+  return cudaGetLastError() == cudaSuccess ? n : -1;
+}
+
+int64_t lstm_act_floats(int64_t S, int which) {
+  switch (which) {
+    case 0: return S * LT * LG;       // xp, G0, G1, dpre
+    case 1: return S * (LT + 1) * LH; // H0, H1, C0, C1
+    case 2: return S * LT * LH;       // dX
+    case 3: return S * LT * LE;       // E, dE
+    case 4: return S * LH;            // dhT
+  }
+  return 0;
+}
+
+}  // namespace flb

@@ -228,3 +228,38 @@ def test_C2_full_size_sampled():
         assert np.max(np.abs(tk_gpu[c] - tk_ref[i])) <= TOL_ROUND
     coords = rng.choice(len(theta), size=20000, replace=False)
     assert agg_err(out[coords], tk_gpu[:, coords], sizes[cohort]) <= TOL_AGG
+
+
+# char-LSTM (a6): ragged clients (1 to 3 steps of B = 4), full round vs the fp64 oracle
+LSTM_BLOCKS = [("emb", 640), ("w_ih0", 8192), ("w_hh0", 262144), ("b_ih0", 1024), ("b_hh0", 1024),
+               ("w_ih1", 262144), ("w_hh1", 262144), ("b_ih1", 1024), ("b_hh1", 1024), ("w_fc", 20480),
+               ("b_fc", 80)]
+
+
+def _lstm_block_errors(a, b):
+    out, o = {}, 0
+    for name, n in LSTM_BLOCKS:
+        out[name] = float(np.max(np.abs(a[o:o + n] - b[o:o + n])))
+        o += n
+    return out
+
+
+def test_lstm_round_small():
+    sizes = np.array([1, 3, 4, 5, 9], dtype=np.int64)
+    wl = synth.preset("C5", n_pop=len(sizes), n_cohort=len(sizes))
+    out, N, ref, Nref, tk, tk_gpu, theta = run_round(wl, sizes, np.arange(len(sizes)))
+    assert N == Nref == sizes.sum()
+    for i in range(len(sizes)):
+        e = np.max(np.abs(tk_gpu[i] - tk[i]))
+        assert e <= 1e-5, (i, _lstm_block_errors(tk_gpu[i], tk[i]))  # fp32 SIMT path: ~2e-7 measured
+    assert np.max(np.abs(out - ref)) <= TOL_ROUND
+    assert np.max(np.abs(out - theta)) > 1e-4  # the round moved the model
+
+
+def test_lstm_round_two_epochs_shuffled_host_population():
+    sizes = np.array([2, 4, 7, 13], dtype=np.int64)
+    wl = synth.preset("C5", n_pop=len(sizes), n_cohort=len(sizes), E=2, shuffle=1)
+    out, N, ref, Nref, tk, tk_gpu, theta = run_round(wl, sizes, np.arange(len(sizes)), on_device=False)
+    for i in range(len(sizes)):
+        assert np.max(np.abs(tk_gpu[i] - tk[i])) <= 1e-5, (i, _lstm_block_errors(tk_gpu[i], tk[i]))
+    assert np.max(np.abs(out - ref)) <= 1e-5
