@@ -20,6 +20,7 @@
 
 #include "dev_util.cuh"
 #include "fl_internal.h"
+#include "tc_common.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -30,8 +31,25 @@ constexpr int LT = 80, LH = 256, LG = 1024, LE = 8, LV = 80;
 constexpr int CL = 8;              // CTAs per client cluster
 constexpr int UPC = LH / CL;       // 32 hidden units per CTA
 constexpr int RPC = 4 * UPC;       // 128 gate rows per CTA
-constexpr int WP = RPC + 1;        // padded pitch of the k-major W_hh slice
-constexpr int REC_SMEM = (LH * WP + 2 * 4 * LH + 4 * RPC + 2 * CL * 4 * UPC) * 4;
+constexpr int WPF = LH + 4;       // fwd: row-major [RPC][LH] slice, pitch 260 (float4 rows, conflict-free)
+constexpr int WPB = RPC + 4;      // bwd: k-major [LH][RPC] slice, pitch 132 (float4 over rows, conflict-free)
+constexpr int REC_SMEM = (LH * WPB + 2 * 4 * LH + 4 * RPC + 2 * CL * 4 * UPC) * 4 + 64;  // + 2 mbarriers
+constexpr uint32_t XCH_BYTES = CL * 4 * UPC * 4;  // bytes one CTA receives per step (8 sources x 4 rows x 32)
+
+// Remote (DSMEM) store of one float into cluster CTA `rank`'s shared memory, completing
+// on that CTA's mbarrier: the consumer waits on its own barrier instead of a cluster-wide
+// barrier (whose release fence is a GPU-scope membar per step).
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_f32(uint32_t raddr, float v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr),
+               "r"(__float_as_uint(v)), "r"(rbar)
+               : "memory");
+}
+static_assert(RPC * WPF <= LH * WPB, "both slice layouts fit the same smem carve-out");
 
 __device__ __forceinline__ float sigm(float v) { return 1.f / (1.f + __expf(-v)); }
 
@@ -52,24 +70,29 @@ struct RecArgs {
   float* dpre;         // bwd: [S][T][LG] gradient of the gate pre-activations
 };
 
-__device__ void load_whh_slice(float* Wt, const float* W, int c) {
-  for (int e = threadIdx.x; e < RPC * LH; e += blockDim.x) {
-    const int rl = e / LH, k = e - rl * LH;
-    Wt[k * WP + rl] = W[(int64_t)grow_of(rl, c) * LH + k];
-  }
-}
-
-// Forward recurrence of one layer for one client (cluster of 8 CTAs, 256 threads each).
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 1) k_lstm_fwd(RecArgs p) {
+// Forward recurrence of one layer for one client (cluster of 8 CTAs, 512 threads each).
+// Thread (rl, kq) = (tid / 4, tid % 4) accumulates gate row rl over k-quarter kq for all 4
+// batch rows with 16 independent FMA chains (float4 loads of W and h); the 4 threads of a row
+// combine with two shuffles.  The next step's input projection is prefetched during the step.
+constexpr int FT = 512;
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(FT, 1) k_lstm_fwd(RecArgs p) {
   pdl_wait();
   cg::cluster_group cl = cg::this_cluster();
   const int c = (int)cl.block_rank(), a = blockIdx.x / CL, tid = threadIdx.x;
   extern __shared__ float sm[];
-  float* Wt = sm;                  // [LH][WP]
-  float* hb = Wt + LH * WP;        // [2][4][LH] h_{t-1} of the 4 batch rows (ping-pong)
+  float* Wr = sm;                  // [RPC][WPF]
+  float* hb = sm + LH * WPB;       // [2][4][LH] h_{t-1} of the 4 batch rows (ping-pong)
   float* gs = hb + 2 * 4 * LH;     // [4][RPC] activated gates of this CTA's rows
-  load_whh_slice(Wt, p.wsrc + (int64_t)a * p.wstride + p.o_whh, c);
-  for (int e = tid; e < 2 * 4 * LH; e += 256) hb[e] = 0.f;
+  uint64_t* hbar = reinterpret_cast<uint64_t*>(sm + LH * WPB + 2 * 4 * LH + 4 * RPC + 2 * CL * 4 * UPC);  // [2]
+  {
+    const float* W = p.wsrc + (int64_t)a * p.wstride + p.o_whh;
+    for (int e = tid; e < RPC * LH / 4; e += FT) {
+      const int rl = e / (LH / 4), k4 = e - rl * (LH / 4);
+      *reinterpret_cast<float4*>(Wr + rl * WPF + 4 * k4) =
+          __ldg(reinterpret_cast<const float4*>(W + (int64_t)grow_of(rl, c) * LH) + k4);
+    }
+  }
+  for (int e = tid; e < 2 * 4 * LH; e += FT) hb[e] = 0.f;
   const int cb = tid >> 5, cu = tid & 31, unit = UPC * c + cu;  // cell owned by threads < 128
   const int64_t cs = (int64_t)a * p.B + cb;
   float cst = 0.f;
@@ -77,103 +100,190 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 1) k_lstm_fwd(
     p.C[cs * (LT + 1) * LH + unit] = 0.f;
     p.H[cs * (LT + 1) * LH + unit] = 0.f;
   }
+  const int rl = tid >> 2, kh = tid & 3, gr = grow_of(rl, c);
+  const int64_t s0 = (int64_t)a * p.B;
+  const float* xr = p.xp + s0 * LT * LG + gr;  // batch row b, step t at xr + (b*LT + t)*LG
+  float xn[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) xn[b] = kh == 0 ? xr[(int64_t)b * LT * LG] : 0.f;
+  if (tid == 0) {
+    tc::mbar_init(hbar, 1);
+    tc::mbar_init(hbar + 1, 1);
+    tc::fence_mbar_init();
+  }
+  // remote addresses of this cell's h slot in every CTA's two buffers and their barriers
+  uint32_t rh[CL], rbar[CL];
+  {
+    const uint32_t lh = tc::smem_u32(hb + cb * LH + unit), lb = tc::smem_u32(hbar);
+#pragma unroll
+    for (int r = 0; r < CL; ++r) rh[r] = mapa_u32(lh, r), rbar[r] = mapa_u32(lb, r);
+  }
   cl.sync();
-  const int rl = tid >> 1, b0 = (tid & 1) * 2, gr = grow_of(rl, c);
-  const int64_t s0 = (int64_t)a * p.B + b0;
+  const bool tg = (rl >> 5) == 2;  // the cell-candidate gate uses tanh
+  float sv[6];
   for (int t = 0; t < LT; ++t) {
     const int cur = t & 1, nxt = cur ^ 1;
-    const float* h0 = hb + (cur * 4 + b0) * LH;
-    const float* h1 = h0 + LH;
-    float acc0 = p.xp[(s0 * LT + t) * LG + gr], acc1 = p.xp[((s0 + 1) * LT + t) * LG + gr];
-#pragma unroll 8
-    for (int k = 0; k < LH; ++k) {
-      const float w = Wt[k * WP + rl];
-      acc0 = fmaf(w, h0[k], acc0);
-      acc1 = fmaf(w, h1[k], acc1);
+    if (tid == 0 && t + 1 < LT) tc::mbar_expect_tx(hbar + nxt, XCH_BYTES);  // h_t lands in buffer nxt
+    if (t > 0) tc::mbar_wait(hbar + cur, ((t - 1) >> 1) & 1);                // h_{t-1} from all 8 CTAs
+    float acc[4] = {xn[0], xn[1], xn[2], xn[3]};
+    if (kh == 0 && t + 1 < LT)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) xn[b] = xr[((int64_t)b * LT + t + 1) * LG];
+    // the 4 threads of a row take interleaved float4 columns (k = 16j + 4kq): their loads of the
+    // same W row and of h fall in distinct banks
+    const float* w = Wr + rl * WPF + 4 * kh;
+    const float* h = hb + cur * 4 * LH + 4 * kh;
+    float ax[4] = {0.f, 0.f, 0.f, 0.f}, ay[4] = {0.f, 0.f, 0.f, 0.f}, az[4] = {0.f, 0.f, 0.f, 0.f},
+          aw[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+    for (int k = 0; k < LH; k += 16) {
+      const float4 wv = *reinterpret_cast<const float4*>(w + k);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const float4 hv = *reinterpret_cast<const float4*>(h + b * LH + k);
+        ax[b] = fmaf(wv.x, hv.x, ax[b]);
+        ay[b] = fmaf(wv.y, hv.y, ay[b]);
+        az[b] = fmaf(wv.z, hv.z, az[b]);
+        aw[b] = fmaf(wv.w, hv.w, aw[b]);
+      }
     }
-    const bool tg = (rl >> 5) == 2;  // the cell-candidate gate uses tanh
-    gs[b0 * RPC + rl] = tg ? tanhf(acc0) : sigm(acc0);
-    gs[(b0 + 1) * RPC + rl] = tg ? tanhf(acc1) : sigm(acc1);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      acc[b] += (ax[b] + ay[b]) + (az[b] + aw[b]);
+      acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], 1);
+      acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], 2);
+    }
+    if (kh == 0)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) gs[b * RPC + rl] = tg ? tanhf(acc[b]) : sigm(acc[b]);
     __syncthreads();
     if (tid < 128) {
       const float ig = gs[cb * RPC + cu], fg = gs[cb * RPC + 32 + cu], gg = gs[cb * RPC + 64 + cu],
                   og = gs[cb * RPC + 96 + cu];
       cst = fg * cst + ig * gg;                 // c_t = f c_{t-1} + i g
-      const float h = og * tanhf(cst);          // h_t = o tanh(c_t)
-      p.C[(cs * (LT + 1) + t + 1) * LH + unit] = cst;
-      p.H[(cs * (LT + 1) + t + 1) * LH + unit] = h;
-      float* g = p.G + (cs * LT + t) * LG + unit;
-      g[0] = ig;
-      g[LH] = fg;
-      g[2 * LH] = gg;
-      g[3 * LH] = og;
+      const float hv = og * tanhf(cst);         // h_t = o tanh(c_t)
+      if (t + 1 < LT)
 #pragma unroll
-      for (int r = 0; r < CL; ++r) cl.map_shared_rank(hb, r)[(nxt * 4 + cb) * LH + unit] = h;
+        for (int r = 0; r < CL; ++r) st_async_f32(rh[r] + nxt * 4 * LH * 4, hv, rbar[r] + nxt * 8);
+      sv[0] = cst, sv[1] = hv, sv[2] = ig, sv[3] = fg, sv[4] = gg, sv[5] = og;
     }
-    cl.sync();  // h_t visible in every CTA; every CTA done reading h_{t-1}
+    __syncthreads();  // gs is rewritten by the next step
+    // No cluster barrier per step: a CTA cannot run ahead into a buffer still being read,
+    // because its next step needs every CTA's h_t, which each sends only after reading h_{t-1}.
+    if (tid < 128) {
+      p.C[(cs * (LT + 1) + t + 1) * LH + unit] = sv[0];
+      p.H[(cs * (LT + 1) + t + 1) * LH + unit] = sv[1];
+      float* g = p.G + (cs * LT + t) * LG + unit;
+      g[0] = sv[2];
+      g[LH] = sv[3];
+      g[2 * LH] = sv[4];
+      g[3 * LH] = sv[5];
+    }
   }
+  cl.sync();  // no CTA exits while a peer may still address its shared memory
 }
 
-// Backward (BPTT) recurrence of one layer for one client.
+// Backward (BPTT) recurrence of one layer for one client.  The cell owners prefetch the next
+// (earlier) step's gates, cell states and external gradient while the current step's
+// W_hhᵀ·dpre partials (thread k, float4 over rows) are formed and reduce-scattered.
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 1) k_lstm_bwd(RecArgs p) {
   pdl_wait();
   cg::cluster_group cl = cg::this_cluster();
   const int c = (int)cl.block_rank(), a = blockIdx.x / CL, tid = threadIdx.x;
   extern __shared__ float sm[];
-  float* Wt = sm;                           // [LH][WP]
-  float* ds = Wt + LH * WP + 2 * 4 * LH;    // [4][RPC] dpre of this CTA's rows
+  float* Wt = sm;                           // [LH][WPB] k-major
+  float* ds = sm + LH * WPB + 2 * 4 * LH;   // [RPC][4] dpre of this CTA's rows (4 batch rows contiguous)
   float* part = ds + 4 * RPC;               // [2][CL src][4][UPC] partial W_hhᵀ·dpre for this CTA's units
-  load_whh_slice(Wt, p.wsrc + (int64_t)a * p.wstride + p.o_whh, c);
+  uint64_t* pbar = reinterpret_cast<uint64_t*>(part + 2 * CL * 4 * UPC);  // [2] partials of a step landed
+  {
+    const float* W = p.wsrc + (int64_t)a * p.wstride + p.o_whh;
+    for (int e = tid; e < RPC * LH; e += 256) {
+      const int rl = e / LH, k = e - rl * LH;
+      Wt[k * WPB + rl] = __ldg(W + (int64_t)grow_of(rl, c) * LH + k);
+    }
+  }
   const int cb = tid >> 5, cu = tid & 31, unit = UPC * c + cu;
   const int64_t cs = (int64_t)a * p.B + cb;
   float dcs = 0.f, dhr = 0.f;  // carried dL/dc_t and the recurrent dL/dh_t of this cell
+  // per-step inputs of the cell owners, prefetched one step ahead
+  float nig = 0.f, nfg = 0.f, ngg = 0.f, nog = 0.f, nct = 0.f, ncp = 0.f, nex = 0.f;
+  auto fetch = [&](int t) {
+    const float* g = p.G + (cs * LT + t) * LG + unit;
+    nig = g[0], nfg = g[LH], ngg = g[2 * LH], nog = g[3 * LH];
+    nct = p.C[(cs * (LT + 1) + t + 1) * LH + unit];
+    ncp = p.C[(cs * (LT + 1) + t) * LH + unit];
+    nex = p.ext_mode == 0 ? ((t == LT - 1) ? p.ext[cs * LH + unit] : 0.f) : p.ext[(cs * LT + t) * LH + unit];
+  };
+  if (tid < 128) fetch(LT - 1);
+  float sd[4];
+  if (tid == 0) {
+    tc::mbar_init(pbar, 1);
+    tc::mbar_init(pbar + 1, 1);
+    tc::fence_mbar_init();
+  }
+  // this thread's partial (column k = tid) goes to unit owner k / UPC: remote slot + barrier
+  const uint32_t rpart = mapa_u32(tc::smem_u32(part + c * 4 * UPC + (tid % UPC)), tid / UPC);
+  const uint32_t rpbar = mapa_u32(tc::smem_u32(pbar), tid / UPC);
   cl.sync();
   for (int t = LT - 1; t >= 0; --t) {
     const int pb = t & 1;
+    if (tid == 0 && t > 0) tc::mbar_expect_tx(pbar + pb, XCH_BYTES);
     if (tid < 128) {
-      float dh = dhr;
-      if (p.ext_mode == 0) dh += (t == LT - 1) ? p.ext[cs * LH + unit] : 0.f;
-      else dh += p.ext[(cs * LT + t) * LH + unit];
-      const float* g = p.G + (cs * LT + t) * LG + unit;
-      const float ig = g[0], fg = g[LH], gg = g[2 * LH], og = g[3 * LH];
-      const float ct = p.C[(cs * (LT + 1) + t + 1) * LH + unit], cp = p.C[(cs * (LT + 1) + t) * LH + unit];
+      const float dh = dhr + nex;
+      const float ig = nig, fg = nfg, gg = ngg, og = nog, ct = nct, cp = ncp;
+      if (t > 0) fetch(t - 1);
       const float tc = tanhf(ct);
       const float dct = dcs + dh * og * (1.f - tc * tc);
       const float di = dct * gg * ig * (1.f - ig), df = dct * cp * fg * (1.f - fg),
                   dg = dct * ig * (1.f - gg * gg), dob = dh * tc * og * (1.f - og);
       dcs = dct * fg;
-      ds[cb * RPC + cu] = di;
-      ds[cb * RPC + 32 + cu] = df;
-      ds[cb * RPC + 64 + cu] = dg;
-      ds[cb * RPC + 96 + cu] = dob;
-      float* d = p.dpre + (cs * LT + t) * LG + unit;
-      d[0] = di;
-      d[LH] = df;
-      d[2 * LH] = dg;
-      d[3 * LH] = dob;
+      ds[cu * 4 + cb] = di;
+      ds[(32 + cu) * 4 + cb] = df;
+      ds[(64 + cu) * 4 + cb] = dg;
+      ds[(96 + cu) * 4 + cb] = dob;
+      sd[0] = di, sd[1] = df, sd[2] = dg, sd[3] = dob;
     }
     __syncthreads();
     {  // partial dL/dh_{t-1}[b][k] over this CTA's 128 rows, scattered to the unit's owner CTA
       const int k = tid;
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      float acc[4];
+      const float* w = Wt + k * WPB;
+      float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, q2 = q0, q3 = q0;  // 16 independent chains
 #pragma unroll 4
-      for (int r = 0; r < RPC; ++r) {
-        const float w = Wt[k * WP + r];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[b] = fmaf(w, ds[b * RPC + r], acc[b]);
+      for (int r = 0; r < RPC; r += 4) {
+        const float4 wv = *reinterpret_cast<const float4*>(w + r);
+        const float4 d0 = *reinterpret_cast<const float4*>(ds + (r + 0) * 4);
+        const float4 d1 = *reinterpret_cast<const float4*>(ds + (r + 1) * 4);
+        const float4 d2 = *reinterpret_cast<const float4*>(ds + (r + 2) * 4);
+        const float4 d3 = *reinterpret_cast<const float4*>(ds + (r + 3) * 4);
+        q0.x = fmaf(wv.x, d0.x, q0.x), q0.y = fmaf(wv.x, d0.y, q0.y), q0.z = fmaf(wv.x, d0.z, q0.z), q0.w = fmaf(wv.x, d0.w, q0.w);
+        q1.x = fmaf(wv.y, d1.x, q1.x), q1.y = fmaf(wv.y, d1.y, q1.y), q1.z = fmaf(wv.y, d1.z, q1.z), q1.w = fmaf(wv.y, d1.w, q1.w);
+        q2.x = fmaf(wv.z, d2.x, q2.x), q2.y = fmaf(wv.z, d2.y, q2.y), q2.z = fmaf(wv.z, d2.z, q2.z), q2.w = fmaf(wv.z, d2.w, q2.w);
+        q3.x = fmaf(wv.w, d3.x, q3.x), q3.y = fmaf(wv.w, d3.y, q3.y), q3.z = fmaf(wv.w, d3.z, q3.z), q3.w = fmaf(wv.w, d3.w, q3.w);
       }
-      float* dst = cl.map_shared_rank(part, k / UPC) + ((pb * CL + c) * 4) * UPC + (k % UPC);
+      acc[0] = (q0.x + q1.x) + (q2.x + q3.x);
+      acc[1] = (q0.y + q1.y) + (q2.y + q3.y);
+      acc[2] = (q0.z + q1.z) + (q2.z + q3.z);
+      acc[3] = (q0.w + q1.w) + (q2.w + q3.w);
+      if (t > 0)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) dst[b * UPC] = acc[b];
+        for (int b = 0; b < 4; ++b) st_async_f32(rpart + (pb * CL * 4 + b) * UPC * 4, acc[b], rpbar + pb * 8);
     }
-    cl.sync();
+    if (t > 0) tc::mbar_wait(pbar + pb, ((LT - 1 - t) >> 1) & 1);  // all 8 CTAs' partials for my units
     if (tid < 128) {  // fixed source order
       float s = 0.f;
 #pragma unroll
       for (int src = 0; src < CL; ++src) s += part[((pb * CL + src) * 4 + cb) * UPC + cu];
       dhr = s;
+      float* d = p.dpre + (cs * LT + t) * LG + unit;  // stored after the barrier (see k_lstm_fwd)
+      d[0] = sd[0];
+      d[LH] = sd[1];
+      d[2 * LH] = sd[2];
+      d[3 * LH] = sd[3];
     }
+    __syncthreads();  // ds is rewritten by the next step
   }
+  cl.sync();  // no CTA exits while a peer may still address its shared memory
 }
 
 // ---------------------------------------------------------------- batched per-client GEMM
@@ -457,7 +567,7 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
   EmbArgs ea{xpack, wa.sidx, wbase, wstride, q.emb, q.wih[0], q.bih[0], q.bhh[0], B, b.E, b.xp};
   launch_pdl(wa.pdl, k_lstm_embed, dim3(A * B), 256, 0, st, ea), ++n;
   RecArgs r0{wbase, wstride, q.whh[0], B, b.xp, b.G0, b.C0, b.H0, nullptr, 0, nullptr};
-  launch_pdl(wa.pdl, k_lstm_fwd, dim3(A * CL), 256, REC_SMEM, st, r0), ++n;
+  launch_pdl(wa.pdl, k_lstm_fwd, dim3(A * CL), FT, REC_SMEM, st, r0), ++n;
   // layer-1 input projection: xp[s][t] = W_ih1 · H0[s][t+1] + b_ih1 + b_hh1
   {
     GemmArgs g{};
@@ -469,7 +579,7 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
     gemm(g);
   }
   RecArgs r1{wbase, wstride, q.whh[1], B, b.xp, b.G1, b.C1, b.H1, nullptr, 0, nullptr};
-  launch_pdl(wa.pdl, k_lstm_fwd, dim3(A * CL), 256, REC_SMEM, st, r1), ++n;
+  launch_pdl(wa.pdl, k_lstm_fwd, dim3(A * CL), FT, REC_SMEM, st, r1), ++n;
   // ---- head (fc SGD) and layer-1 BPTT
   HeadArgs ha{b.H1, ypack, wa.sidx, wa.bs, wbase, wstride, slots, L.P_pad, q.wfc, q.bfc, B, lr, b.dhT};
   launch_pdl(wa.pdl, k_lstm_head, dim3(A), 256, LV * LH * 4, st, ha), ++n;
