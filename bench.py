@@ -355,7 +355,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None,
-                "dtype": "f32" if args.math == 1 else "tf32",
+                "dtype": "f32" if (args.math == 1 or wl.model == "lstm") else "tf32",
                 "precision_note": "tensor-core GEMM operands tf32, fp32 accumulate; fp32 master weights, SGD, "
                                   "softmax-CE; fp64 FedAvg accumulation",
                 "data": "synthetic (seeded, SURVEY §8d laws), device-resident",

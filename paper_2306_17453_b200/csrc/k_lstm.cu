@@ -295,9 +295,11 @@ struct Opnd {
   const float* base;
   int64_t sa, sxr, sxt, syr, syt;
   int Tx, Ty;
-  __device__ __forceinline__ float at(int a, int x, int y) const {
-    return base[a * sa + (int64_t)(x / Tx) * sxr + (int64_t)(x % Tx) * sxt + (int64_t)(y / Ty) * syr +
-                (int64_t)(y % Ty) * syt];
+  __device__ __forceinline__ int64_t xoff(int a, int x) const {
+    return a * sa + (Tx == 0x7fffffff ? (int64_t)x * sxt : (int64_t)(x / Tx) * sxr + (int64_t)(x % Tx) * sxt);
+  }
+  __device__ __forceinline__ int64_t yoff(int y) const {
+    return Ty == 0x7fffffff ? (int64_t)y * syt : (int64_t)(y / Ty) * syr + (int64_t)(y % Ty) * syt;
   }
 };
 struct GemmArgs {
@@ -321,11 +323,17 @@ __global__ void __launch_bounds__(256) k_lstm_gemm(GemmArgs p) {
   const int a = blockIdx.z, i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   float acc[4][4] = {};
+  // a thread loads tile row x = tid % 64 (fixed for the whole K loop) at k = tid / 64 + 4q
+  const int lx = threadIdx.x & 63, lk = threadIdx.x >> 6;
+  const bool va = i0 + lx < p.M, vb = j0 + lx < p.N;
+  const float* pa = p.A.base + (va ? p.A.xoff(a, i0 + lx) : 0);
+  const float* pb = p.Bm.base + (vb ? p.Bm.xoff(a, j0 + lx) : 0);
   for (int k0 = 0; k0 < p.K; k0 += 16) {
-    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
-      const int kk = e >> 6, x = e & 63;
-      As[kk][x] = (i0 + x < p.M && k0 + kk < p.K) ? p.A.at(a, i0 + x, k0 + kk) : 0.f;
-      Bs[kk][x] = (j0 + x < p.N && k0 + kk < p.K) ? p.Bm.at(a, j0 + x, k0 + kk) : 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int kk = lk + 4 * q, k = k0 + kk;
+      As[kk][lx] = (va && k < p.K) ? pa[p.A.yoff(k)] : 0.f;
+      Bs[kk][lx] = (vb && k < p.K) ? pb[p.Bm.yoff(k)] : 0.f;
     }
     __syncthreads();
 #pragma unroll
