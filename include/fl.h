@@ -24,7 +24,7 @@
  *    fixed world size (fixed client order, fp64 accumulation).
  *  - There is no CPU fallback: entry points that compute need a CUDA device
  *    (sm_100a) and return FL_ERR_CUDA without one.  Only fl_place_plan,
- *    fl_pack_plan, fl_n_params and fl_abi_version are host-only.
+ *    fl_pack_plan, fl_lb_fit, fl_n_params and fl_abi_version are host-only.
  */
 #ifndef FL_B200_H
 #define FL_B200_H
@@ -59,8 +59,13 @@ typedef enum {
  * count m = ceil(n/B) descending, ties by client id ascending (reading A15);
  * BU/LB append each client to the worker with the lowest load, ties to the
  * lowest worker id.  BU load = Σ m (L370); LB load = Σ Eq. 3
- * prediction a·m + b·ln(c·m) + d, clamped to >= 1e-12 (L380-388). */
-typedef enum { FL_PLACE_BU = 0, FL_PLACE_LB = 1, FL_PLACE_RR = 2, FL_PLACE_SRR = 3 } fl_policy;
+ * prediction a·m + b·ln(c·m) + d, clamped to >= 1e-12 (L380-388).
+ * FL_PLACE_LB_GPU is LB with one Eq. 3 fit per GPU (lb_coef = [world_size][4]):
+ * workers are ordered fastest-first by the predicted time of the cohort's largest
+ * client (L385-386), each client goes to the worker with the lowest predicted load
+ * Σ Eq. 3(coef[w], m), ties to the earlier worker in that order. */
+typedef enum { FL_PLACE_BU = 0, FL_PLACE_LB = 1, FL_PLACE_RR = 2, FL_PLACE_SRR = 3,
+               FL_PLACE_LB_GPU = 4 } fl_policy;
 
 typedef struct fl_ctx fl_ctx; /* opaque; owns device buffers, stream, events, NCCL comm */
 
@@ -130,6 +135,18 @@ fl_status fl_place_plan(int32_t policy, const int64_t* cohort_ids, int64_t n_coh
                         int32_t world_size, const double* lb_coef,
                         int64_t* out_ids, int64_t* out_off);
 
+/* LB's time model: least-squares fit of Eq. 3
+ * y = a·x + b·ln(c·x) + d to n >= 4 records (x[i] = batches m >= 1 of a trained
+ * client, y[i] = its measured training time, any unit).  Because
+ * b·ln(c·x) + d = b·ln x + (b·ln c + d), c is not identifiable: the fit
+ * returns c = 1 and the exact least-squares minimiser over (a, b, d) (Householder
+ * QR).  It is accepted if a >= 0 and it predicts > 0 over [min x, max x];
+ * otherwise the fallback is the line a·x + d with a >= 0, else the mean.
+ * coef_out[4] = (a, b, c, d); *kind_out = 0 Eq. 3, 1 line, 2 constant (nullable);
+ * *mse_out = mean squared residual (nullable).  FL_ERR_INVALID if n < 4 or x < 1. */
+fl_status fl_lb_fit(const double* x, const double* y, int64_t n, double* coef_out, int32_t* kind_out,
+                    double* mse_out);
+
 /* Ragged packer for one worker list ids[n]: seg_off[n+1] prefix sums of
  * n_samples in list order; steps[n] = E·ceil(n_k/B). */
 fl_status fl_pack_plan(const int64_t* ids, int64_t n, const int64_t* n_samples, int64_t n_clients,
@@ -184,6 +201,17 @@ fl_status fl_get_client_params(fl_ctx* ctx, int64_t client_id, float* out);
 /* Current θ_g (host float32[P], canonical) / replace it. */
 fl_status fl_get_global_params(fl_ctx* ctx, float* out);
 fl_status fl_set_global_params(fl_ctx* ctx, const float* params);
+
+/* LB timing records ("collects the training time of each client").  With
+ * records on, fl_train_clients records a CUDA event on a client's group stream after
+ * the wave in which its last SGD step runs; fl_get_client_times then returns, per
+ * local client in plan order, ids[i], m[i] = ceil(n/B) and t_ms[i] = device time from
+ * the end of staging to that event (the client's completion time on this GPU: clients
+ * train concurrently, so this is the time a client of that size costs the GPU's round).
+ * Arrays have room for n_local = clients placed on this rank; blocks until the round's
+ * training is done.  FL_ERR_STATE if no round was trained with records on. */
+fl_status fl_set_timing_records(fl_ctx* ctx, int32_t on);
+fl_status fl_get_client_times(fl_ctx* ctx, int64_t* ids, int64_t* m, double* t_ms, int64_t* n_local);
 
 /* Stats of the last fl_round. */
 fl_status fl_get_stats(fl_ctx* ctx, fl_round_stats* out);

@@ -66,6 +66,11 @@ def lib():
         L.orc_fedavg.argtypes = [_f64p, _i64p, C.c_int64, C.c_int64, _f64p, C.POINTER(C.c_int64)]
         L.orc_fedavg_eq12.restype = C.c_int
         L.orc_fedavg_eq12.argtypes = [_f64p, _i64p, C.c_int64, C.c_int64, _i64p, C.c_int64, _f64p]
+        L.orc_place_lb_gpu.restype = C.c_int
+        L.orc_place_lb_gpu.argtypes = [_i64p, C.c_int64, _i64p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                                       _i64p, _i64p]
+        L.orc_eq3_fit.restype = C.c_int
+        L.orc_eq3_fit.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_double)]
         _lib = L
     return _lib
 
@@ -103,6 +108,30 @@ def place(policy: str, cohort, n_samples, B: int, G: int, lb=None):
     if rc != 0:
         raise ValueError("invalid placement input")
     return ids, off
+
+
+def place_lb_gpu(cohort, n_samples, B: int, G: int, coef):
+    """LB with one Eq. 3 fit per worker, coef [G][4]. Returns (ids[K], off[G+1])."""
+    cohort, n_samples = _i64(cohort), _i64(n_samples)
+    coef = np.ascontiguousarray(coef, dtype=np.float64).reshape(G, 4)
+    ids = np.empty(len(cohort), dtype=np.int64)
+    off = np.empty(G + 1, dtype=np.int64)
+    rc = lib().orc_place_lb_gpu(cohort, len(cohort), n_samples, len(n_samples), B, G, coef.ctypes.data, ids, off)
+    if rc != 0:
+        raise ValueError("invalid placement input")
+    return ids, off
+
+
+def eq3_fit(m, t):
+    """Least-squares Eq. 3 fit: (coef[4], kind, mse); kind 0 Eq. 3, 1 line, 2 constant."""
+    m = np.ascontiguousarray(m, dtype=np.float64)
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    coef = np.empty(4, dtype=np.float64)
+    mse = C.c_double(0.0)
+    kind = lib().orc_eq3_fit(m.ctypes.data, t.ctypes.data, len(m), coef.ctypes.data, C.byref(mse))
+    if kind < 0:
+        raise ValueError("eq3_fit needs >= 4 records with m >= 1")
+    return coef, int(kind), float(mse.value)
 
 
 def pack(ids, n_samples, B: int, E: int):

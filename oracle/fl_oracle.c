@@ -138,6 +138,143 @@ int orc_place(int policy, const int64_t* cohort, int64_t K, const int64_t* n_sam
   return 0;
 }
 
+/*
+ * LB with one Eq. 3 fit per worker.  coef = [G][4].  "sorts the
+ * workers by GPU type, from the fastest to the slowest, using the predicted
+ * training time of the biggest client": worker order = ascending
+ * Eq. 3 prediction at the cohort's largest m (ties by worker id).  Clients by
+ * m descending, id ascending.  "assigns the current client to the
+ * worker whose load is lower" with load = Σ predicted time of its clients
+ * (P:388); ties go to the earlier worker in the fastest-first order.
+ */
+int orc_place_lb_gpu(const int64_t* cohort, int64_t K, const int64_t* n_samples, int64_t n_pop,
+                     int64_t B, int64_t G, const double* coef, int64_t* out_ids, int64_t* out_off) {
+  if (G < 1 || B < 1 || K < 0) return -1;
+  for (int64_t i = 0; i < K; ++i)
+    if (cohort[i] < 0 || cohort[i] >= n_pop) return -1;
+  orc_item* it = (orc_item*)malloc(sizeof(orc_item) * (K ? K : 1));
+  int64_t mmax = 1;
+  for (int64_t i = 0; i < K; ++i) {
+    it[i].m = batches(n_samples[cohort[i]], B); it[i].id = cohort[i]; it[i].pos = i;
+    if (it[i].m > mmax) mmax = it[i].m;
+  }
+  qsort(it, (size_t)K, sizeof(orc_item), cmp_m_desc_id_asc);
+  /* fastest-first order by insertion sort (stable: equal predictions keep worker id order) */
+  int64_t* ord = (int64_t*)malloc(sizeof(int64_t) * (size_t)G);
+  for (int64_t w = 0; w < G; ++w) {
+    int64_t j = w;
+    double tw = orc_eq3(coef + 4 * w, (double)mmax);
+    while (j > 0 && orc_eq3(coef + 4 * ord[j - 1], (double)mmax) > tw) { ord[j] = ord[j - 1]; --j; }
+    ord[j] = w;
+  }
+  double* load = (double*)calloc((size_t)G, sizeof(double));
+  int64_t* worker = (int64_t*)malloc(sizeof(int64_t) * (K ? K : 1));
+  for (int64_t i = 0; i < K; ++i) {
+    int64_t best = ord[0];
+    for (int64_t q = 1; q < G; ++q)
+      if (load[ord[q]] < load[best]) best = ord[q];
+    worker[i] = best;
+    load[best] += orc_eq3(coef + 4 * best, (double)it[i].m);
+  }
+  int64_t* cnt = (int64_t*)calloc((size_t)G + 1, sizeof(int64_t));
+  for (int64_t i = 0; i < K; ++i) cnt[worker[i] + 1]++;
+  for (int64_t w = 0; w < G; ++w) cnt[w + 1] += cnt[w];
+  for (int64_t w = 0; w <= G; ++w) out_off[w] = cnt[w];
+  for (int64_t i = 0; i < K; ++i) out_ids[cnt[worker[i]]++] = it[i].id;
+  free(cnt); free(worker); free(load); free(ord); free(it);
+  return 0;
+}
+
+/*
+ * LB's fit ("fits the data points to the function in" Eq. 3,
+ * y = a x + b log(c x) + d, x = batches, y = training time).  Written as the
+ * plain definition: the (a, b, c, d) minimising the mean squared error.  Since
+ * b log(c x) + d = b log x + (b log c + d), every c gives the same curves, so
+ * c = 1 and the minimiser over (a, b, d) solves the 3x3 normal equations
+ * (Xᵀ X) β = Xᵀ y, X = [x, log x, 1] (Gaussian elimination, partial pivoting).
+ * Acceptance (reading R12): a >= 0 ("the linear term ensures that the
+ * bigger clients are predicted to take longer") and predictions > 0
+ * on [min x, max x] ("never predicts negative values"); the minimum of
+ * a x + b log x + d on an interval is at an end point or at x = -b/a.  Else the
+ * line y = a x + d (normal equations over [x, 1]) if a >= 0 and positive on the
+ * range, else the constant mean(y).  Returns 0 / 1 / 2 for the three kinds, -1
+ * for n < 4 or any x < 1.
+ */
+static int orc_solve(double* M, double* v, int p) { /* M[p][p] β = v, in place; 0 ok */
+  for (int c = 0; c < p; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < p; ++r) if (fabs(M[r * p + c]) > fabs(M[piv * p + c])) piv = r;
+    if (M[piv * p + c] == 0.0) return -1;
+    for (int k = 0; k < p; ++k) { double t = M[c * p + k]; M[c * p + k] = M[piv * p + k]; M[piv * p + k] = t; }
+    { double t = v[c]; v[c] = v[piv]; v[piv] = t; }
+    for (int r = c + 1; r < p; ++r) {
+      double f = M[r * p + c] / M[c * p + c];
+      for (int k = c; k < p; ++k) M[r * p + k] -= f * M[c * p + k];
+      v[r] -= f * v[c];
+    }
+  }
+  for (int c = p - 1; c >= 0; --c) {
+    double s = v[c];
+    for (int k = c + 1; k < p; ++k) s -= M[c * p + k] * v[k];
+    v[c] = s / M[c * p + c];
+  }
+  return 0;
+}
+
+int orc_eq3_fit(const double* x, const double* y, int64_t n, double* coef, double* mse) {
+  if (n < 4) return -1;
+  double xmin = x[0], xmax = x[0], ymean = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (!(x[i] >= 1.0)) return -1;
+    if (x[i] < xmin) xmin = x[i];
+    if (x[i] > xmax) xmax = x[i];
+    ymean += y[i];
+  }
+  ymean /= (double)n;
+  int kind = 2;
+  coef[0] = 0.0; coef[1] = 0.0; coef[2] = 1.0; coef[3] = ymean;
+  double M[9] = {0}, v[3] = {0};
+  for (int64_t i = 0; i < n; ++i) {
+    double r[3] = {x[i], log(x[i]), 1.0};
+    for (int j = 0; j < 3; ++j) {
+      v[j] += r[j] * y[i];
+      for (int k = 0; k < 3; ++k) M[j * 3 + k] += r[j] * r[k];
+    }
+  }
+  if (xmax > xmin && orc_solve(M, v, 3) == 0) {
+    double a = v[0], b = v[1], d = v[2];
+    double f1 = a * xmin + b * log(xmin) + d, f2 = a * xmax + b * log(xmax) + d;
+    double lo = f1 < f2 ? f1 : f2;
+    if (a > 0.0 && b < 0.0) {
+      double xs = -b / a;
+      if (xs > xmin && xs < xmax) { double f3 = a * xs + b * log(xs) + d; if (f3 < lo) lo = f3; }
+    }
+    if (a >= 0.0 && lo > 0.0) { kind = 0; coef[0] = a; coef[1] = b; coef[3] = d; }
+  }
+  if (kind != 0 && xmax > xmin) {
+    double M2[4] = {0}, v2[2] = {0};
+    for (int64_t i = 0; i < n; ++i) {
+      double r[2] = {x[i], 1.0};
+      for (int j = 0; j < 2; ++j) {
+        v2[j] += r[j] * y[i];
+        for (int k = 0; k < 2; ++k) M2[j * 2 + k] += r[j] * r[k];
+      }
+    }
+    if (orc_solve(M2, v2, 2) == 0 && v2[0] >= 0.0 && v2[0] * xmin + v2[1] > 0.0) {
+      kind = 1; coef[0] = v2[0]; coef[1] = 0.0; coef[3] = v2[1];
+    }
+  }
+  if (mse) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      double e = coef[0] * x[i] + coef[1] * log(x[i]) + coef[3] - y[i];
+      s += e * e;
+    }
+    *mse = s / (double)n;
+  }
+  return kind;
+}
+
 /* Packer for one worker list: seg_off[i+1] = seg_off[i] + n_i; steps_i = E * m_i. */
 void orc_pack(const int64_t* ids, int64_t K, const int64_t* n_samples, int64_t B, int64_t E,
               int64_t* seg_off, int64_t* steps) {

@@ -23,14 +23,15 @@ FL_OK, FL_ERR_INVALID, FL_ERR_STATE, FL_ERR_OOM, FL_ERR_CUDA, FL_ERR_NCCL, FL_ER
 STATUS = {0: "FL_OK", 1: "FL_ERR_INVALID", 2: "FL_ERR_STATE", 3: "FL_ERR_OOM", 4: "FL_ERR_CUDA", 5: "FL_ERR_NCCL",
           6: "FL_ERR_EMPTY", 7: "FL_ERR_UNSUPPORTED"}
 MODEL = {"logreg": 0, "cnn": 1, "speech": 2, "lstm": 3}
-POLICY = {"bu": 0, "lb": 1, "rr": 2, "srr": 3}
+POLICY = {"bu": 0, "lb": 1, "rr": 2, "srr": 3, "lb_gpu": 4}
 ABI_VERSION = 1
 
 # Symbols include/fl.h declares (checked by tests/test_abi.py).
 EXPORTS = ["fl_abi_version", "fl_n_params", "fl_place_plan", "fl_pack_plan", "fl_nccl_unique_id", "fl_round_init",
            "fl_place", "fl_train_clients", "fl_aggregate", "fl_round", "fl_fedavg_vectors", "fl_get_local_plan",
            "fl_get_client_params", "fl_get_global_params", "fl_set_global_params", "fl_get_stats",
-           "fl_set_profiling", "fl_get_kernel_stats", "fl_get_stream", "fl_last_error", "fl_round_destroy", "fl_debug_read"]
+           "fl_set_profiling", "fl_get_kernel_stats", "fl_get_stream", "fl_last_error", "fl_round_destroy", "fl_debug_read",
+           "fl_lb_fit", "fl_set_timing_records", "fl_get_client_times"]
 
 
 class FLError(RuntimeError):
@@ -103,6 +104,9 @@ def lib():
             "fl_last_error": (C.c_char_p, [vp]),
             "fl_round_destroy": (None, [vp]),
             "fl_debug_read": (C.c_int, [vp, C.c_char_p, vp, i64]),
+            "fl_lb_fit": (C.c_int, [vp, vp, i64, vp, vp, vp]),
+            "fl_set_timing_records": (C.c_int, [vp, i32]),
+            "fl_get_client_times": (C.c_int, [vp, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -153,6 +157,20 @@ def fl_pack_plan(ids, n_samples, batch_size, local_epochs):
     if rc != FL_OK:
         raise FLError(rc, "fl_pack_plan")
     return seg, steps
+
+
+def fl_lb_fit(m, t):
+    """Eq. 3 least-squares fit of timing records (include/fl.h): returns (coef[4], kind, mse)."""
+    m = np.ascontiguousarray(m, np.float64)
+    t = np.ascontiguousarray(t, np.float64)
+    if len(m) != len(t):
+        raise FLError(FL_ERR_INVALID, "fl_lb_fit: m and t differ in length")
+    coef = np.empty(4, np.float64)
+    kind, mse = C.c_int32(0), C.c_double(0.0)
+    rc = lib().fl_lb_fit(_ptr(m), _ptr(t), len(m), _ptr(coef), C.byref(kind), C.byref(mse))
+    if rc != FL_OK:
+        raise FLError(rc, "fl_lb_fit")
+    return coef, int(kind.value), float(mse.value)
 
 
 def fl_nccl_unique_id() -> bytes:
@@ -300,6 +318,19 @@ class Ctx:
         out = np.empty(shape, dtype)
         self._check(lib().fl_debug_read(self._h, name.encode(), _ptr(out), out.nbytes), "fl_debug_read")
         return out
+
+    def fl_set_timing_records(self, on=True):
+        self._check(lib().fl_set_timing_records(self._h, int(bool(on))), "fl_set_timing_records")
+
+    def fl_get_client_times(self):
+        """LB timing records of the last trained round: (ids, m, t_ms), plan order."""
+        n = C.c_int64(0)
+        self._check(lib().fl_get_client_times(self._h, None, None, None, C.byref(n)), "fl_get_client_times")
+        k = int(n.value)
+        ids, m, t = np.empty(k, np.int64), np.empty(k, np.int64), np.empty(k, np.float64)
+        self._check(lib().fl_get_client_times(self._h, _ptr(ids), _ptr(m), _ptr(t), C.byref(n)),
+                    "fl_get_client_times")
+        return ids, m, t
 
     def fl_get_stats(self):
         st = fl_round_stats()

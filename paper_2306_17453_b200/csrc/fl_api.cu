@@ -247,6 +247,11 @@ struct fl_ctx {
   std::vector<cudaEvent_t> ev_join;
   cudaEvent_t ev_fork = nullptr;
   int64_t part_group_z = 0;
+  // LB timing records (fl_set_timing_records): one event per (group, wave) in which some
+  // client's last step runs; rec_of_exec[e] = index into rec_ev of exec position e's event
+  bool rec_on = false, rec_valid = false;
+  std::vector<cudaEvent_t> rec_ev;
+  std::vector<int64_t> rec_of_exec;
 };
 
 // ---------------------------------------------------------------- error helpers
@@ -304,6 +309,15 @@ fl_status fl_place_plan(int32_t policy, const int64_t* cohort_ids, int64_t n_coh
                           out_ids, out_off);
 }
 
+fl_status fl_lb_fit(const double* x, const double* y, int64_t n, double* coef_out, int32_t* kind_out,
+                    double* mse_out) {
+  if (!x || !y || !coef_out) return FL_ERR_INVALID;
+  const int kind = lb_fit(x, y, n, coef_out, mse_out);
+  if (kind < 0) return FL_ERR_INVALID;
+  if (kind_out) *kind_out = kind;
+  return FL_OK;
+}
+
 fl_status fl_pack_plan(const int64_t* ids, int64_t n, const int64_t* n_samples, int64_t n_clients, int32_t batch_size,
                        int32_t local_epochs, int64_t* seg_off, int64_t* steps) {
   if ((!ids && n > 0) || !n_samples) return FL_ERR_INVALID;
@@ -348,6 +362,8 @@ void fl_round_destroy(fl_ctx* c) {
   for (cudaEvent_t e : c->ev_join)
     if (e) cudaEventDestroy(e);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  for (cudaEvent_t e : c->rec_ev)
+    if (e) cudaEventDestroy(e);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
 }
@@ -745,6 +761,26 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   // ---- local SGD
   c->cb.xrows = c->xpack_cap / L.D_pack;
   int64_t tl = 0;
+  // LB records: event slot per (group, last wave of some client of that group)
+  std::vector<int64_t> rec_slot;  // [n_waves] flat wave -> event index or -1
+  c->rec_valid = false;
+  if (c->rec_on) {
+    rec_slot.assign((size_t)ws.n_waves, -1);
+    c->rec_of_exec.assign((size_t)K, -1);
+    int64_t nev = 0;
+    for (int g = 0; g < ws.ngroups; ++g)
+      for (int64_t el = 0; el < ws.gn[(size_t)g]; ++el) {
+        const int64_t e = ws.gbase[(size_t)g] + el;
+        const int64_t k = (lstm || cnn) ? ws.gw0[(size_t)g] + c->steps_exec[(size_t)e] - 1 : 0;
+        if (rec_slot[(size_t)k] < 0) rec_slot[(size_t)k] = nev++;
+        c->rec_of_exec[(size_t)e] = rec_slot[(size_t)k];
+      }
+    while ((int64_t)c->rec_ev.size() < nev) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c->rec_ev.push_back(e);
+    }
+  }
   if (K > 0) {
     if (cnn) {
       // groups run concurrently on their own streams, forked from and joined into st. Waves
@@ -783,6 +819,8 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
             return set_err(c, FL_ERR_CUDA, "tensor-core kernel launch / tensor map failed (group %d wave %lld)", g,
                            (long long)t);
           tl += nl;
+          if (c->rec_on && rec_slot[(size_t)k] >= 0)
+            CK(cudaEventRecord(c->rec_ev[(size_t)rec_slot[(size_t)k]], gst[(size_t)g]));
         }
       }
       if (hostprof)
@@ -806,6 +844,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
         if (nl < 0) return set_err(c, FL_ERR_CUDA, "lstm wave %lld launch failed", (long long)k);
         c->prof.end(K_LSTM, 381.5e6 * (double)sum_bs, 2.0 * 4.0 * ws.A[(size_t)k] * L.P_pad, st);
         tl += nl;
+        if (c->rec_on && rec_slot[(size_t)k] >= 0) CK(cudaEventRecord(c->rec_ev[(size_t)rec_slot[(size_t)k]], st));
       }
     } else {
       c->prof.begin(st);
@@ -814,9 +853,12 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       double S = 0;
       for (int64_t e = 0; e < K; ++e) S += (double)c->n_exec[(size_t)e] * E;
       c->prof.end(K_LOGREG, 3.0 * 2.0 * S * 7840, 4.0 * S * 785 + 8.0 * K * L.P_pad, st);
+      // one CTA per client inside one launch: every client's record is the launch's end
+      if (c->rec_on) CK(cudaEventRecord(c->rec_ev[0], st));
     }
     CKL();
   }
+  c->rec_valid = c->rec_on;
   CK(cudaEventRecord(c->ev_trained, st));
   c->kernels = launches + tl;
   c->train_launches = tl;
@@ -915,6 +957,35 @@ fl_status fl_round(fl_ctx* c, const int64_t* cohort_ids, int64_t n_cohort, int32
     CK(cudaEventSynchronize(c->ev_end));
     fill_stats(c, &c->stats);
     *stats = c->stats;
+  }
+  return FL_OK;
+}
+
+fl_status fl_set_timing_records(fl_ctx* c, int32_t on) {
+  if (!c) return FL_ERR_INVALID;
+  c->rec_on = on != 0;
+  return FL_OK;
+}
+
+fl_status fl_get_client_times(fl_ctx* c, int64_t* ids, int64_t* m, double* t_ms, int64_t* n_local) {
+  if (!c) return FL_ERR_INVALID;
+  if (!c->rec_valid) return set_err(c, FL_ERR_STATE, "no round trained with timing records on");
+  const int64_t K = (int64_t)c->exec.size(), B = c->cfg.batch_size;
+  if (n_local) *n_local = K;
+  if (!ids && !m && !t_ms) return FL_OK;
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaEventSynchronize(c->ev_trained));
+  // exec order -> plan order
+  for (int64_t e = 0; e < K; ++e) {
+    const int64_t i = c->exec[(size_t)e];  // index into local_ids (plan order)
+    const int64_t id = c->local_ids[(size_t)i];
+    if (ids) ids[i] = id;
+    if (m) m[i] = (c->n_samples[(size_t)id] + B - 1) / B;
+    if (t_ms) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->ev_staged, c->rec_ev[(size_t)c->rec_of_exec[(size_t)e]]));
+      t_ms[i] = ms;
+    }
   }
   return FL_OK;
 }

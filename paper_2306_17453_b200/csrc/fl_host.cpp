@@ -25,6 +25,7 @@ double eq3_cost(const double* coef, double m) {
 
 int place(int policy, const int64_t* cohort, int64_t K, const int64_t* n_samples, int64_t n_clients,
           int64_t B, int64_t G, const double* lb, int64_t* out_ids, int64_t* out_off) {
+  if (policy == FL_PLACE_LB_GPU) return place_lb_gpu(cohort, K, n_samples, n_clients, B, G, lb, out_ids, out_off);
   if (G < 1 || B < 1 || K < 0 || K > n_clients) return FL_ERR_INVALID;
   if (policy < FL_PLACE_BU || policy > FL_PLACE_SRR) return FL_ERR_INVALID;
   if (policy == FL_PLACE_LB && !lb) return FL_ERR_INVALID;
@@ -73,6 +74,134 @@ int place(int policy, const int64_t* cohort, int64_t K, const int64_t* n_samples
   for (int64_t w = 0; w <= G; ++w) out_off[w] = cnt[(size_t)w];
   for (int64_t i = 0; i < K; ++i) out_ids[cnt[(size_t)worker[(size_t)i]]++] = cohort[order[(size_t)i]];
   return FL_OK;
+}
+
+// LB with one Eq. 3 fit per GPU: "sorts the workers by GPU type, from the fastest
+// to the slowest, using the predicted training time of the biggest client", then
+// each client (m desc, id asc) goes to the worker whose predicted load is lowest; ties go to
+// the earlier worker in fastest-first order.  coef = [G][4].
+int place_lb_gpu(const int64_t* cohort, int64_t K, const int64_t* n_samples, int64_t n_clients, int64_t B,
+                 int64_t G, const double* coef, int64_t* out_ids, int64_t* out_off) {
+  if (G < 1 || B < 1 || K < 0 || K > n_clients || !coef) return FL_ERR_INVALID;
+  std::vector<char> seen((size_t)n_clients, 0);
+  int64_t mmax = 1;
+  for (int64_t i = 0; i < K; ++i) {
+    int64_t c = cohort[i];
+    if (c < 0 || c >= n_clients || seen[(size_t)c] || n_samples[c] < 1) return FL_ERR_INVALID;
+    seen[(size_t)c] = 1;
+    mmax = std::max(mmax, n_batches(n_samples[c], B));
+  }
+  std::vector<int64_t> wo((size_t)G);  // fastest-first worker order
+  std::iota(wo.begin(), wo.end(), 0);
+  std::vector<double> tbig((size_t)G);
+  for (int64_t w = 0; w < G; ++w) tbig[(size_t)w] = eq3_cost(coef + 4 * w, (double)mmax);
+  std::stable_sort(wo.begin(), wo.end(), [&](int64_t a, int64_t b) { return tbig[(size_t)a] < tbig[(size_t)b]; });
+  std::vector<int64_t> order((size_t)K);
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    int64_t ma = n_batches(n_samples[cohort[a]], B), mb = n_batches(n_samples[cohort[b]], B);
+    if (ma != mb) return ma > mb;
+    return cohort[a] < cohort[b];
+  });
+  std::vector<int64_t> worker((size_t)K);
+  std::vector<double> load((size_t)G, 0.0);
+  for (int64_t i = 0; i < K; ++i) {
+    int64_t best = wo[0];
+    for (int64_t q = 1; q < G; ++q)
+      if (load[(size_t)wo[(size_t)q]] < load[(size_t)best]) best = wo[(size_t)q];
+    worker[(size_t)i] = best;
+    load[(size_t)best] += eq3_cost(coef + 4 * best, (double)n_batches(n_samples[cohort[order[(size_t)i]]], B));
+  }
+  std::vector<int64_t> cnt((size_t)G + 1, 0);
+  for (int64_t i = 0; i < K; ++i) cnt[(size_t)worker[(size_t)i] + 1]++;
+  for (int64_t w = 0; w < G; ++w) cnt[(size_t)w + 1] += cnt[(size_t)w];
+  for (int64_t w = 0; w <= G; ++w) out_off[w] = cnt[(size_t)w];
+  for (int64_t i = 0; i < K; ++i) out_ids[cnt[(size_t)worker[(size_t)i]]++] = cohort[order[(size_t)i]];
+  return FL_OK;
+}
+
+// Least-squares fit of Eq. 3 to timing records.  b·log(c·x) + d =
+// b·log x + (b·log c + d): c is not identifiable, so c = 1 and the fit is the linear
+// least-squares problem over the basis (x, log x, 1) — its global minimiser, solved by
+// Householder QR of the n×3 design.  The fit is accepted if a >= 0 (bigger clients take
+// longer) and it predicts > 0 over the observed range [x_min, x_max]
+// (P:439); otherwise the fallback is the line y = a·x + d with a >= 0, and
+// a constant (the mean) if that slope is negative.  Returns the kind (0 Eq. 3, 1 line,
+// 2 constant) or -1 if n < 4.
+static int lsq_qr(const double* x, const double* y, int64_t n, int p, double* beta) {
+  // columns: 0 -> x, 1 -> log x, 2 -> 1 (p = 2 uses columns {x, 1})
+  std::vector<double> A((size_t)n * p), r(y, y + n);
+  for (int64_t i = 0; i < n; ++i) {
+    A[(size_t)i * p + 0] = x[i];
+    if (p == 3) A[(size_t)i * p + 1] = log(x[i]);
+    A[(size_t)i * p + p - 1] = 1.0;
+  }
+  std::vector<double> diag((size_t)p);
+  for (int j = 0; j < p; ++j) {  // Householder reflection zeroing column j below the diagonal
+    double nrm = 0;
+    for (int64_t i = j; i < n; ++i) nrm += A[(size_t)i * p + j] * A[(size_t)i * p + j];
+    nrm = sqrt(nrm);
+    if (nrm == 0) return -1;
+    const double alpha = A[(size_t)j * p + j] > 0 ? -nrm : nrm;
+    A[(size_t)j * p + j] -= alpha;  // v = column - alpha·e_j, stored in place
+    double vv = 0;
+    for (int64_t i = j; i < n; ++i) vv += A[(size_t)i * p + j] * A[(size_t)i * p + j];
+    for (int q = j + 1; q < p; ++q) {
+      double d = 0;
+      for (int64_t i = j; i < n; ++i) d += A[(size_t)i * p + j] * A[(size_t)i * p + q];
+      d = 2 * d / vv;
+      for (int64_t i = j; i < n; ++i) A[(size_t)i * p + q] -= d * A[(size_t)i * p + j];
+    }
+    double d = 0;
+    for (int64_t i = j; i < n; ++i) d += A[(size_t)i * p + j] * r[(size_t)i];
+    d = 2 * d / vv;
+    for (int64_t i = j; i < n; ++i) r[(size_t)i] -= d * A[(size_t)i * p + j];
+    diag[(size_t)j] = alpha;
+  }
+  double scale = 0;
+  for (int j = 0; j < p; ++j) scale = std::max(scale, fabs(diag[(size_t)j]));
+  for (int j = p - 1; j >= 0; --j) {  // back substitution R·beta = Qᵀy
+    if (fabs(diag[(size_t)j]) <= 1e-12 * scale) return -1;
+    double s = r[(size_t)j];
+    for (int q = j + 1; q < p; ++q) s -= A[(size_t)j * p + q] * beta[q];
+    beta[j] = s / diag[(size_t)j];
+  }
+  return 0;
+}
+
+int lb_fit(const double* x, const double* y, int64_t n, double* coef, double* mse) {
+  if (n < 4 || !x || !y || !coef) return -1;
+  double xmin = x[0], xmax = x[0], ymean = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (!(x[i] >= 1.0)) return -1;
+    xmin = std::min(xmin, x[i]);
+    xmax = std::max(xmax, x[i]);
+    ymean += y[i];
+  }
+  ymean /= (double)n;
+  int kind = 2;
+  double beta[3];
+  coef[0] = 0, coef[1] = 0, coef[2] = 1, coef[3] = ymean;
+  if (lsq_qr(x, y, n, 3, beta) == 0) {
+    const double a = beta[0], b = beta[1], d = beta[2];
+    double lo = std::min(a * xmin + b * log(xmin) + d, a * xmax + b * log(xmax) + d);
+    if (a > 0 && b < 0) {
+      const double xs = -b / a;  // interior minimum of a convex a·x + b·log x + d
+      if (xs > xmin && xs < xmax) lo = std::min(lo, a * xs + b * log(xs) + d);
+    }
+    if (a >= 0 && lo > 0) kind = 0, coef[0] = a, coef[1] = b, coef[3] = d;
+  }
+  if (kind != 0 && lsq_qr(x, y, n, 2, beta) == 0 && beta[0] >= 0 && beta[0] * xmin + beta[1] > 0)
+    kind = 1, coef[0] = beta[0], coef[1] = 0, coef[3] = beta[1];
+  if (mse) {
+    double s = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      const double e = coef[0] * x[i] + coef[1] * log(x[i]) + coef[3] - y[i];
+      s += e * e;
+    }
+    *mse = s / (double)n;
+  }
+  return kind;
 }
 
 int pack(const int64_t* ids, int64_t n, const int64_t* n_samples, int64_t n_clients, int64_t B, int64_t E,
