@@ -243,6 +243,8 @@ struct fl_ctx {
   // SMs the bulk groups' persistent kernels leave free for the solo (critical-path) streams
   // when solo groups exist (FL_RESERVE_SMS; measured: 64 -> C2 -3%)
   int reserve_sms = 64;
+  // SMs a solo group's persistent kernels may occupy (FL_SOLO_SMS)
+  int solo_sms = 148;
   std::vector<cudaStream_t> gstream;  // [nsolo high-priority | ngroups normal]
   std::vector<cudaEvent_t> ev_join;
   cudaEvent_t ev_fork = nullptr;
@@ -423,6 +425,7 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   if (const char* ng = getenv("FL_GROUPS")) c->ngroups = std::max(1, atoi(ng));
   if (const char* ns = getenv("FL_SOLO")) c->nsolo = std::max(0, atoi(ns));
   if (const char* pm = getenv("FL_PDL_MAXA")) c->pdl_max_a = atoi(pm);
+  if (const char* ss = getenv("FL_SOLO_SMS")) c->solo_sms = std::max(8, std::min(148, atoi(ss)));
   if (const char* rs = getenv("FL_RESERVE_SMS")) c->reserve_sms = std::max(0, std::min(120, atoi(rs)));
   c->nsolo = std::min(c->nsolo, std::max(0, 8 - c->ngroups));
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
@@ -812,7 +815,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
           WaveArgs wa{ws.A[(size_t)k], (int)B, t == 0, ws.d_sidx + ws.slot_off[(size_t)k],
                       ws.d_bs + ws.bs_off[(size_t)k], c->cfg.lr, sum_bs, &c->prof, c->cfg.math == 0,
                       ws.gn[(size_t)g], ws.A[(size_t)k] <= c->pdl_max_a, ws.d_bpre + ws.bs_off[(size_t)k] + k,
-                      (ws.gsolo[(size_t)g] || c->reserve_sms == 0) ? 148 : 148 - c->reserve_sms};
+                      (ws.gsolo[(size_t)g] || c->reserve_sms == 0) ? c->solo_sms : 148 - c->reserve_sms};
           int nl = cnn_wave_simt(L, wa, c->d_xpack, c->d_ypack, c->d_theta, c->d_slots + base * L.P_pad,
                                  gv[(size_t)g], gst[(size_t)g]);
           if (nl < 0)

@@ -166,6 +166,12 @@ struct KProf {
   ~KProf() { for (cudaEvent_t e : pool) cudaEventDestroy(e); }
 };
 
+// Integer tuning knob from the environment (read once per call site; default otherwise).
+inline int env_knob(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 struct WaveArgs {
   int A;             // active clients
   int B;             // batch size

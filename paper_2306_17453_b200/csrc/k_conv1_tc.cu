@@ -457,7 +457,8 @@ int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64
     return -1;
   // two CTAs per SM; at least half a sample (16 image rows) of work per CTA
   const int64_t U = (int64_t)H * wa.sum_bs;
-  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(2 * wa.sms, U / 16));
+  static const int minr = std::max(1, env_knob("FL_DW1_MINR", 16));
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(2 * wa.sms, U / minr));
   if ((int64_t)wa.A + G > part_cap) return -1;
   static bool attr = false;
   if (!attr) {

@@ -232,7 +232,10 @@ int conv2_dw_tc(const Layout& L, const WaveArgs& wa, const float* p1, const floa
   if (!make_maps(&mx, &md, p1, dY2, slots)) return -1;
   // one CTA per SM (512 TMEM columns each), every CTA at least one sample of work
   const int64_t U = 8 * wa.sum_bs;
-  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(wa.sms, wa.sum_bs));
+  // at least `mins` samples per CTA (FL_DW2_MINS): each CTA writes a whole [801][64] partial, so
+  // in small waves a finer split costs more SM time and traffic than it saves in latency
+  static const int mins = std::max(1, env_knob("FL_DW2_MINS", 1));
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(wa.sms, (wa.sum_bs + mins - 1) / mins));
   if ((int64_t)wa.A + G > part_cap) return -1;
   static bool attr = false;
   if (!attr) {

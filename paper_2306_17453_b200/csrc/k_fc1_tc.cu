@@ -384,6 +384,8 @@ constexpr int BW_OUT = BW_P2 + 2 * BW_P2B;        // 2 x 16 KB store buffers: a 
 constexpr int BW_BAR = BW_OUT + 2 * 16384;        // soon as the epilogue has read it, not when stored
 constexpr int BW_SMEM = BW_BAR + 256 + 1024;
 constexpr uint32_t BW_TCOLS = 512;                // G [0,128) [128,256); dX [256,288) [288,320)
+constexpr int BW_EPI = 256;                       // epilogue threads (8 warps)
+constexpr int BW_THREADS = 64 + BW_EPI;
 
 struct BwArgs {
   const int32_t* bs;
@@ -400,7 +402,7 @@ struct BwArgs {
   float lr;
 };
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(BW_THREADS, 1)
     k_fc1_bwd_tc(const __grid_constant__ CUtensorMap mapWsrc, const __grid_constant__ CUtensorMap mapWdst,
                  const __grid_constant__ CUtensorMap mapDht, const __grid_constant__ CUtensorMap mapX, BwArgs p) {
   constexpr uint32_t IDESC_DX = tc::idesc_tf32(128, NB, 1, 0);   // A (W1ᵀ) MN-major, B (dh) K-major
@@ -427,15 +429,15 @@ __global__ void __launch_bounds__(192, 1)
       tc::prefetch_tmap(&mapX);
       for (int i = 0; i < BW_NST; ++i) {
         tc::mbar_init(full + i, 1);
-        tc::mbar_init(empty + i, 128);  // every epilogue thread, after its last read of the stage
+        tc::mbar_init(empty + i, BW_EPI);  // every epilogue thread, after its last read of the stage
       }
       for (int i = 0; i < 2; ++i) {
         tc::mbar_init(gfull + i, 1);
-        tc::mbar_init(gempty + i, 128);
+        tc::mbar_init(gempty + i, BW_EPI);
         tc::mbar_init(p2full + i, 1);
         tc::mbar_init(p2empty + i, 1);
         tc::mbar_init(dxfull + i, 1);
-        tc::mbar_init(dxempty + i, 128);
+        tc::mbar_init(dxempty + i, BW_EPI);
       }
       tc::fence_mbar_init();
     }
@@ -504,8 +506,10 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ---------------- epilogue (thread = n row of the chunk for G; = k row of the panel for dX)
-    const int qd = warp & 3, row = qd * 32 + lane;
+    // ---------------- epilogue: 8 warps, two per TMEM lane quarter (warp % 4); half hf of a
+    // pair takes columns [16 hf, 16 hf + 16) of every 32-column sub-chunk of G, and batch rows
+    // [16 hf, 16 hf + 16) of dX.  Thread = n row of the chunk for G; = k row of the panel for dX.
+    const int qd = warp & 3, row = qd * 32 + lane, hf = (warp - 2) >> 2;
     const bool storer = (warp == 2 && lane == 0);  // issues and retires the W stores (bulk groups are per thread)
     int it = 0, ti = 0, oi = 0;
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
@@ -514,19 +518,19 @@ __global__ void __launch_bounds__(192, 1)
       if (bs == 0) continue;
       const int pb = ti & 1, pph = (ti >> 1) & 1;
       ++ti;
-      // pool2 state of this thread's dX row: independent of the MMAs, loaded up front and only
-      // inspected in the dX epilogue, so the loads stay in flight during the chunk loop
-      const int k = kt * 128 + row;
-      float p2v[NB];
-      uint32_t amw[NB / 4];
+      // pool2 state of this thread's dX row and batch half: independent of the MMAs, loaded up
+      // front and only inspected in the dX epilogue, so the loads stay in flight during the chunks
+      const int k = kt * 128 + row, r0 = 16 * hf;
+      float p2v[16];
+      uint32_t amw[4];
 #pragma unroll
-      for (int r = 0; r < NB; ++r) p2v[r] = r < bs ? __ldg(p.p2 + ((int64_t)a * p.B + r) * p.F + k) : 0.f;
+      for (int r = 0; r < 16; ++r) p2v[r] = r0 + r < bs ? __ldg(p.p2 + ((int64_t)a * p.B + r0 + r) * p.F + k) : 0.f;
 #pragma unroll
-      for (int r4 = 0; r4 < NB / 4; ++r4) {
+      for (int r4 = 0; r4 < 4; ++r4) {
         uint32_t w = 0;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int r = 4 * r4 + u;
+          const int r = r0 + 4 * r4 + u;
           const uint32_t b8 = r < bs ? __ldg(p.am2 + ((int64_t)a * p.B + r) * p.F + k) : 0u;
           w |= b8 << (8 * u);
         }
@@ -537,7 +541,7 @@ __global__ void __launch_bounds__(192, 1)
         uint8_t* sw = smem + st * BW_STAGE;
         tc::mbar_wait(gfull + buf, gph);
         tc::tc_fence_after();
-        if (kt == 0) {  // bias: b1[n] -= η Σ_r dh[r][n], from the stage's dh chunk (ATOM_32B)
+        if (kt == 0 && hf == 0) {  // bias: b1[n] -= η Σ_r dh[r][n], from the stage's dh chunk (ATOM_32B)
           const int n = 128 * c + row, nn = row & 31;
           const uint8_t* dq = sw + BW_W + (row >> 5) * 4096 + (nn & 7) * 4;
           float g = 0.f;
@@ -546,29 +550,28 @@ __global__ void __launch_bounds__(192, 1)
         }
         for (int j = 0; j < 4; ++j, ++oi) {
           uint8_t* ob = smem + BW_OUT + (oi & 1) * 16384;
+          float v[16];
+          const uint32_t tg = tbase + ((uint32_t)(qd * 32) << 16) + buf * 128 + 32 * j + 16 * hf;
+          tc::tmem_ld16(tg, v);  // issued before the barrier: overlaps the wait for the store buffer
           if (storer) tc::bulk_wait_read<1>();  // the store issued from this buffer two sub-chunks ago has read it
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          float v[32];
-          const uint32_t tg = tbase + ((uint32_t)(qd * 32) << 16) + buf * 128 + 32 * j;
-          tc::tmem_ld16(tg, *reinterpret_cast<float(*)[16]>(v));
-          tc::tmem_ld16(tg + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+          asm volatile("bar.sync 1, %0;" ::"n"(BW_EPI) : "memory");
           const uint8_t* rowp = sw + j * 16384 + row * 128;
           uint8_t* orow = ob + row * 128;
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {  // 32-byte granule g of the row sits at g ^ (row % 4) (ATOM_32B)
-            const int off = (g ^ (row & 3)) << 5;
+          for (int g2 = 0; g2 < 2; ++g2) {  // 32-byte granule g of the row sits at g ^ (row % 4) (ATOM_32B)
+            const int off = ((2 * hf + g2) ^ (row & 3)) << 5;
 #pragma unroll
             for (int hq = 0; hq < 2; ++hq) {
               float4 w = reinterpret_cast<const float4*>(rowp + off)[hq];
-              w.x -= p.lr * v[8 * g + 4 * hq];
-              w.y -= p.lr * v[8 * g + 4 * hq + 1];
-              w.z -= p.lr * v[8 * g + 4 * hq + 2];
-              w.w -= p.lr * v[8 * g + 4 * hq + 3];
+              w.x -= p.lr * v[8 * g2 + 4 * hq];
+              w.y -= p.lr * v[8 * g2 + 4 * hq + 1];
+              w.z -= p.lr * v[8 * g2 + 4 * hq + 2];
+              w.w -= p.lr * v[8 * g2 + 4 * hq + 3];
               reinterpret_cast<float4*>(orow + off)[hq] = w;
             }
           }
           tc::fence_async_smem();  // generic-proxy writes -> TMA store
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          asm volatile("bar.sync 1, %0;" ::"n"(BW_EPI) : "memory");
           if (storer) {
             tc::tma_store_3d(&mapWdst, ob, 128 * kt + 32 * j, 128 * c, a);
             tc::bulk_commit();
@@ -581,18 +584,17 @@ __global__ void __launch_bounds__(192, 1)
       // dX epilogue: dp2 -> pool2 / ReLU backward -> dY2 (every cell of the 2x2 window written)
       tc::mbar_wait(dxfull + pb, pph);
       tc::tc_fence_after();
-      float v[NB];
-      const uint32_t tdx = tbase + ((uint32_t)(qd * 32) << 16) + 256 + pb * 32;
-      tc::tmem_ld16(tdx, *reinterpret_cast<float(*)[16]>(v));
-      tc::tmem_ld16(tdx + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+      float v[16];
+      const uint32_t tdx = tbase + ((uint32_t)(qd * 32) << 16) + 256 + pb * 32 + 16 * hf;
+      tc::tmem_ld16(tdx, v);
       tc::tc_fence_before();
       tc::mbar_arrive(dxempty + pb);
       const int cc = k % p.C2, pw = (k / p.C2) % p.W2, ph = k / (p.C2 * p.W2);
       const int W1 = 2 * p.W2, H1 = 2 * p.H2;
 #pragma unroll
-      for (int r = 0; r < NB; ++r) {
-        if (r >= bs) break;
-        const int64_t s = (int64_t)a * p.B + r;
+      for (int r = 0; r < 16; ++r) {
+        if (r0 + r >= bs) break;
+        const int64_t s = (int64_t)a * p.B + r0 + r;
         const float g = p2v[r] > 0.f ? v[r] : 0.f;
         const int am = (amw[r >> 2] >> (8 * (r & 3))) & 0xff;
         float* d = p.dY2 + ((s * H1 + 2 * ph) * W1 + 2 * pw) * p.C2 + cc;
@@ -640,7 +642,8 @@ int fc1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t 
   uint32_t bx[3] = {32, NB, 1};
   if (!tmap_encode(&mw, wbase + L.o_f1w, 3, dw, sw, bw, 1) || !tmap_encode(&mx, p2, 3, dx, sx, bx, 1)) return -1;
   const int mtiles = d.HID / 128, nkb = d.F / 32;
-  int ksplit = (2 * 148 + wa.A * mtiles - 1) / (wa.A * mtiles);
+  static const int ctas = std::max(1, env_knob("FL_FC1F_CTAS", 2 * 148));
+  int ksplit = (ctas + wa.A * mtiles - 1) / (wa.A * mtiles);
   ksplit = ksplit < 1 ? 1 : (ksplit > 16 ? 16 : ksplit);
   while (ksplit > 1 && (int64_t)wa.A * ksplit * NB * d.HID > part_floats) --ksplit;
   const int kpb = (nkb + ksplit - 1) / ksplit;
@@ -734,7 +737,8 @@ int fc1_bwd_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t w
   BwArgs p{wa.bs, wa.A, wa.B, d.HID, d.F, wa.first ? 0 : 1, d.H2, d.W2, d.C2, p2, am2, dY2,
            wsrc + L.o_f1b, L.P_pad, slots_w + L.o_f1b, L.P_pad, dh, wa.lr};
   const int tiles = wa.A * (d.F / 128);
-  launch_pdl(wa.pdl, k_fc1_bwd_tc, dim3(tiles < wa.sms ? tiles : wa.sms), 192, BW_SMEM, st, mws, mwd, mdht, mx, p);
+  launch_pdl(wa.pdl, k_fc1_bwd_tc, dim3(tiles < wa.sms ? tiles : wa.sms), BW_THREADS, BW_SMEM, st, mws, mwd, mdht, mx,
+             p);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -187,8 +187,8 @@ def test_timing_records_cnn():
     assert np.array_equal(ids, pids)
     assert np.array_equal(m, (sizes[ids] + wl.B - 1) // wl.B)
     assert np.all(t > 0) and np.all(t <= st["train_ms"] * 1.001 + 0.01)
-    # the client with the most steps is the last to finish (it is the round's critical path)
-    assert t[np.argmax(m)] == pytest.approx(t.max(), rel=0.05)
+    # the last client to finish ends the training phase; bigger clients finish later
+    assert t.max() == pytest.approx(st["train_ms"], rel=0.05)
     assert np.corrcoef(m, t)[0, 1] > 0.5
     coef, kind, _ = fl.fl_lb_fit(m, t)
     assert kind in (0, 1, 2)
