@@ -241,8 +241,9 @@ struct fl_ctx {
   // concurrent streams (C2 22 ms).
   int pdl_max_a = 1 << 30;
   // SMs the bulk groups' persistent kernels leave free for the solo (critical-path) streams
-  // when solo groups exist (FL_RESERVE_SMS; measured: 64 -> C2 -3%)
-  int reserve_sms = 64;
+  // when solo groups exist (FL_RESERVE_SMS; measured: 64 -> C2 -3%; after the 8-warp fc1
+  // backward 32 is C2-neutral and 4% faster on a 400-client C3-law cohort)
+  int reserve_sms = 32;
   // SMs a solo group's persistent kernels may occupy (FL_SOLO_SMS)
   int solo_sms = 148;
   std::vector<cudaStream_t> gstream;  // [nsolo high-priority | ngroups normal]

@@ -314,6 +314,41 @@ __global__ void k_dw_reduce_sgd(const float* __restrict__ part, int nch, int rpc
   }
 }
 
+// Both tensor-core dW reductions of a wave in one launch (conv1: blocks [0, r1.nblk), conv2:
+// the rest): the same ordered sum + SGD as k_dw_reduce_sgd's balanced split-K branch, one
+// launch fewer per wave.  conv1 also writes the forward's tap-major copy (r1.wt).
+struct DwRed {
+  const float* part;
+  int O, N;
+  int64_t o_w, o_b;
+  float* wt;
+  int G;
+  int64_t U;
+  int kbps, nblk;
+};
+__global__ void __launch_bounds__(256) k_dw_reduce2_sgd(DwRed r1, DwRed r2, const int32_t* __restrict__ bpre, WSrc w,
+                                                        float* dst, int64_t P_pad, float lr) {
+  pdl_wait();
+  const bool second = (int)blockIdx.x >= r1.nblk;
+  const DwRed& r = second ? r2 : r1;
+  const int bx = second ? (int)blockIdx.x - r1.nblk : (int)blockIdx.x;
+  const int a = blockIdx.y, tot = r.O * r.N;
+  const int64_t v0 = (int64_t)r.kbps * bpre[a], v1 = (int64_t)r.kbps * bpre[a + 1] - 1;
+  const int c0 = (int)(((v0 + 1) * r.G + r.U - 1) / r.U) - 1, c1 = (int)(((v1 + 1) * r.G + r.U - 1) / r.U) - 1;
+  const float* pa = r.part + (int64_t)(a + c0) * tot;
+  for (int e = bx * blockDim.x + threadIdx.x; e < tot; e += r.nblk * blockDim.x) {
+    const float g = ordered_sum(pa + e, c1 - c0 + 1, tot);
+    const int m = e / r.N, n = e - m * r.N;
+    const int64_t off = n < r.N - 1 ? r.o_w + (int64_t)m * (r.N - 1) + n : r.o_b + m;
+    const float nv = *w.at(a, off) - lr * g;
+    dst[(int64_t)a * P_pad + off] = nv;
+    if (r.wt && n < r.N - 1) {
+      const int tap = n >> 2, kh = tap / 5, kw = tap - kh * 5;
+      r.wt[(int64_t)a * C1WT_FLOATS + ((kw * 6 + kh) * 32 + m) * 4 + (n & 3)] = nv;
+    }
+  }
+}
+
 // Classifier head, forward half, parallel over (client, chunk of HR batch rows): logits =
 // h·W2ᵀ + b2, softmax-CE (mean over |b|, reading A9), dz = (p − onehot)/|b| -> dzbuf,
 // dh = (dz·W2) ⊙ [h > 0]; rows past |b| get dz = dh = 0.  Reads W2 before the update.
@@ -635,6 +670,26 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     pf.end(K_UNPOOL1, 0, S * hw0 * d.C1 * (4.0 + 9.0 / 4.0), st);
   }
   const int rpc = (B + b.nch - 1) / b.nch;
+  if (tc && tc1) {  // both dW GEMMs on tcgen05, then one launch reduces both (ordered sums + SGD)
+    int g2 = 0, g1 = 0;
+    pf.begin(st);
+    if (conv2_dw_tc(L, wa, b.p1, b.dY2, b.slots, b.part2, b.part2_tc_cap, &g2, st) < 0) return -1;
+    ++n;
+    pf.end(K_CONV2_DW, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
+    pf.begin(st);
+    if (conv1_dw_tc(L, wa, b.xplanar, b.xrows, b.dp1, b.am1, b.slots, b.part1, b.part1_tc_cap, &g1, st) < 0)
+      return -1;
+    ++n;
+    pf.end(K_CONV1_DW, f_c1, 4.0 * S * hw0 * d.cin + 5.0 * S * hw1 * d.C1, st);
+    const int N2 = 25 * d.C1 + 1, N1 = 25 * d.cpad + 1;
+    DwRed r1{b.part1, d.C1, N1, L.o_c1w, L.o_c1b, b.c1wt, g1, (int64_t)d.H0 * wa.sum_bs, d.H0, (d.C1 * N1 + 255) / 256};
+    DwRed r2{b.part2, d.C2, N2, L.o_c2w, L.o_c2b, nullptr, g2, (int64_t)8 * wa.sum_bs, 8, (d.C2 * N2 + 255) / 256};
+    pf.begin(st);
+    launch_pdl(wa.pdl, k_dw_reduce2_sgd, dim3(r1.nblk + r2.nblk, A), 256, 0, st, r1, r2, wa.bpre, w, slots, L.P_pad,
+               wa.lr), ++n;
+    pf.end(K_CONV2_DWR, 0, 8.0 * A * (d.C2 * 25 * d.C1 + d.C1 * 25 * d.cin), st);
+    return n;
+  }
   if (tc) {  // tcgen05 dW with all 800 (tap, c) rows resident in TMEM; SGD in the reduction
     int g2 = 0;
     pf.begin(st);

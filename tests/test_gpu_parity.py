@@ -20,6 +20,7 @@ import paper_2306_17453_b200 as fl  # noqa: E402
 
 TOL_ROUND = 1e-3
 TOL_AGG = 1e-6
+TOL_DRIFT = 1e-2  # per-client envelope for 126-step trajectories (reading R14)
 
 
 def make_ctx(wl, sizes, x, y, theta, on_device=True, **kw):
@@ -228,6 +229,58 @@ def test_C2_full_size_sampled():
         assert np.max(np.abs(tk_gpu[c] - tk_ref[i])) <= TOL_ROUND
     coords = rng.choice(len(theta), size=20000, replace=False)
     assert agg_err(out[coords], tk_gpu[:, coords], sizes[cohort]) <= TOL_AGG
+
+
+def test_C3_full_size_decomposed():
+    """The north-star workload (BASELINE configs[2]: 1,000 of 10,000 CIFAR-shaped clients,
+    E = 2, B = 32) trained as one round on this GPU; parity by decomposition (SURVEY §8c,
+    "Full-round parity at scale"; θ_new is linear in the θ_k):
+      (i)  the aggregation of the GPU's own θ_k at full size within 1e-6 (reading R9);
+      (ii) θ_k of 12 random clients with <= 16 SGD steps within 1e-3 of the fp64 oracle;
+      (iii) the 4 largest clients (126 steps) on the TF32 path AND on the FP32 SIMT path
+           (math = 1) within the drift envelope 1e-2 (reading R14): over 126 steps the
+           dynamics amplify any fp32 rounding — the FP32 path itself departs from fp64 by
+           ~4e-3 — so a per-client 1e-3 bar is unattainable there, while θ_new, which the
+           north star bounds, is 6.8e-5 from the full fp64 oracle over all 1,000 clients
+           (scripts/c3_full_oracle.py -> profiles/r01/c3_parity.json).
+    Placement across 8 GPUs changes none of this: per-client training is placement-independent
+    and the multi-rank reduction is covered by tests/test_dist_gloo.py."""
+    wl = synth.preset("C3")
+    sizes_all = synth.client_sizes(wl)
+    ids = np.sort(synth.cohort(wl))
+    _, x, y = synth.population(wl, sizes_all, clients=ids)
+    sizes = sizes_all[ids]  # the library's population = the cohort's clients, re-indexed
+    theta = synth.init_params("cnn")
+    ctx, keep = make_ctx(wl, sizes, x, y, theta)
+    cohort = np.arange(len(ids))
+    ctx.fl_place(cohort)
+    ctx.fl_train_clients(0)
+    rng = np.random.default_rng(3)
+    order = np.argsort(-sizes, kind="stable")
+    big = list(order[:4])
+    small = list(rng.choice(np.where(sizes <= 8 * wl.B)[0], size=12, replace=False))
+    tk_big = np.stack([ctx.fl_get_client_params(c) for c in big])
+    tk_small = np.stack([ctx.fl_get_client_params(c) for c in small])
+    coords = rng.choice(len(theta), size=20000, replace=False)
+    tk_gpu_c = np.stack([ctx.fl_get_client_params(c)[coords] for c in cohort])
+    out, N = ctx.fl_aggregate()
+    assert N == sizes.sum() and len(cohort) == 1000
+    ea = agg_err(out[coords], tk_gpu_c, sizes)
+    assert ea <= TOL_AGG
+    ctx.close()
+    ctx1, keep1 = make_ctx(wl, sizes, x, y, theta, math=1)
+    ctx1.fl_place(np.array(big))
+    ctx1.fl_train_clients(0)
+    tk_simt = np.stack([ctx1.fl_get_client_params(c) for c in big])
+    pop_off = np.concatenate([[0], np.cumsum(sizes)])
+    tk_ref, _ = oracle.train_clients("cnn", theta, x, y, pop_off, np.array(big + small), wl.B, wl.E, wl.lr)
+    e_small = [float(np.max(np.abs(tk_small[i] - tk_ref[4 + i]))) for i in range(12)]
+    e_big = [float(np.max(np.abs(tk_big[i] - tk_ref[i]))) for i in range(4)]
+    e_simt = [float(np.max(np.abs(tk_simt[i] - tk_ref[i]))) for i in range(4)]
+    print("C3: agg", ea, "small", ["%.1e" % e for e in e_small], "big tf32", ["%.1e" % e for e in e_big],
+          "big fp32", ["%.1e" % e for e in e_simt])
+    assert max(e_small) <= TOL_ROUND, e_small
+    assert max(e_big) <= TOL_DRIFT and max(e_simt) <= TOL_DRIFT, (e_big, e_simt)
 
 
 # char-LSTM (a6): ragged clients (1 to 3 steps of B = 4), full round vs the fp64 oracle
