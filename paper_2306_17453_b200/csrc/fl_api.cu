@@ -255,6 +255,10 @@ struct fl_ctx {
   bool rec_on = false, rec_valid = false;
   std::vector<cudaEvent_t> rec_ev;
   std::vector<int64_t> rec_of_exec;
+  // pipelined staging of a host population: copies + pack of chunk q run on cst and
+  // complete on ev_chunk[q]; the waves of local step t >= chunk_t0[q] wait for it
+  cudaStream_t cst = nullptr;
+  std::vector<cudaEvent_t> ev_chunk;
 };
 
 // ---------------------------------------------------------------- error helpers
@@ -367,6 +371,9 @@ void fl_round_destroy(fl_ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   for (cudaEvent_t e : c->rec_ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ev_chunk)
+    if (e) cudaEventDestroy(e);
+  if (c->cst) cudaStreamDestroy(c->cst);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
 }
@@ -441,6 +448,7 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
     CK(cudaEventCreateWithFlags(&c->ev_join[(size_t)g], cudaEventDisableTiming));
   }
   if (!c->pop_dev) {
+    CK(cudaStreamCreateWithFlags(&c->cst, cudaStreamNonBlocking));
     // borrowed host population: pin it so per-round staging copies run at full PCIe rate
     size_t xb = (size_t)c->pop_off.back() * (size_t)c->L.D_in * sizeof(float);
     if (cudaHostRegister((void*)c->x, xb, cudaHostRegisterReadOnly) == cudaSuccess) c->host_registered = true;
@@ -541,6 +549,39 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
     c->N_local += c->n_exec[(size_t)e];
   }
   const int64_t R = c->pseg[(size_t)K];
+  // Packed row order (every kernel reaches a sample through the per-wave sidx tables, so any
+  // order works): chunk-major, client-major inside a chunk.  Chunk q holds batches
+  // [chunk_t0[q], chunk_t0[q+1]) of every client — the rows first needed by local SGD step
+  // t in that range — so a host population can be staged chunk by chunk while earlier
+  // steps train.  Chunks double in length (1, 1, 2, 4, ...); one chunk when the order of
+  // a client's rows is shuffled (any step may need any row) or the data is device-resident.
+  const bool cnn_pipe = (L.model == FL_MODEL_CNN_CIFAR || L.model == FL_MODEL_CNN_SPEECH) && !c->pop_dev &&
+                        !c->cfg.shuffle && getenv("FL_NO_PIPE_STAGE") == nullptr;
+  std::vector<int64_t> chunk_t0{0};
+  {
+    int64_t mmax = 0;
+    for (int64_t e = 0; e < K; ++e) mmax = std::max(mmax, (c->n_exec[(size_t)e] + B - 1) / B);
+    if (cnn_pipe)
+      for (int64_t t = 1; t < mmax; t *= 2) chunk_t0.push_back(t);
+    chunk_t0.push_back(std::max<int64_t>(mmax, 1) + (cnn_pipe ? 0 : 1 << 30));
+  }
+  const int64_t NQ = (int64_t)chunk_t0.size() - 1;
+  std::vector<int64_t> cbase((size_t)(K * NQ)), qoff((size_t)NQ + 1, 0);  // cbase[e*NQ+q]: first packed row
+  for (int64_t q = 0, r = 0; q < NQ; ++q) {
+    qoff[(size_t)q] = r;
+    for (int64_t e = 0; e < K; ++e) {
+      cbase[(size_t)(e * NQ + q)] = r;
+      const int64_t n = c->n_exec[(size_t)e];
+      r += std::max<int64_t>(0, std::min(n, chunk_t0[(size_t)q + 1] * B) - std::min(n, chunk_t0[(size_t)q] * B));
+    }
+    qoff[(size_t)q + 1] = r;
+  }
+  auto prow = [&](int64_t e, int64_t i) {  // packed row of client e's row i
+    const int64_t j = i / B;
+    int64_t q = 0;
+    while (chunk_t0[(size_t)q + 1] <= j) ++q;
+    return cbase[(size_t)(e * NQ + q)] + (i - std::min(i, chunk_t0[(size_t)q] * B));
+  };
   WaveSched& ws = c->ws;
   ws.ngroups = NG;
   ws.gbase.assign((size_t)NG + 1, 0);
@@ -594,7 +635,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   int32_t* h_bpre = h_steps + K;  // per wave: prefix sums of |b| over its A clients (A + 1 entries)
   for (int64_t e = 0; e < K; ++e) {
     int64_t id = c->local_ids[(size_t)c->exec[(size_t)e]];
-    for (int64_t i = 0; i < c->n_exec[(size_t)e]; ++i) h_src[c->pseg[(size_t)e] + i] = c->pop_off[(size_t)id] + i;
+    for (int64_t i = 0; i < c->n_exec[(size_t)e]; ++i) h_src[prow(e, i)] = c->pop_off[(size_t)id] + i;
     h_n[e] = c->n_exec[(size_t)e];
     h_steps[e] = (int32_t)c->steps_exec[(size_t)e];
   }
@@ -617,7 +658,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
           for (int64_t r = 0; r < B; ++r) {
             const int64_t i = j * B + r;
             if (i < n) {
-              srow[r] = (int32_t)(c->pseg[(size_t)e] + perm[(size_t)i]);
+              srow[r] = (int32_t)prow(e, perm[(size_t)i]);
               ++bsz;
             } else {
               srow[r] = -1;
@@ -736,29 +777,49 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   CK(cudaEventRecord(c->ev_tab, st));
   c->tab_pending = true;
   h2d += (int64_t)(sizeof(int64_t) * (R + K + ws.n_waves + 1) + sizeof(int32_t) * (n_sidx + 2 * n_bs + K + ws.n_waves));
-  // stage the cohort's samples: device population -> gather; host population -> H2D copies
+  // stage the cohort's samples: device population -> gather; host population -> H2D copies,
+  // chunk by chunk on the copy stream (the previous round has released xpack once st reaches
+  // ev_start), each chunk packed as soon as it lands
   const float* xsrc = (const float*)c->x;
   const int32_t* ysrc = c->y;
   const int64_t* srow = c->d_src_row;
+  c->prof.begin(st);
   if (!c->pop_dev && R > 0) {
-    for (int64_t e = 0; e < K; ++e) {
-      int64_t id = c->local_ids[(size_t)c->exec[(size_t)e]];
-      int64_t r0 = c->pop_off[(size_t)id], n = c->n_exec[(size_t)e];
-      CK(cudaMemcpyAsync(c->d_stage + c->pseg[(size_t)e] * L.D_in, (const float*)c->x + r0 * L.D_in,
-                         sizeof(float) * n * L.D_in, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(c->d_ystage + c->pseg[(size_t)e], c->y + r0, sizeof(int32_t) * n, cudaMemcpyHostToDevice,
-                         st));
+    while ((int64_t)c->ev_chunk.size() < NQ) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->ev_chunk.push_back(e);
+    }
+    cudaStream_t cs = c->prof.on ? st : c->cst;  // a profiled round stays serialised on st
+    if (cs != st) CK(cudaStreamWaitEvent(cs, c->ev_start, 0));
+    for (int64_t q = 0; q < NQ; ++q) {
+      for (int64_t e = 0; e < K; ++e) {
+        const int64_t n = c->n_exec[(size_t)e];
+        const int64_t i0 = std::min(n, chunk_t0[(size_t)q] * B), i1 = std::min(n, chunk_t0[(size_t)q + 1] * B);
+        if (i1 <= i0) continue;
+        const int64_t id = c->local_ids[(size_t)c->exec[(size_t)e]], r0 = c->pop_off[(size_t)id] + i0;
+        const int64_t dst = cbase[(size_t)(e * NQ + q)];
+        CK(cudaMemcpyAsync(c->d_stage + dst * L.D_in, (const float*)c->x + r0 * L.D_in,
+                           sizeof(float) * (i1 - i0) * L.D_in, cudaMemcpyHostToDevice, cs));
+        CK(cudaMemcpyAsync(c->d_ystage + dst, c->y + r0, sizeof(int32_t) * (i1 - i0), cudaMemcpyHostToDevice, cs));
+      }
+      const int64_t q0 = qoff[(size_t)q], nq = qoff[(size_t)q + 1] - q0;
+      if (cnn)
+        launches += pack_cnn(L, c->d_stage + q0 * L.D_in, nullptr, nq, c->d_xpack + q0 * L.D_pack,
+                             c->cb.xplanar + q0 * 16 * L.d.H0 * (L.d.W0 + 4), cs);
+      else
+        launches += gather_rows_f32(c->d_stage + q0 * L.D_in, nullptr, nq, L.D_pack, c->d_xpack + q0 * L.D_pack, cs);
+      launches += gather_i32(c->d_ystage + q0, nullptr, nq, c->d_ypack + q0, cs);
+      CK(cudaEventRecord(c->ev_chunk[(size_t)q], cs));
     }
     h2d += R * (int64_t)(L.D_in * sizeof(float) + sizeof(int32_t));
-    xsrc = c->d_stage;
-    ysrc = c->d_ystage;
-    srow = nullptr;
+    CK(cudaStreamWaitEvent(st, c->ev_chunk[0], 0));  // wave 0 needs chunk 0 (batch 0 of every client)
+  } else {
+    if (cnn) launches += pack_cnn(L, xsrc, srow, R, c->d_xpack, c->cb.xplanar, st);
+    else launches += gather_rows_f32(xsrc, srow, R, L.D_pack, c->d_xpack, st);
+    launches += gather_i32(ysrc, srow, R, c->d_ypack, st);
   }
-  c->prof.begin(st);
-  if (cnn) launches += pack_cnn(L, xsrc, srow, R, c->d_xpack, c->cb.xplanar, st);
-  else launches += gather_rows_f32(xsrc, srow, R, L.D_pack, c->d_xpack, st);
   if (cnn && c->cfg.math == 0 && conv1_tc_supported(L)) launches += c1wt_pack(c->d_theta + L.o_c1w, c->cb.c1wt_g, st);
-  launches += gather_i32(ysrc, srow, R, c->d_ypack, st);
   c->prof.end(K_PACK, 0, (double)R * (4.0 * (L.D_in + L.D_pack) + 8.0), st);
   CKL();
   CK(cudaEventRecord(c->ev_staged, st));
@@ -807,7 +868,15 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       }
       static const bool hostprof = getenv("FL_HOSTPROF") != nullptr;
       const auto th0 = std::chrono::steady_clock::now();
+      int64_t next_q = 1;
       for (int64_t t = 0; t < max_w; ++t) {
+        if (next_q < NQ && t == chunk_t0[(size_t)next_q] && !c->pop_dev && R > 0) {  // chunk next_q staged
+          for (int g = 0; g < ws.ngroups; ++g)
+            if (ws.gn[(size_t)g] && t < ws.gnw[(size_t)g] && gst[(size_t)g] != st)
+              CK(cudaStreamWaitEvent(gst[(size_t)g], c->ev_chunk[(size_t)next_q], 0));
+          if (c->prof.on) CK(cudaStreamWaitEvent(st, c->ev_chunk[(size_t)next_q], 0));
+          ++next_q;
+        }
         for (int g = 0; g < ws.ngroups; ++g) {
           if (ws.gn[(size_t)g] == 0 || t >= ws.gnw[(size_t)g]) continue;
           const int64_t k = ws.gw0[(size_t)g] + t, base = ws.gbase[(size_t)g];
