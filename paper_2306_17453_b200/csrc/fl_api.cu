@@ -784,34 +784,43 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   const int32_t* ysrc = c->y;
   const int64_t* srow = c->d_src_row;
   c->prof.begin(st);
+  cudaStream_t cs_stage = st;
+  int64_t q_issued = 0;
+  auto stage_chunk = [&](int64_t q) -> bool {  // H2D of chunk q's rows, then pack them, on cs_stage
+    for (int64_t e = 0; e < K; ++e) {
+      const int64_t n = c->n_exec[(size_t)e];
+      const int64_t i0 = std::min(n, chunk_t0[(size_t)q] * B), i1 = std::min(n, chunk_t0[(size_t)q + 1] * B);
+      if (i1 <= i0) continue;
+      const int64_t id = c->local_ids[(size_t)c->exec[(size_t)e]], r0 = c->pop_off[(size_t)id] + i0;
+      const int64_t dst = cbase[(size_t)(e * NQ + q)];
+      if (cudaMemcpyAsync(c->d_stage + dst * L.D_in, (const float*)c->x + r0 * L.D_in,
+                          sizeof(float) * (i1 - i0) * L.D_in, cudaMemcpyHostToDevice, cs_stage) != cudaSuccess ||
+          cudaMemcpyAsync(c->d_ystage + dst, c->y + r0, sizeof(int32_t) * (i1 - i0), cudaMemcpyHostToDevice,
+                          cs_stage) != cudaSuccess)
+        return false;
+    }
+    const int64_t q0 = qoff[(size_t)q], nq = qoff[(size_t)q + 1] - q0;
+    if (cnn)
+      launches += pack_cnn(L, c->d_stage + q0 * L.D_in, nullptr, nq, c->d_xpack + q0 * L.D_pack,
+                           c->cb.xplanar + q0 * 16 * L.d.H0 * (L.d.W0 + 4), cs_stage);
+    else
+      launches += gather_rows_f32(c->d_stage + q0 * L.D_in, nullptr, nq, L.D_pack, c->d_xpack + q0 * L.D_pack,
+                                  cs_stage);
+    launches += gather_i32(c->d_ystage + q0, nullptr, nq, c->d_ypack + q0, cs_stage);
+    return cudaEventRecord(c->ev_chunk[(size_t)q], cs_stage) == cudaSuccess;
+  };
   if (!c->pop_dev && R > 0) {
     while ((int64_t)c->ev_chunk.size() < NQ) {
       cudaEvent_t e;
       CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       c->ev_chunk.push_back(e);
     }
-    cudaStream_t cs = c->prof.on ? st : c->cst;  // a profiled round stays serialised on st
-    if (cs != st) CK(cudaStreamWaitEvent(cs, c->ev_start, 0));
-    for (int64_t q = 0; q < NQ; ++q) {
-      for (int64_t e = 0; e < K; ++e) {
-        const int64_t n = c->n_exec[(size_t)e];
-        const int64_t i0 = std::min(n, chunk_t0[(size_t)q] * B), i1 = std::min(n, chunk_t0[(size_t)q + 1] * B);
-        if (i1 <= i0) continue;
-        const int64_t id = c->local_ids[(size_t)c->exec[(size_t)e]], r0 = c->pop_off[(size_t)id] + i0;
-        const int64_t dst = cbase[(size_t)(e * NQ + q)];
-        CK(cudaMemcpyAsync(c->d_stage + dst * L.D_in, (const float*)c->x + r0 * L.D_in,
-                           sizeof(float) * (i1 - i0) * L.D_in, cudaMemcpyHostToDevice, cs));
-        CK(cudaMemcpyAsync(c->d_ystage + dst, c->y + r0, sizeof(int32_t) * (i1 - i0), cudaMemcpyHostToDevice, cs));
-      }
-      const int64_t q0 = qoff[(size_t)q], nq = qoff[(size_t)q + 1] - q0;
-      if (cnn)
-        launches += pack_cnn(L, c->d_stage + q0 * L.D_in, nullptr, nq, c->d_xpack + q0 * L.D_pack,
-                             c->cb.xplanar + q0 * 16 * L.d.H0 * (L.d.W0 + 4), cs);
-      else
-        launches += gather_rows_f32(c->d_stage + q0 * L.D_in, nullptr, nq, L.D_pack, c->d_xpack + q0 * L.D_pack, cs);
-      launches += gather_i32(c->d_ystage + q0, nullptr, nq, c->d_ypack + q0, cs);
-      CK(cudaEventRecord(c->ev_chunk[(size_t)q], cs));
-    }
+    cs_stage = c->prof.on ? st : c->cst;  // a profiled round stays serialised on st
+    if (cs_stage != st) CK(cudaStreamWaitEvent(cs_stage, c->ev_start, 0));
+    // chunks 0 and 1 now; chunk q >= 2 is issued from the wave loop when step chunk_t0[q-1]
+    // is issued, so the first waves are not queued behind every copy of the round
+    for (; q_issued < std::min<int64_t>(NQ, 2); ++q_issued)
+      if (!stage_chunk(q_issued)) return set_err(c, FL_ERR_CUDA, "staging copy failed");
     h2d += R * (int64_t)(L.D_in * sizeof(float) + sizeof(int32_t));
     CK(cudaStreamWaitEvent(st, c->ev_chunk[0], 0));  // wave 0 needs chunk 0 (batch 0 of every client)
   } else {
@@ -870,6 +879,8 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       const auto th0 = std::chrono::steady_clock::now();
       int64_t next_q = 1;
       for (int64_t t = 0; t < max_w; ++t) {
+        while (q_issued < NQ && !c->pop_dev && R > 0 && chunk_t0[(size_t)q_issued - 1] <= t)
+          if (!stage_chunk(q_issued++)) return set_err(c, FL_ERR_CUDA, "staging copy failed");
         if (next_q < NQ && t == chunk_t0[(size_t)next_q] && !c->pop_dev && R > 0) {  // chunk next_q staged
           for (int g = 0; g < ws.ngroups; ++g)
             if (ws.gn[(size_t)g] && t < ws.gnw[(size_t)g] && gst[(size_t)g] != st)
