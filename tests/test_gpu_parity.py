@@ -121,7 +121,7 @@ def test_logreg_shuffled_multi_epoch_host_population():
 RAGGED = np.array([1, 7, 32, 33, 70, 45], dtype=np.int64)
 
 
-@pytest.mark.parametrize("E,shuffle,on_device", [(1, 0, True), (2, 1, True), (2, 1, False)])
+@pytest.mark.parametrize("E,shuffle,on_device", [(1, 0, True), (2, 1, True), (2, 1, False), (2, 0, False)])
 def test_cnn_round_ragged(E, shuffle, on_device):
     wl = synth.preset("C2", n_pop=len(RAGGED), n_cohort=len(RAGGED), E=E, shuffle=shuffle)
     cohort = np.array([4, 0, 2, 5, 1, 3])
@@ -133,6 +133,29 @@ def test_cnn_round_ragged(E, shuffle, on_device):
     err = np.max(np.abs(out - ref))
     assert err <= TOL_ROUND, err
     assert np.max(np.abs(out - theta)) > 1e-4  # the round moved the model
+
+
+def test_host_population_pipelined_staging_is_bit_exact():
+    """A host population with shuffle = 0 is staged in chunks (batches [2^(q-1), 2^q) of every
+    client) overlapped with training, packed in chunk-major row order; every kernel reaches a
+    sample through the sidx tables, so θ_k and θ_new must equal the device-resident run's bit
+    for bit (clients up to 17 batches: 6 chunks, E = 2 re-reads chunk rows in epoch 2)."""
+    wl = synth.preset("C2", n_pop=40, n_cohort=40, E=2)
+    sizes = synth.client_sizes(wl)
+    sizes[:3] = [544, 1, 33]
+    _, x, y = synth.population(wl, sizes)
+    theta = synth.init_params("cnn")
+    res = []
+    for on_dev in (True, False):
+        ctx, keep = make_ctx(wl, sizes, x, y, theta, on_device=on_dev)
+        ctx.fl_place(np.arange(40))
+        ctx.fl_train_clients(0)
+        tk = np.stack([ctx.fl_get_client_params(c) for c in (0, 1, 2, 17)])
+        out, _ = ctx.fl_aggregate()
+        res.append((tk, out))
+        ctx.close()
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1], res[1][1])
 
 
 def test_speech_round_small():
