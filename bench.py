@@ -317,6 +317,8 @@ def main():
         barrier(world)
     ms_total = allmax(e0.elapsed_time(e1), world)
     st = ctx.fl_get_stats()
+    # "timedelta workers": slowest minus fastest rank's training time of the last round
+    timedelta = allmax(st["train_ms"], world) + allmax(-st["train_ms"], world)
     ms_step = ms_total / args.steps
     value = len(cohort) * args.steps / (ms_total * 1e-3)
     clocks = clk.summary()
@@ -362,8 +364,9 @@ def main():
                 "config": {"workload": desc, "clients": int(len(cohort)), "samples": int(sizes.sum()),
                            "B": wl.B, "E": wl.E, "lr": wl.lr, "model": wl.model, "parallelism": f"clients x{world}",
                            "l2": "per-round working set >> 126 MB L2 (no flush needed)"},
-                "round_stats": {k: st[k] for k in ["round_ms", "place_ms", "stage_ms", "train_ms", "agg_ms",
-                                                   "allreduce_ms", "waves", "steps_local", "kernels"]},
+                "round_stats": dict({k: st[k] for k in ["round_ms", "place_ms", "stage_ms", "train_ms", "agg_ms",
+                                                        "allreduce_ms", "waves", "steps_local", "kernels"]},
+                                    timedelta_ms=timedelta),
                 "kernels": kernel_table(kstats, args.math),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": int(st["kernels"]) * args.steps}

@@ -73,6 +73,12 @@ class RoundDriver:
                 self.coef, self.kinds = self._fit_all()
                 pol, coef = "lb_gpu", self.coef
         stats = self.ctx.fl_round(cohort, policy=pol, lb_coef=coef, round_index=round_index)
+        if self.world > 1 and self.allgather is not None:
+            # "timedelta workers": slowest minus fastest rank's training time this round
+            tr = np.asarray(self.allgather(np.array([stats["train_ms"], 0.0, 0.0, 0.0])), np.float64).reshape(-1, 4)
+            stats["timedelta_ms"] = float(tr[:, 0].max() - tr[:, 0].min())
+        else:
+            stats["timedelta_ms"] = 0.0
         if self.policy == "lb":
             _, m, t = self.ctx.fl_get_client_times()
             self.records.append((m.astype(np.float64), t))

@@ -85,3 +85,82 @@ def test_more_ranks_than_clients_gives_empty_shares():
     allreduce is unchanged (fl_aggregate handles K_local = 0)."""
     ids, off = fl.fl_place_plan("bu", [0, 1, 2], [5, 9, 1, 4], 4, 8)
     assert list(np.diff(off)) == [1, 1, 1, 0, 0, 0, 0, 0]
+
+
+# ------------------------------------------------------------------ LB loop across ranks (f1, f4)
+class _FakeCtx:
+    """Stands in for a rank's fl_ctx on CPU: placement through the library's host planner,
+    training time from a per-rank cost model t = speed · m (a heterogeneous pair of GPUs,
+    PAPER.md L427-430), completion records as fl_get_client_times returns them."""
+
+    def __init__(self, rank, world, sizes, B, speed):
+        self.cfg = type("C", (), {"world_size": world, "rank": rank})()
+        self.rank, self.world, self.sizes, self.B, self.speed = rank, world, sizes, B, speed
+        self.seen = []
+
+    def fl_set_timing_records(self, on=True):
+        pass
+
+    def fl_round(self, cohort, policy="bu", lb_coef=None, round_index=0):
+        ids, off = fl.fl_place_plan(policy, cohort, self.sizes, self.B, self.world, lb_coef)
+        self.seen.append((policy, None if lb_coef is None else np.array(lb_coef)))
+        self.local = ids[off[self.rank]:off[self.rank + 1]]
+        m = (self.sizes[self.local] + self.B - 1) // self.B
+        self.t = self.speed * m.astype(np.float64) + 0.5  # per-client job time of this GPU (L378)
+        return {"train_ms": float(self.speed * m.sum()), "clients_total": len(cohort)}
+
+    def fl_get_client_times(self):
+        m = (self.sizes[self.local] + self.B - 1) // self.B
+        return self.local, m, self.t
+
+
+def _lb_worker(rank, world, port, q):
+    try:
+        from paper_2306_17453_b200.driver import RoundDriver, sample_cohort
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+
+        def allgather(v):
+            out = [None] * world
+            dist.all_gather_object(out, np.asarray(v, np.float64).tolist())
+            return np.array(out)
+
+        wl = synth.preset("C3", n_pop=400, n_cohort=120)
+        sizes = synth.client_sizes(wl)
+        ctx = _FakeCtx(rank, world, sizes, wl.B, speed=1.0 if rank == 0 else 3.0)
+        drv = RoundDriver(ctx, policy="lb", allgather=allgather)
+        loads = []
+        for r in range(3):
+            st = drv.run(sample_cohort(400, 120, wl.seed, r), r)
+            loads.append(allgather([st["train_ms"], 0, 0, 0])[:, 0].tolist())
+        q.put((rank, [p for p, _ in ctx.seen], drv.coef.tolist(), loads, st["timedelta_ms"]))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, "error", repr(e), None, None))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_lb_loop_two_ranks_heterogeneous():
+    """RR bootstrap (L375), then every rank fits its own records (L378) and all ranks place
+    with the same gathered per-GPU fits (FL_PLACE_LB_GPU): the 3x slower rank gets ~1/3 of
+    the batches and the timedelta (L412) shrinks from RR's."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_lb_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    for rank, pols, coef, loads, td in res:
+        assert pols != "error", coef
+        assert pols == ["rr", "lb_gpu", "lb_gpu"]
+        # both ranks hold the same gathered fits; rank 1's slope is 3x rank 0's
+        assert np.allclose(coef, res[0][2])
+        assert coef[1][0] == pytest.approx(3 * coef[0][0], rel=1e-6)
+    loads = res[0][3]
+    rr_gap = abs(loads[0][0] - loads[0][1]) / max(loads[0])
+    lb_gap = abs(loads[2][0] - loads[2][1]) / max(loads[2])
+    assert lb_gap < 0.1 < rr_gap, (loads, rr_gap, lb_gap)
+    assert res[0][4] == pytest.approx(abs(loads[2][0] - loads[2][1]))
