@@ -366,6 +366,87 @@ __global__ void __launch_bounds__(256) k_lstm_gemm(GemmArgs p) {
     }
 }
 
+// 128x128 tiles, 8x8 outputs per thread (two 4-row x two 4-column quads, 64 apart, read as
+// float4 from shared memory), BK = 8 with register prefetch of the next k-tile.  Every output
+// accumulates its K products in ascending k with one fmaf each, the same order as the 64x64
+// k_lstm_gemm, so results are bit-identical; the 8x8 register block halves shared-memory
+// traffic per FMA.
+constexpr int G2_T = 128, G2_K = 8, G2_P = G2_T + 4;
+__global__ void __launch_bounds__(256) k_lstm_gemm128(GemmArgs p) {
+  pdl_wait();
+  __shared__ __align__(16) float As[2][G2_K][G2_P];
+  __shared__ __align__(16) float Bs[2][G2_K][G2_P];
+  const int a = blockIdx.z, i0 = blockIdx.y * G2_T, j0 = blockIdx.x * G2_T;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  // Loads of a 128 x 8 operand tile: 4 elements per thread.  Row-contiguous operands (the
+  // row index is the unit-stride one): thread = row lx, k = lk + 2q (a warp reads 32
+  // consecutive rows).  k-contiguous operands: thread = row tid/2, k = 4·(tid&1) + q (two
+  // threads read one row's 8 consecutive k).
+  const bool ka = p.A.Ty == 0x7fffffff && p.A.syt == 1, kb = p.Bm.Ty == 0x7fffffff && p.Bm.syt == 1;
+  const int rA = ka ? threadIdx.x >> 1 : threadIdx.x & 127, kA = ka ? 4 * (threadIdx.x & 1) : threadIdx.x >> 7;
+  const int rB = kb ? threadIdx.x >> 1 : threadIdx.x & 127, kB = kb ? 4 * (threadIdx.x & 1) : threadIdx.x >> 7;
+  const int dA = ka ? 1 : 2, dB = kb ? 1 : 2;  // k step between a thread's 4 elements
+  const bool va = i0 + rA < p.M, vb = j0 + rB < p.N;
+  const float* pa = p.A.base + (va ? p.A.xoff(a, i0 + rA) : 0);
+  const float* pb = p.Bm.base + (vb ? p.Bm.xoff(a, j0 + rB) : 0);
+  float ra[4], rb[4];
+  auto gload = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = k0 + kA + dA * q, kq = k0 + kB + dB * q;
+      ra[q] = (va && k < p.K) ? pa[p.A.yoff(k)] : 0.f;
+      rb[q] = (vb && kq < p.K) ? pb[p.Bm.yoff(kq)] : 0.f;
+    }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) As[buf][kA + dA * q][rA] = ra[q], Bs[buf][kB + dB * q][rB] = rb[q];
+  };
+  float acc[8][8] = {};
+  gload(0);
+  sstore(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < p.K; k0 += G2_K) {
+    const bool more = k0 + G2_K < p.K;
+    if (more) gload(k0 + G2_K);
+#pragma unroll
+    for (int kk = 0; kk < G2_K; ++kk) {
+      float av[8], bv[8];
+      *reinterpret_cast<float4*>(av) = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+      *reinterpret_cast<float4*>(av + 4) = *reinterpret_cast<const float4*>(&As[buf][kk][64 + ty * 4]);
+      *reinterpret_cast<float4*>(bv) = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+      *reinterpret_cast<float4*>(bv + 4) = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tx * 4]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[u][v] = fmaf(av[u], bv[v], acc[u][v]);
+    }
+    if (more) {
+      sstore(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int i = i0 + (u < 4 ? ty * 4 + u : 64 + ty * 4 + u - 4);
+      const int j = j0 + (v < 4 ? tx * 4 + v : 64 + tx * 4 + v - 4);
+      if (i >= p.M || j >= p.N) continue;
+      const int64_t o = (int64_t)(i / p.To) * p.o_r + (int64_t)(i % p.To) * p.o_t + (int64_t)j * p.o_j;
+      if (p.mode == 0) {
+        float r = acc[u][v];
+        if (p.bias0) r += p.bias0[a * p.b_sa + j];
+        if (p.bias1) r += p.bias1[a * p.b_sa + j];
+        p.out[a * p.o_sa + o] = r;
+      } else {
+        p.out[a * p.o_sa + o] = p.src[a * p.src_sa + o] - p.lr * acc[u][v];
+      }
+    }
+}
+
 // ---------------------------------------------------------------- embedding, layer-0 input
 // E[s][t][j] = emb[x_t][j]; Xp0[s][t][n] = W_ih0[n]·E[s][t] + b_ih0[n] + b_hh0[n].  One CTA per slot.
 struct EmbArgs {
@@ -566,8 +647,12 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
   }
   const int64_t S_T1 = (int64_t)(LT + 1) * LH;  // per-slot stride of H / C
   int n = 0;
+  static const bool g128 = env_knob("FL_LSTM_GEMM64", 0) == 0;
   auto gemm = [&](const GemmArgs& g) {
-    launch_pdl(wa.pdl, k_lstm_gemm, dim3((g.N + 63) / 64, (g.M + 63) / 64, A), 256, 0, st, g);
+    if (g128)
+      launch_pdl(wa.pdl, k_lstm_gemm128, dim3((g.N + G2_T - 1) / G2_T, (g.M + G2_T - 1) / G2_T, A), 256, 0, st, g);
+    else
+      launch_pdl(wa.pdl, k_lstm_gemm, dim3((g.N + 63) / 64, (g.M + 63) / 64, A), 256, 0, st, g);
     ++n;
   };
   const int M = B * LT;  // (batch row, time) rows per client
