@@ -22,8 +22,8 @@ timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_d
   --log-file gpurun_out/traffic.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_traffic.log 2>&1
 echo "traffic exit $?"
 for k in ${FULL_KERNELS:-k_fc1_bwd_tc k_conv5_tc k_conv2_dw_tc k_conv1_dw_tc k_conv1_fwd_tc}; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k "regex:$k" -s 2 -c 1 \
-    -o gpurun_out/full_$k python scripts/wave_once.py 100 2 2 > gpurun_out/ncu_full_$k.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$k" -s 1 -c 1 \
+    -o gpurun_out/full_$k python scripts/wave_once.py 100 3 2 > gpurun_out/ncu_full_$k.log 2>&1
   echo "full $k exit $?"
 done
 ls -la gpurun_out | tail -20
