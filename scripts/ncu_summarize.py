@@ -16,7 +16,7 @@ import sys
 CLASS = [  # (kernel-name regex, bench class); first match wins
     (r"k_fc1_bwd_tc", "fc1_dw_sgd"), (r"k_fc1_dw_tc", "fc1_dw_sgd"), (r"k_fc1_dx_tc", "fc1_dx"),
     (r"k_fc1_fwd", "fc1_fwd"), (r"k_conv5_tc<64", "conv2_fwd"), (r"k_conv5_tc<32", "conv2_dx"),
-    (r"k_conv2_dw_tc", "conv2_dw"), (r"k_dw2_reduce_sgd", "conv2_dw_reduce_sgd"), (r"k_conv1_dw_tc", "conv1_dw"),
+    (r"k_conv2_dw_tc", "conv2_dw"), (r"k_dw2_reduce_sgd|k_dw_reduce2_sgd", "conv2_dw_reduce_sgd"), (r"k_conv1_dw_tc", "conv1_dw"),
     (r"k_dw_reduce_sgd", "conv1_dw_reduce_sgd"), (r"k_conv1_fwd_tc", "conv1_fwd"), (r"k_head", "head_fc2_ce"),
     (r"k_pack|k_c1wt|k_gather", "pack"), (r"k_fedavg|k_finalize", "fedavg_accum"),
 ]
