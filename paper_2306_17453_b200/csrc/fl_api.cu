@@ -258,7 +258,8 @@ struct fl_ctx {
   // pipelined staging of a host population: copies + pack of chunk q run on cst and
   // complete on ev_chunk[q]; the waves of local step t >= chunk_t0[q] wait for it
   cudaStream_t cst = nullptr;
-  std::vector<cudaEvent_t> ev_chunk;
+  cudaStream_t pst = nullptr;  // high-priority pack stream: a pack kernel waiting for SMs never stalls the copies
+  std::vector<cudaEvent_t> ev_chunk, ev_copy;
 };
 
 // ---------------------------------------------------------------- error helpers
@@ -373,7 +374,10 @@ void fl_round_destroy(fl_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_chunk)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ev_copy)
+    if (e) cudaEventDestroy(e);
   if (c->cst) cudaStreamDestroy(c->cst);
+  if (c->pst) cudaStreamDestroy(c->pst);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
 }
@@ -449,6 +453,7 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   }
   if (!c->pop_dev) {
     CK(cudaStreamCreateWithFlags(&c->cst, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithPriority(&c->pst, cudaStreamNonBlocking, prio_hi));
     // borrowed host population: pin it so per-round staging copies run at full PCIe rate
     size_t xb = (size_t)c->pop_off.back() * (size_t)c->L.D_in * sizeof(float);
     if (cudaHostRegister((void*)c->x, xb, cudaHostRegisterReadOnly) == cudaSuccess) c->host_registered = true;
@@ -786,34 +791,52 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   c->prof.begin(st);
   cudaStream_t cs_stage = st;
   int64_t q_issued = 0;
+  // With several chunks (pipelined CNN staging) each chunk is staged group by group (exec
+  // order is group-contiguous, so a group's rows of a chunk are contiguous) and completes on
+  // its own event ev_chunk[q·NGc + g]: a group's waves wait only for their own rows.
+  const int64_t NGc = NQ > 1 ? ws.ngroups : 1;
   auto stage_chunk = [&](int64_t q) -> bool {  // H2D of chunk q's rows, then pack them, on cs_stage
-    for (int64_t e = 0; e < K; ++e) {
-      const int64_t n = c->n_exec[(size_t)e];
-      const int64_t i0 = std::min(n, chunk_t0[(size_t)q] * B), i1 = std::min(n, chunk_t0[(size_t)q + 1] * B);
-      if (i1 <= i0) continue;
-      const int64_t id = c->local_ids[(size_t)c->exec[(size_t)e]], r0 = c->pop_off[(size_t)id] + i0;
-      const int64_t dst = cbase[(size_t)(e * NQ + q)];
-      if (cudaMemcpyAsync(c->d_stage + dst * L.D_in, (const float*)c->x + r0 * L.D_in,
-                          sizeof(float) * (i1 - i0) * L.D_in, cudaMemcpyHostToDevice, cs_stage) != cudaSuccess ||
-          cudaMemcpyAsync(c->d_ystage + dst, c->y + r0, sizeof(int32_t) * (i1 - i0), cudaMemcpyHostToDevice,
-                          cs_stage) != cudaSuccess)
+    for (int64_t g = 0; g < NGc; ++g) {
+      const int64_t e0 = NGc == 1 ? 0 : ws.gbase[(size_t)g], e1 = NGc == 1 ? K : ws.gbase[(size_t)g + 1];
+      for (int64_t e = e0; e < e1; ++e) {
+        const int64_t n = c->n_exec[(size_t)e];
+        const int64_t i0 = std::min(n, chunk_t0[(size_t)q] * B), i1 = std::min(n, chunk_t0[(size_t)q + 1] * B);
+        if (i1 <= i0) continue;
+        const int64_t id = c->local_ids[(size_t)c->exec[(size_t)e]], r0 = c->pop_off[(size_t)id] + i0;
+        const int64_t dst = cbase[(size_t)(e * NQ + q)];
+        if (cudaMemcpyAsync(c->d_stage + dst * L.D_in, (const float*)c->x + r0 * L.D_in,
+                            sizeof(float) * (i1 - i0) * L.D_in, cudaMemcpyHostToDevice, cs_stage) != cudaSuccess ||
+            cudaMemcpyAsync(c->d_ystage + dst, c->y + r0, sizeof(int32_t) * (i1 - i0), cudaMemcpyHostToDevice,
+                            cs_stage) != cudaSuccess)
+          return false;
+      }
+      const int64_t q0 = e0 < K ? cbase[(size_t)(e0 * NQ + q)] : qoff[(size_t)q + 1];
+      const int64_t nq = (e1 < K ? cbase[(size_t)(e1 * NQ + q)] : qoff[(size_t)q + 1]) - q0;
+      // copies stay on the copy stream; the pack of these rows runs on ps once they landed
+      cudaStream_t ps = cs_stage == st ? st : c->pst;
+      if (ps != cs_stage && (cudaEventRecord(c->ev_copy[(size_t)(q * NGc + g)], cs_stage) != cudaSuccess ||
+                             cudaStreamWaitEvent(ps, c->ev_copy[(size_t)(q * NGc + g)], 0) != cudaSuccess))
         return false;
+      if (nq > 0) {
+        if (cnn)
+          launches += pack_cnn(L, c->d_stage + q0 * L.D_in, nullptr, nq, c->d_xpack + q0 * L.D_pack,
+                               c->cb.xplanar + q0 * 16 * L.d.H0 * (L.d.W0 + 4), ps);
+        else
+          launches += gather_rows_f32(c->d_stage + q0 * L.D_in, nullptr, nq, L.D_pack, c->d_xpack + q0 * L.D_pack,
+                                      ps);
+        launches += gather_i32(c->d_ystage + q0, nullptr, nq, c->d_ypack + q0, ps);
+      }
+      if (cudaEventRecord(c->ev_chunk[(size_t)(q * NGc + g)], ps) != cudaSuccess) return false;
     }
-    const int64_t q0 = qoff[(size_t)q], nq = qoff[(size_t)q + 1] - q0;
-    if (cnn)
-      launches += pack_cnn(L, c->d_stage + q0 * L.D_in, nullptr, nq, c->d_xpack + q0 * L.D_pack,
-                           c->cb.xplanar + q0 * 16 * L.d.H0 * (L.d.W0 + 4), cs_stage);
-    else
-      launches += gather_rows_f32(c->d_stage + q0 * L.D_in, nullptr, nq, L.D_pack, c->d_xpack + q0 * L.D_pack,
-                                  cs_stage);
-    launches += gather_i32(c->d_ystage + q0, nullptr, nq, c->d_ypack + q0, cs_stage);
-    return cudaEventRecord(c->ev_chunk[(size_t)q], cs_stage) == cudaSuccess;
+    return true;
   };
   if (!c->pop_dev && R > 0) {
-    while ((int64_t)c->ev_chunk.size() < NQ) {
-      cudaEvent_t e;
+    while ((int64_t)c->ev_chunk.size() < NQ * NGc) {
+      cudaEvent_t e, f;
       CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&f, cudaEventDisableTiming));
       c->ev_chunk.push_back(e);
+      c->ev_copy.push_back(f);
     }
     cs_stage = c->prof.on ? st : c->cst;  // a profiled round stays serialised on st
     if (cs_stage != st) CK(cudaStreamWaitEvent(cs_stage, c->ev_start, 0));
@@ -822,7 +845,8 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
     for (; q_issued < std::min<int64_t>(NQ, 2); ++q_issued)
       if (!stage_chunk(q_issued)) return set_err(c, FL_ERR_CUDA, "staging copy failed");
     h2d += R * (int64_t)(L.D_in * sizeof(float) + sizeof(int32_t));
-    CK(cudaStreamWaitEvent(st, c->ev_chunk[0], 0));  // wave 0 needs chunk 0 (batch 0 of every client)
+    // one chunk: everything waits for it; several: each group waits for its own rows (wave loop)
+    if (NQ == 1) CK(cudaStreamWaitEvent(st, c->ev_chunk[0], 0));
   } else {
     if (cnn) launches += pack_cnn(L, xsrc, srow, R, c->d_xpack, c->cb.xplanar, st);
     else launches += gather_rows_f32(xsrc, srow, R, L.D_pack, c->d_xpack, st);
@@ -877,15 +901,15 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       }
       static const bool hostprof = getenv("FL_HOSTPROF") != nullptr;
       const auto th0 = std::chrono::steady_clock::now();
-      int64_t next_q = 1;
+      int64_t next_q = 0;
+      const bool piped = !c->pop_dev && R > 0 && NQ > 1;
       for (int64_t t = 0; t < max_w; ++t) {
         while (q_issued < NQ && !c->pop_dev && R > 0 && chunk_t0[(size_t)q_issued - 1] <= t)
           if (!stage_chunk(q_issued++)) return set_err(c, FL_ERR_CUDA, "staging copy failed");
-        if (next_q < NQ && t == chunk_t0[(size_t)next_q] && !c->pop_dev && R > 0) {  // chunk next_q staged
+        if (piped && next_q < NQ && t == chunk_t0[(size_t)next_q]) {  // group g's rows of chunk next_q staged
           for (int g = 0; g < ws.ngroups; ++g)
-            if (ws.gn[(size_t)g] && t < ws.gnw[(size_t)g] && gst[(size_t)g] != st)
-              CK(cudaStreamWaitEvent(gst[(size_t)g], c->ev_chunk[(size_t)next_q], 0));
-          if (c->prof.on) CK(cudaStreamWaitEvent(st, c->ev_chunk[(size_t)next_q], 0));
+            if (ws.gn[(size_t)g] && t < ws.gnw[(size_t)g])
+              CK(cudaStreamWaitEvent(gst[(size_t)g], c->ev_chunk[(size_t)(next_q * NGc + g)], 0));
           ++next_q;
         }
         for (int g = 0; g < ws.ngroups; ++g) {
