@@ -329,6 +329,9 @@ def main():
     kstats = ctx.fl_get_kernel_stats()
     ctx.fl_set_profiling(False)
     roof = roofline(kstats, args.math, st_p["round_ms"])
+    ctx.close()  # the e2e context below needs the memory (C4: ~60 GB of activations per context)
+    del xd, yd
+    torch.cuda.empty_cache()
     # e2e: the public API with HOST buffers; H2D of this rank's cohort rows and D2H of θ_new per step
     e2e = None
     if not args.no_e2e:
@@ -357,7 +360,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None,
-                "dtype": "f32" if (args.math == 1 or wl.model == "lstm") else "tf32",
+                # speech and LSTM run FP32 SIMT kernels; CNN/logreg GEMMs TF32
+                "dtype": "f32" if (args.math == 1 or wl.model in ("lstm", "speech")) else "tf32",
                 "precision_note": "tensor-core GEMM operands tf32, fp32 accumulate; fp32 master weights, SGD, "
                                   "softmax-CE; fp64 FedAvg accumulation",
                 "data": "synthetic (seeded, SURVEY §8d laws), device-resident",
@@ -371,7 +375,6 @@ def main():
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": int(st["kernels"]) * args.steps}
         print(json.dumps(line), flush=True)
-    ctx.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
