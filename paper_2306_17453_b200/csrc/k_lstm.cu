@@ -3,12 +3,13 @@
 // softmax-CE (mean over |b|), BPTT, SGD (a7) — one wave = one step of every active client.
 //
 // The recurrences are the critical path (T dependent phases per layer, forward and
-// backward), so they run as thread-block CLUSTERS of 8 CTAs per client: each CTA keeps its
-// 128-row slice of W_hh (the i, f, g, o rows of 32 hidden units, padded k-major so the
+// backward), so they run as thread-block CLUSTERS of 16 CTAs per client (a non-portable
+// cluster size; 87 KB of shared memory per CTA so two CTAs share an SM): each CTA keeps its
+// 64-row slice of W_hh (the i, f, g, o rows of 16 hidden units, padded k-major so the
 // forward and the transposed backward products are both bank-conflict free) resident in
-// shared memory for all T steps, owns those 32 units' cell state, and exchanges h_t (forward)
+// shared memory for all T steps, owns those 16 units' cell state, and exchanges h_t (forward)
 // or the partial W_hhᵀ·dpre sums (backward, reduce-scatter) through distributed shared memory
-// with one cluster barrier per time step.  Everything that is not on the recurrence — the
+// with st.async stores that complete on the receivers' mbarriers (no per-step cluster barrier).  Everything that is not on the recurrence — the
 // input projections, dX of layer 2, every weight gradient (K = |b|·T) with the SGD step in its
 // epilogue, the embedding and the fc head — is batched per client outside the time loop.
 // Deterministic: every sum has a fixed order.
@@ -28,9 +29,9 @@ namespace flb {
 namespace {
 
 constexpr int LT = 80, LH = 256, LG = 1024, LE = 8, LV = 80;
-constexpr int CL = 8;              // CTAs per client cluster
-constexpr int UPC = LH / CL;       // 32 hidden units per CTA
-constexpr int RPC = 4 * UPC;       // 128 gate rows per CTA
+constexpr int CL = 16;             // CTAs per client cluster (non-portable size: 2 CTAs fit per SM)
+constexpr int UPC = LH / CL;       // 16 hidden units per CTA
+constexpr int RPC = 4 * UPC;       // 64 gate rows per CTA
 constexpr int WPF = LH + 4;       // fwd: row-major [RPC][LH] slice, pitch 260 (float4 rows, conflict-free)
 constexpr int WPB = RPC + 4;      // bwd: k-major [LH][RPC] slice, pitch 132 (float4 over rows, conflict-free)
 constexpr int REC_SMEM = (LH * WPB + 2 * 4 * LH + 4 * RPC + 2 * CL * 4 * UPC) * 4 + 64;  // + 2 mbarriers
@@ -54,7 +55,7 @@ static_assert(RPC * WPF <= LH * WPB, "both slice layouts fit the same smem carve
 __device__ __forceinline__ float sigm(float v) { return 1.f / (1.f + __expf(-v)); }
 
 // global gate row of local row rl of cluster rank c: gate rl/32 (i, f, g, o), unit 32c + rl%32
-__device__ __forceinline__ int grow_of(int rl, int c) { return (rl >> 5) * LH + UPC * c + (rl & 31); }
+__device__ __forceinline__ int grow_of(int rl, int c) { return (rl / UPC) * LH + UPC * c + (rl % UPC); }
 
 struct RecArgs {
   const float* wsrc;   // client a's parameters at wsrc + a*wstride (θ_g on the first wave: stride 0)
@@ -74,8 +75,9 @@ struct RecArgs {
 // Thread (rl, kq) = (tid / 4, tid % 4) accumulates gate row rl over k-quarter kq for all 4
 // batch rows with 16 independent FMA chains (float4 loads of W and h); the 4 threads of a row
 // combine with two shuffles.  The next step's input projection is prefetched during the step.
-constexpr int FT = 512;
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(FT, 1) k_lstm_fwd(RecArgs p) {
+constexpr int FT = 4 * RPC;  // thread (row, k-quarter)
+constexpr int NOWN = 4 * UPC;  // cell-owner threads: (batch row, unit)
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(FT, 2) k_lstm_fwd(RecArgs p) {
   pdl_wait();
   cg::cluster_group cl = cg::this_cluster();
   const int c = (int)cl.block_rank(), a = blockIdx.x / CL, tid = threadIdx.x;
@@ -93,10 +95,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(FT, 1) k_lstm_fwd(R
     }
   }
   for (int e = tid; e < 2 * 4 * LH; e += FT) hb[e] = 0.f;
-  const int cb = tid >> 5, cu = tid & 31, unit = UPC * c + cu;  // cell owned by threads < 128
+  const int cb = tid / UPC, cu = tid % UPC, unit = UPC * c + cu;  // cell owned by threads < NOWN
   const int64_t cs = (int64_t)a * p.B + cb;
   float cst = 0.f;
-  if (tid < 128) {
+  if (tid < NOWN) {
     p.C[cs * (LT + 1) * LH + unit] = 0.f;
     p.H[cs * (LT + 1) * LH + unit] = 0.f;
   }
@@ -111,15 +113,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(FT, 1) k_lstm_fwd(R
     tc::mbar_init(hbar + 1, 1);
     tc::fence_mbar_init();
   }
-  // remote addresses of this cell's h slot in every CTA's two buffers and their barriers
-  uint32_t rh[CL], rbar[CL];
-  {
-    const uint32_t lh = tc::smem_u32(hb + cb * LH + unit), lb = tc::smem_u32(hbar);
-#pragma unroll
-    for (int r = 0; r < CL; ++r) rh[r] = mapa_u32(lh, r), rbar[r] = mapa_u32(lb, r);
-  }
+  // this cell's h slot and the barriers, mapped into each peer's shared memory at the store
+  const uint32_t lh = tc::smem_u32(hb + cb * LH + unit), lb = tc::smem_u32(hbar);
   cl.sync();
-  const bool tg = (rl >> 5) == 2;  // the cell-candidate gate uses tanh
+  const bool tg = rl / UPC == 2;  // the cell-candidate gate uses tanh
   float sv[6];
   for (int t = 0; t < LT; ++t) {
     const int cur = t & 1, nxt = cur ^ 1;
@@ -157,20 +154,20 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(FT, 1) k_lstm_fwd(R
 #pragma unroll
       for (int b = 0; b < 4; ++b) gs[b * RPC + rl] = tg ? tanhf(acc[b]) : sigm(acc[b]);
     __syncthreads();
-    if (tid < 128) {
-      const float ig = gs[cb * RPC + cu], fg = gs[cb * RPC + 32 + cu], gg = gs[cb * RPC + 64 + cu],
-                  og = gs[cb * RPC + 96 + cu];
+    if (tid < NOWN) {
+      const float ig = gs[cb * RPC + cu], fg = gs[cb * RPC + UPC + cu], gg = gs[cb * RPC + 2 * UPC + cu],
+                  og = gs[cb * RPC + 3 * UPC + cu];
       cst = fg * cst + ig * gg;                 // c_t = f c_{t-1} + i g
       const float hv = og * tanhf(cst);         // h_t = o tanh(c_t)
       if (t + 1 < LT)
 #pragma unroll
-        for (int r = 0; r < CL; ++r) st_async_f32(rh[r] + nxt * 4 * LH * 4, hv, rbar[r] + nxt * 8);
+        for (int r = 0; r < CL; ++r) st_async_f32(mapa_u32(lh + nxt * 4 * LH * 4, r), hv, mapa_u32(lb + nxt * 8, r));
       sv[0] = cst, sv[1] = hv, sv[2] = ig, sv[3] = fg, sv[4] = gg, sv[5] = og;
     }
     __syncthreads();  // gs is rewritten by the next step
     // No cluster barrier per step: a CTA cannot run ahead into a buffer still being read,
     // because its next step needs every CTA's h_t, which each sends only after reading h_{t-1}.
-    if (tid < 128) {
+    if (tid < NOWN) {
       p.C[(cs * (LT + 1) + t + 1) * LH + unit] = sv[0];
       p.H[(cs * (LT + 1) + t + 1) * LH + unit] = sv[1];
       float* g = p.G + (cs * LT + t) * LG + unit;
@@ -186,7 +183,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(FT, 1) k_lstm_fwd(R
 // Backward (BPTT) recurrence of one layer for one client.  The cell owners prefetch the next
 // (earlier) step's gates, cell states and external gradient while the current step's
 // W_hhᵀ·dpre partials (thread k, float4 over rows) are formed and reduce-scattered.
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 1) k_lstm_bwd(RecArgs p) {
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2) k_lstm_bwd(RecArgs p) {
   pdl_wait();
   cg::cluster_group cl = cg::this_cluster();
   const int c = (int)cl.block_rank(), a = blockIdx.x / CL, tid = threadIdx.x;
@@ -202,7 +199,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 1) k_lstm_bwd(
       Wt[k * WPB + rl] = __ldg(W + (int64_t)grow_of(rl, c) * LH + k);
     }
   }
-  const int cb = tid >> 5, cu = tid & 31, unit = UPC * c + cu;
+  const int cb = tid / UPC, cu = tid % UPC, unit = UPC * c + cu;
   const int64_t cs = (int64_t)a * p.B + cb;
   float dcs = 0.f, dhr = 0.f;  // carried dL/dc_t and the recurrent dL/dh_t of this cell
   // per-step inputs of the cell owners, prefetched one step ahead
@@ -214,7 +211,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 1) k_lstm_bwd(
     ncp = p.C[(cs * (LT + 1) + t) * LH + unit];
     nex = p.ext_mode == 0 ? ((t == LT - 1) ? p.ext[cs * LH + unit] : 0.f) : p.ext[(cs * LT + t) * LH + unit];
   };
-  if (tid < 128) fetch(LT - 1);
+  if (tid < NOWN) fetch(LT - 1);
   float sd[4];
   if (tid == 0) {
     tc::mbar_init(pbar, 1);
@@ -228,7 +225,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 1) k_lstm_bwd(
   for (int t = LT - 1; t >= 0; --t) {
     const int pb = t & 1;
     if (tid == 0 && t > 0) tc::mbar_expect_tx(pbar + pb, XCH_BYTES);
-    if (tid < 128) {
+    if (tid < NOWN) {
       const float dh = dhr + nex;
       const float ig = nig, fg = nfg, gg = ngg, og = nog, ct = nct, cp = ncp;
       if (t > 0) fetch(t - 1);
@@ -238,9 +235,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 1) k_lstm_bwd(
                   dg = dct * ig * (1.f - gg * gg), dob = dh * tc * og * (1.f - og);
       dcs = dct * fg;
       ds[cu * 4 + cb] = di;
-      ds[(32 + cu) * 4 + cb] = df;
-      ds[(64 + cu) * 4 + cb] = dg;
-      ds[(96 + cu) * 4 + cb] = dob;
+      ds[(UPC + cu) * 4 + cb] = df;
+      ds[(2 * UPC + cu) * 4 + cb] = dg;
+      ds[(3 * UPC + cu) * 4 + cb] = dob;
       sd[0] = di, sd[1] = df, sd[2] = dg, sd[3] = dob;
     }
     __syncthreads();
@@ -270,7 +267,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 1) k_lstm_bwd(
         for (int b = 0; b < 4; ++b) st_async_f32(rpart + (pb * CL * 4 + b) * UPC * 4, acc[b], rpbar + pb * 8);
     }
     if (t > 0) tc::mbar_wait(pbar + pb, ((LT - 1 - t) >> 1) & 1);  // all 8 CTAs' partials for my units
-    if (tid < 128) {  // fixed source order
+    if (tid < NOWN) {  // fixed source order
       float s = 0.f;
 #pragma unroll
       for (int src = 0; src < CL; ++src) s += part[((pb * CL + src) * 4 + cb) * UPC + cu];
@@ -642,6 +639,10 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
   if (!attr) {
     cudaFuncSetAttribute(k_lstm_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, REC_SMEM);
     cudaFuncSetAttribute(k_lstm_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, REC_SMEM);
+    if (CL > 8) {  // 16-CTA clusters are a non-portable size
+      cudaFuncSetAttribute(k_lstm_fwd, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_lstm_bwd, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
     cudaFuncSetAttribute(k_lstm_head, cudaFuncAttributeMaxDynamicSharedMemorySize, LV * LH * 4);
     attr = true;
   }
