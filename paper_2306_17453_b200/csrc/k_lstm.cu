@@ -33,7 +33,7 @@ constexpr int CL = 16;             // CTAs per client cluster (non-portable size
 constexpr int UPC = LH / CL;       // 16 hidden units per CTA
 constexpr int RPC = 4 * UPC;       // 64 gate rows per CTA
 constexpr int WPF = LH + 4;       // fwd: row-major [RPC][LH] slice, pitch 260 (float4 rows, conflict-free)
-constexpr int WPB = RPC + 4;      // bwd: k-major [LH][RPC] slice, pitch 132 (float4 over rows, conflict-free)
+constexpr int WPB = RPC + 4;      // bwd: k-major [LH][RPC] slice, pitch 68 (float4 over rows)
 constexpr int REC_SMEM = (LH * WPB + 2 * 4 * LH + 4 * RPC + 2 * CL * 4 * UPC) * 4 + 64;  // + 2 mbarriers
 constexpr uint32_t XCH_BYTES = CL * 4 * UPC * 4;  // bytes one CTA receives per step (8 sources x 4 rows x 32)
 
@@ -71,7 +71,7 @@ struct RecArgs {
   float* dpre;         // bwd: [S][T][LG] gradient of the gate pre-activations
 };
 
-// Forward recurrence of one layer for one client (cluster of 8 CTAs, 512 threads each).
+// Forward recurrence of one layer for one client (cluster of CL = 16 CTAs, 4·RPC = 256 threads each).
 // Thread (rl, kq) = (tid / 4, tid % 4) accumulates gate row rl over k-quarter kq for all 4
 // batch rows with 16 independent FMA chains (float4 loads of W and h); the 4 threads of a row
 // combine with two shuffles.  The next step's input projection is prefetched during the step.
@@ -121,7 +121,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(FT, 2) k_lstm_fwd(R
   for (int t = 0; t < LT; ++t) {
     const int cur = t & 1, nxt = cur ^ 1;
     if (tid == 0 && t + 1 < LT) tc::mbar_expect_tx(hbar + nxt, XCH_BYTES);  // h_t lands in buffer nxt
-    if (t > 0) tc::mbar_wait(hbar + cur, ((t - 1) >> 1) & 1);                // h_{t-1} from all 8 CTAs
+    if (t > 0) tc::mbar_wait(hbar + cur, ((t - 1) >> 1) & 1);                // h_{t-1} from all CL CTAs
     float acc[4] = {xn[0], xn[1], xn[2], xn[3]};
     if (kh == 0 && t + 1 < LT)
 #pragma unroll
@@ -266,7 +266,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2) k_lstm_bwd(
 #pragma unroll
         for (int b = 0; b < 4; ++b) st_async_f32(rpart + (pb * CL * 4 + b) * UPC * 4, acc[b], rpbar + pb * 8);
     }
-    if (t > 0) tc::mbar_wait(pbar + pb, ((LT - 1 - t) >> 1) & 1);  // all 8 CTAs' partials for my units
+    if (t > 0) tc::mbar_wait(pbar + pb, ((LT - 1 - t) >> 1) & 1);  // all CL CTAs' partials for my units
     if (tid < NOWN) {  // fixed source order
       float s = 0.f;
 #pragma unroll
