@@ -74,7 +74,9 @@ __global__ void __launch_bounds__(F_THREADS, 1)
   // would stall other streams' kernels) or touching anything it writes.
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the shared array (an integer round trip would turn every
+  // epilogue access into a generic LD/ST instead of LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Q_BAR);
   uint64_t* empty = full + Q_NST;
   uint64_t* afull = empty + Q_NST;
@@ -269,7 +271,9 @@ __global__ void __launch_bounds__(192, 1)
   pdl_wait();
   const int a0 = c1_client_of(p.bpre, p.A, u0 / H);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the shared array (an integer round trip would turn every
+  // epilogue access into a generic LD/ST instead of LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + D_BAR);
   uint64_t* empty = full + D_NST;
   uint64_t* bready = empty + D_NST;  // B tile expanded (128 arrivals)

@@ -74,7 +74,9 @@ __global__ void __launch_bounds__(192, 1)
   pdl_wait();
   const int a0 = client_of(p.bpre, p.A, u0 >> 3);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the shared array (an integer round trip would turn every
+  // epilogue access into a generic LD/ST instead of LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;

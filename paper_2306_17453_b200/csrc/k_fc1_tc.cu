@@ -52,7 +52,9 @@ __global__ void __launch_bounds__(192, 1)
   // would stall other streams' kernels) or touching anything it writes.
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the shared array (an integer round trip would turn every
+  // epilogue access into a generic LD/ST instead of LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + FW_BAR);
   uint64_t* empty = full + FW_NST;
   uint64_t* tfull = empty + FW_NST;
@@ -162,7 +164,9 @@ __global__ void __launch_bounds__(192, 1)
   // would stall other streams' kernels) or touching anything it writes.
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the shared array (an integer round trip would turn every
+  // epilogue access into a generic LD/ST instead of LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + DX_BAR);
   uint64_t* empty = full + DX_NST;
   uint64_t* tfull = empty + DX_NST;
@@ -282,7 +286,9 @@ __global__ void __launch_bounds__(192, 1)
   // would stall other streams' kernels) or touching anything it writes.
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the shared array (an integer round trip would turn every
+  // epilogue access into a generic LD/ST instead of LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sw = smem;                  // W tile
   uint8_t* sa = smem + DW_W;           // dhᵀ
   uint8_t* sbp = sa + DW_A;            // p2ᵀ
@@ -410,7 +416,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   const int KT = p.F / 128, T = p.A * KT, nch = p.HID / 128;
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the shared array (an integer round trip would turn every
+  // epilogue access into a generic LD/ST instead of LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + BW_BAR);
   uint64_t* empty = full + BW_NST;
   uint64_t* gfull = empty + BW_NST;
