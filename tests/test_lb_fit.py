@@ -211,3 +211,29 @@ def test_lb_loop_three_rounds():
     assert np.all(np.isfinite(theta))
     # records accumulate across rounds ("keep all the data")
     assert sum(len(r[0]) for r in drv.records) == 48
+
+
+@pytest.mark.gpu
+def test_timing_records_logreg_and_lstm():
+    """Every model records: logreg trains all clients in one launch (one shared record),
+    the LSTM's waves are serial, so a client with more steps finishes strictly later."""
+    import paper_2306_17453_b200 as fl
+    ctx, sizes, wl = _ctx("logreg", "C1")
+    ctx.fl_set_timing_records(True)
+    ctx.fl_round(synth.cohort(wl))
+    ids, m, t = ctx.fl_get_client_times()
+    assert len(ids) == wl.n_cohort and np.all(t > 0) and np.all(t == t[0])
+    ctx.close()
+    wl = synth.preset("C5", n_pop=6, n_cohort=6)
+    sizes = np.array([4, 8, 12, 4, 20, 9], dtype=np.int64)
+    _, x, y = synth.population(wl, sizes)
+    ctx = fl.fl_round_init(fl.Config(model="lstm", batch_size=4, lr=wl.lr), sizes, x, y, synth.init_params("lstm"))
+    ctx.fl_set_timing_records(True)
+    ctx.fl_round(np.arange(6))
+    ids, m, t = ctx.fl_get_client_times()
+    for i in range(6):
+        for j in range(6):
+            if m[i] > m[j]:
+                assert t[i] > t[j]
+            elif m[i] == m[j]:
+                assert t[i] == t[j]
