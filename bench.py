@@ -62,26 +62,40 @@ def pop_for(wl):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md).
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    The sampler is started before the region and waits for its first sample (nvidia-smi takes
+    ~100 ms to start); samples carry a timestamp and only those inside [mark_start, mark_end]
+    are summarised (the nearest ones if the region is shorter than the 20 ms interval)."""
+
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpus):
         self.gpus = gpus
         self.proc = None
         self.path = tempfile.mktemp(suffix=".csv")
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100", "-i", ",".join(map(str, self.gpus))],
+                                          "-lms", "20", "-i", ",".join(map(str, self.gpus))],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
+            deadline = time.time() + 5.0
+            while time.time() < deadline and os.path.getsize(self.path) == 0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def __exit__(self, *a):
         if self.proc:
@@ -92,22 +106,34 @@ class ClockSampler:
                 self.proc.kill()
             self.f.close()
 
+    @staticmethod
+    def _ts(field):
+        import datetime
+        try:
+            return datetime.datetime.strptime(field.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return None
+
     def summary(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         rows = []
         for line in open(self.path):
             p = [s.strip() for s in line.split(",")]
-            if len(p) >= 9 and p[1].replace(".", "").isdigit():
-                rows.append(p)
+            if len(p) >= 10 and p[2].replace(".", "").isdigit():
+                rows.append((self._ts(p[0]), p[1:]))
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
-        sm = [float(r[1]) for r in rows]
-        mx = max(float(r[2]) for r in rows)
+        inside = [r for t, r in rows if t is not None and self.t0 is not None and self.t1 is not None
+                  and self.t0 - 0.025 <= t <= self.t1 + 0.025]
+        sel = inside or [r for _, r in rows]
+        sm = [float(r[1]) for r in sel]
+        mx = max(float(r[2]) for r in sel)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows),
-                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+        reasons = sorted({names[i] for r in sel for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": reasons, "samples": len(sel),
+                "samples_in_timed_region": len(inside),
+                "power_w_max": max((float(r[3]) for r in sel if r[3].replace(".", "").isdigit()), default=None)}
 
 
 def peaks():
@@ -308,12 +334,14 @@ def main():
     with ClockSampler(list(range(world)) if rank == 0 else [local]) as clk:
         barrier(world)
         torch.cuda.synchronize()
+        clk.mark_start()
         e0.record(stream)
         for _ in range(args.steps):
             ctx.fl_round(cohort, round_index=rnd, stats=False)
             rnd += 1
         e1.record(stream)
         torch.cuda.synchronize()
+        clk.mark_end()
         barrier(world)
     ms_total = allmax(e0.elapsed_time(e1), world)
     st = ctx.fl_get_stats()
