@@ -180,6 +180,121 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(FT, 2) k_lstm_fwd(R
   cl.sync();  // no CTA exits while a peer may still address its shared memory
 }
 
+// Forward recurrence, register-resident variant: W_hh is constant over the T steps, so each
+// thread keeps its 4-row x 16-column segment of the CTA's slice in registers for the whole
+// sequence.  Thread (rg, ks) = (tid / 16, tid % 16) owns rows 4·rg .. 4·rg+3 and columns
+// {4·ks + 64·j + u}; per step it reads 16 float4 of h_{t-1} (each feeds 4 rows, 16 FMAs) and
+// the 16 partial (row, batch) sums of a row group are reduce-scattered over its 16 lanes
+// with 15 shuffles (fixed butterfly order); lane ks then owns (row, batch) j = bitrev4(ks).
+// Shared-memory traffic per step is a quarter of k_lstm_fwd's (which re-reads h for every row).
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(FT, 2) k_lstm_fwd_reg(RecArgs p) {
+  pdl_wait();
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank(), a = blockIdx.x / CL, tid = threadIdx.x;
+  extern __shared__ float sm[];
+  float* hb = sm + LH * WPB;       // [2][4][LH] h_{t-1} of the 4 batch rows (ping-pong)
+  float* gs = hb + 2 * 4 * LH;     // [4][RPC] activated gates of this CTA's rows
+  uint64_t* hbar = reinterpret_cast<uint64_t*>(sm + LH * WPB + 2 * 4 * LH + 4 * RPC + 2 * CL * 4 * UPC);  // [2]
+  const int rg = tid >> 4, ks = tid & 15;
+  float4 w[4][4];  // [row r][column block j]: W_hh[row 4rg+r][4ks + 64j .. +3]
+  {
+    const float* W = p.wsrc + (int64_t)a * p.wstride + p.o_whh;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        w[r][j] = __ldg(reinterpret_cast<const float4*>(W + (int64_t)grow_of(4 * rg + r, c) * LH + 4 * ks + 64 * j));
+  }
+  for (int e = tid; e < 2 * 4 * LH; e += FT) hb[e] = 0.f;
+  const int cb = tid / UPC, cu = tid % UPC, unit = UPC * c + cu;  // cell owned by threads < NOWN
+  const int64_t cs = (int64_t)a * p.B + cb;
+  float cst = 0.f;
+  if (tid < NOWN) {
+    p.C[cs * (LT + 1) * LH + unit] = 0.f;
+    p.H[cs * (LT + 1) * LH + unit] = 0.f;
+  }
+  // the (row, batch) this lane owns after the reduce-scatter
+  const int jo = ((ks & 1) << 3) | ((ks & 2) << 1) | ((ks & 4) >> 1) | ((ks & 8) >> 3);
+  const int orow = 4 * rg + (jo >> 2), ob = jo & 3, gr = grow_of(orow, c);
+  const int64_t s0 = (int64_t)a * p.B;
+  const float* xr = p.xp + (s0 + ob) * LT * LG + gr;  // step t at xr + t*LG
+  float xn = xr[0];
+  if (tid == 0) {
+    tc::mbar_init(hbar, 1);
+    tc::mbar_init(hbar + 1, 1);
+    tc::fence_mbar_init();
+  }
+  const uint32_t lh = tc::smem_u32(hb + cb * LH + unit), lb = tc::smem_u32(hbar);
+  cl.sync();
+  const bool tg = orow / UPC == 2;  // the cell-candidate gate uses tanh
+  float sv[6];
+  for (int t = 0; t < LT; ++t) {
+    const int cur = t & 1, nxt = cur ^ 1;
+    if (tid == 0 && t + 1 < LT) tc::mbar_expect_tx(hbar + nxt, XCH_BYTES);
+    if (t > 0) tc::mbar_wait(hbar + cur, ((t - 1) >> 1) & 1);
+    const float xcur = xn;
+    if (t + 1 < LT) xn = xr[(int64_t)(t + 1) * LG];
+    float v[16];  // v[r*4 + b]
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = 0.f;
+    const float* h = hb + cur * 4 * LH + 4 * ks;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const float4 hv = *reinterpret_cast<const float4*>(h + b * LH + 64 * j);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          float q = v[r * 4 + b];
+          q = fmaf(w[r][j].x, hv.x, q);
+          q = fmaf(w[r][j].y, hv.y, q);
+          q = fmaf(w[r][j].z, hv.z, q);
+          q = fmaf(w[r][j].w, hv.w, q);
+          v[r * 4 + b] = q;
+        }
+      }
+    // reduce-scatter over the 16 lanes of the row group: level L keeps the half selected by
+    // lane bit L and adds the partner's other half
+#pragma unroll
+    for (int L = 0; L < 4; ++L) {
+      const int n = 16 >> L, hlf = n >> 1;
+      const bool up = (ks >> L) & 1;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i < hlf) {
+          const float send = up ? v[i] : v[i + hlf];
+          const float keep = up ? v[i + hlf] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1 << L);
+        }
+      }
+    }
+    const float pre = v[0] + xcur;
+    gs[ob * RPC + orow] = tg ? tanhf(pre) : sigm(pre);
+    __syncthreads();
+    if (tid < NOWN) {
+      const float ig = gs[cb * RPC + cu], fg = gs[cb * RPC + UPC + cu], gg = gs[cb * RPC + 2 * UPC + cu],
+                  og = gs[cb * RPC + 3 * UPC + cu];
+      cst = fg * cst + ig * gg;                 // c_t = f c_{t-1} + i g
+      const float hv = og * tanhf(cst);         // h_t = o tanh(c_t)
+      if (t + 1 < LT)
+#pragma unroll
+        for (int r = 0; r < CL; ++r) st_async_f32(mapa_u32(lh + nxt * 4 * LH * 4, r), hv, mapa_u32(lb + nxt * 8, r));
+      sv[0] = cst, sv[1] = hv, sv[2] = ig, sv[3] = fg, sv[4] = gg, sv[5] = og;
+    }
+    __syncthreads();  // gs is rewritten by the next step
+    if (tid < NOWN) {
+      p.C[(cs * (LT + 1) + t + 1) * LH + unit] = sv[0];
+      p.H[(cs * (LT + 1) + t + 1) * LH + unit] = sv[1];
+      float* g = p.G + (cs * LT + t) * LG + unit;
+      g[0] = sv[2];
+      g[LH] = sv[3];
+      g[2 * LH] = sv[4];
+      g[3 * LH] = sv[5];
+    }
+  }
+  cl.sync();  // no CTA exits while a peer may still address its shared memory
+}
+
 // Backward (BPTT) recurrence of one layer for one client.  The cell owners prefetch the next
 // (earlier) step's gates, cell states and external gradient while the current step's
 // W_hhᵀ·dpre partials (thread k, float4 over rows) are formed and reduce-scattered.
@@ -638,9 +753,11 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_lstm_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, REC_SMEM);
+    cudaFuncSetAttribute(k_lstm_fwd_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, REC_SMEM);
     cudaFuncSetAttribute(k_lstm_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, REC_SMEM);
     if (CL > 8) {  // 16-CTA clusters are a non-portable size
       cudaFuncSetAttribute(k_lstm_fwd, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_lstm_fwd_reg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaFuncSetAttribute(k_lstm_bwd, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     }
     cudaFuncSetAttribute(k_lstm_head, cudaFuncAttributeMaxDynamicSharedMemorySize, LV * LH * 4);
@@ -661,7 +778,9 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
   EmbArgs ea{xpack, wa.sidx, wbase, wstride, q.emb, q.wih[0], q.bih[0], q.bhh[0], B, b.E, b.xp};
   launch_pdl(wa.pdl, k_lstm_embed, dim3(A * B), 256, 0, st, ea), ++n;
   RecArgs r0{wbase, wstride, q.whh[0], B, b.xp, b.G0, b.C0, b.H0, nullptr, 0, nullptr};
-  launch_pdl(wa.pdl, k_lstm_fwd, dim3(A * CL), FT, REC_SMEM, st, r0), ++n;
+  static const bool fwd_reg = env_knob("FL_LSTM_FWD_SMEM", 0) == 0;
+  auto fwd = fwd_reg ? k_lstm_fwd_reg : k_lstm_fwd;
+  launch_pdl(wa.pdl, fwd, dim3(A * CL), FT, REC_SMEM, st, r0), ++n;
   // layer-1 input projection: xp[s][t] = W_ih1 · H0[s][t+1] + b_ih1 + b_hh1
   {
     GemmArgs g{};
@@ -673,7 +792,7 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
     gemm(g);
   }
   RecArgs r1{wbase, wstride, q.whh[1], B, b.xp, b.G1, b.C1, b.H1, nullptr, 0, nullptr};
-  launch_pdl(wa.pdl, k_lstm_fwd, dim3(A * CL), FT, REC_SMEM, st, r1), ++n;
+  launch_pdl(wa.pdl, fwd, dim3(A * CL), FT, REC_SMEM, st, r1), ++n;
   // ---- head (fc SGD) and layer-1 BPTT
   HeadArgs ha{b.H1, ypack, wa.sidx, wa.bs, wbase, wstride, slots, L.P_pad, q.wfc, q.bfc, B, lr, b.dhT};
   launch_pdl(wa.pdl, k_lstm_head, dim3(A), 256, LV * LH * 4, st, ha), ++n;
