@@ -51,7 +51,9 @@ bool make_layout(int model, Layout* L) {
   CnnDims& d = L->d;
   if (model == FL_MODEL_CNN_CIFAR) { d.cin = 3; d.H0 = 32; d.W0 = 32; d.HID = 512; d.NCLS = 10; }
   else { d.cin = 1; d.H0 = 40; d.W0 = 98; d.HID = 256; d.NCLS = 35; }
-  d.cpad = 4; d.C1 = 32; d.C2 = 64;
+  // pixels padded to 4 channels (one 16-byte TMA/UMMA column) for the CIFAR tensor-core path;
+  // the 1-channel speech input stays unpadded (its FP32 conv1 would do 4x the work otherwise)
+  d.cpad = model == FL_MODEL_CNN_CIFAR ? 4 : 1; d.C1 = 32; d.C2 = 64;
   d.H1 = d.H0 / 2; d.W1 = d.W0 / 2; d.H2 = d.H1 / 2; d.W2 = d.W1 / 2;
   d.F = d.C2 * d.H2 * d.W2;
   L->D_in = d.cin * d.H0 * d.W0;
@@ -682,7 +684,9 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   // device capacity (grow-only; allocation happens on the first round of a given size)
   CK(grow_dev(c->d_slots, c->slots_cap, std::max<int64_t>(K, 1) * L.P_pad));
   CK(grow_dev(c->d_xpack, c->xpack_cap, std::max<int64_t>(R, 1) * L.D_pack));
-  if (L.model == FL_MODEL_CNN_CIFAR || L.model == FL_MODEL_CNN_SPEECH)
+  // shifted planar copies of the input exist only for the tensor-core conv1 dW
+  const bool want_planar = L.model == FL_MODEL_CNN_CIFAR && c->cfg.math == 0 && conv1_tc_supported(L);
+  if (want_planar)
     CK(grow_dev(c->cb.xplanar, c->cb.xplanar_cap, (c->xpack_cap / L.D_pack) * 16 * L.d.H0 * (L.d.W0 + 4)));
   CK(grow_dev(c->d_ypack, c->ypack_cap, R));
   CK(grow_dev(c->d_src_row, c->src_cap, R));
@@ -820,7 +824,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       if (nq > 0) {
         if (cnn)
           launches += pack_cnn(L, c->d_stage + q0 * L.D_in, nullptr, nq, c->d_xpack + q0 * L.D_pack,
-                               c->cb.xplanar + q0 * 16 * L.d.H0 * (L.d.W0 + 4), ps);
+                               want_planar ? c->cb.xplanar + q0 * 16 * L.d.H0 * (L.d.W0 + 4) : nullptr, ps);
         else
           launches += gather_rows_f32(c->d_stage + q0 * L.D_in, nullptr, nq, L.D_pack, c->d_xpack + q0 * L.D_pack,
                                       ps);
@@ -848,7 +852,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
     // one chunk: everything waits for it; several: each group waits for its own rows (wave loop)
     if (NQ == 1) CK(cudaStreamWaitEvent(st, c->ev_chunk[0], 0));
   } else {
-    if (cnn) launches += pack_cnn(L, xsrc, srow, R, c->d_xpack, c->cb.xplanar, st);
+    if (cnn) launches += pack_cnn(L, xsrc, srow, R, c->d_xpack, want_planar ? c->cb.xplanar : nullptr, st);
     else launches += gather_rows_f32(xsrc, srow, R, L.D_pack, c->d_xpack, st);
     launches += gather_i32(ysrc, srow, R, c->d_ypack, st);
   }

@@ -132,13 +132,17 @@ int fedavg_finalize(const double* S, int64_t P, const float* theta_g, const doub
 // CHW fp32 -> HWC with channels padded to 4 (16-byte pixels).
 // ---------------------------------------------------------------------------------
 __global__ void k_pack_cnn(const float* __restrict__ x, const int64_t* __restrict__ src_row, int64_t rows, int cin,
-                           int HW, float* __restrict__ out, float* __restrict__ planar) {
+                           int HW, float* __restrict__ out, float* __restrict__ planar, int cpad) {
   const int64_t tot = rows * HW;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / HW;
     const int pix = (int)(e - r * HW);
     const int64_t s = src_row ? src_row[r] : r;
     const float* src = x + s * (int64_t)cin * HW + pix;
+    if (cpad == 1) {  // one channel, unpadded
+      out[e] = src[0];
+      continue;
+    }
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     v.x = src[0];
     if (cin > 1) v.y = src[HW];
@@ -180,7 +184,8 @@ int pack_cnn(const Layout& L, const float* x_src, const int64_t* src_row, int64_
              float* xplanar, cudaStream_t st) {
   if (rows <= 0) return 0;
   int HW = L.d.H0 * L.d.W0;
-  k_pack_cnn<<<grid_for(rows * HW, 256, 1 << 20), 256, 0, st>>>(x_src, src_row, rows, L.d.cin, HW, xpack, nullptr);
+  k_pack_cnn<<<grid_for(rows * HW, 256, 1 << 20), 256, 0, st>>>(x_src, src_row, rows, L.d.cin, HW, xpack, nullptr,
+                                                                  L.d.cpad);
   if (!xplanar) return 1;
   k_pack_shifted_planar<<<grid_for(rows * L.d.H0 * (L.d.W0 + 4), 256, 1 << 20), 256, 0, st>>>(
       xpack, rows, L.d.H0, L.d.W0, xplanar);
