@@ -16,61 +16,66 @@
 namespace flb {
 namespace {
 
-constexpr int TM = 64, TN = 64, TK = 16, NT = 256;
+constexpr int TK = 16, NT = 256;
 
 // C[m][n] = Σ_k A(z,m,k)·Bv(z,n,k) for problem z; op.store() consumes C.
-template <class Op>
+// BM x BN tile (32 or 64 each), 256 threads as 16 x 16, each thread a (BM/16) x (BN/16)
+// register block; narrow layers (N or M <= 32) get narrow tiles so no half-empty tile is
+// loaded and multiplied.  The k loop runs in ascending order with one fmaf per product for
+// every tile shape, so the shape never changes a result bit.
+template <class Op, int BM, int BN>
 __global__ void __launch_bounds__(NT) k_gemm(const Op op) {
+  constexpr int RM = BM / 16, RN = BN / 16;
   const int z = blockIdx.z;
   int M, N, kb, ke;
   if (!op.setup(z, M, N, kb, ke)) return;
-  const int m0 = blockIdx.x * TM, n0 = blockIdx.y * TN;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   if (m0 >= M || n0 >= N) return;
-  __shared__ float As[TK][TM + 4];
-  __shared__ float Bs[TK][TN + 4];
+  __shared__ float As[TK][BM + 4];
+  __shared__ float Bs[TK][BN + 4];
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-  float acc[4][4];
+  float acc[RM][RN];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < RM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < RN; ++j) acc[i][j] = 0.f;
   for (int k0 = kb; k0 < ke; k0 += TK) {
 #pragma unroll
-    for (int i = 0; i < (TM * TK) / NT; ++i) {
+    for (int i = 0; i < (BM * TK) / NT; ++i) {
       const int e = tid + i * NT;
       int mm, kk;
-      if (Op::kAK) { mm = e / TK; kk = e % TK; } else { mm = e % TM; kk = e / TM; }
+      if (Op::kAK) { mm = e / TK; kk = e % TK; } else { mm = e % BM; kk = e / BM; }
       const int m = m0 + mm, k = k0 + kk;
       As[kk][mm] = (m < M && k < ke) ? op.A(z, m, k) : 0.f;
     }
 #pragma unroll
-    for (int i = 0; i < (TN * TK) / NT; ++i) {
+    for (int i = 0; i < (BN * TK) / NT; ++i) {
       const int e = tid + i * NT;
       int nn, kk;
-      if (Op::kBK) { nn = e / TK; kk = e % TK; } else { nn = e % TN; kk = e / TN; }
+      if (Op::kBK) { nn = e / TK; kk = e % TK; } else { nn = e % BN; kk = e / BN; }
       const int n = n0 + nn, k = k0 + kk;
       Bs[kk][nn] = (n < N && k < ke) ? op.Bv(z, n, k) : 0.f;
     }
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < TK; ++kk) {
-      float a[4], b[4];
+      float a[RM], b[RN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+      for (int i = 0; i < RM; ++i) a[i] = As[kk][ty * RM + i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+      for (int j = 0; j < RN; ++j) b[j] = Bs[kk][tx * RN + j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < RN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < RM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+    for (int j = 0; j < RN; ++j) {
+      const int m = m0 + ty * RM + i, n = n0 + tx * RN + j;
       if (m < M && n < N) op.store(z, m, n, acc[i][j]);
     }
 }
@@ -548,8 +553,13 @@ __global__ void __launch_bounds__(512) k_head(const float* __restrict__ h, const
 
 template <class Op>
 void launch(const Op& op, int Mmax, int Nmax, int Z, cudaStream_t st) {
-  dim3 grid((Mmax + TM - 1) / TM, (Nmax + TN - 1) / TN, Z);
-  k_gemm<Op><<<grid, NT, 0, st>>>(op);
+  static const bool t64 = env_knob("FL_SIMT_TILE64", 0) != 0;  // 64 x 64 everywhere (bit-identical)
+  const bool nm = !t64 && Mmax <= 32, nn = !t64 && Nmax <= 32;
+  dim3 grid((Mmax + (nm ? 31 : 63)) / (nm ? 32 : 64), (Nmax + (nn ? 31 : 63)) / (nn ? 32 : 64), Z);
+  if (nm && nn) k_gemm<Op, 32, 32><<<grid, NT, 0, st>>>(op);
+  else if (nm) k_gemm<Op, 32, 64><<<grid, NT, 0, st>>>(op);
+  else if (nn) k_gemm<Op, 64, 32><<<grid, NT, 0, st>>>(op);
+  else k_gemm<Op, 64, 64><<<grid, NT, 0, st>>>(op);
 }
 
 }  // namespace
