@@ -202,6 +202,38 @@ struct FcFwd {
   }
 };
 
+// fc1 forward split over K (small waves: a client's F = 15,360-long dot products would
+// otherwise run on HID/64 blocks): z = client·S + chunk, partial sums to part[z][m][n].
+struct FcFwdPart {
+  static constexpr bool kAK = true, kBK = true;
+  const float* X;
+  const int32_t* bs;
+  int B, F, HID, S;
+  WSrc w;
+  int64_t o_w;
+  float* part;  // [A·S][B][HID]
+  __device__ bool setup(int z, int& M, int& N, int& kb, int& ke) const {
+    const int a = z / S, c = z - a * S, kc = (F + S - 1) / S;
+    M = bs[a]; N = HID; kb = c * kc; ke = min(F, kb + kc);
+    return M > 0 && kb < ke;
+  }
+  __device__ float A(int z, int m, int k) const { return X[((int64_t)(z / S) * B + m) * F + k]; }
+  __device__ float Bv(int z, int n, int k) const { return *w.at(z / S, o_w + (int64_t)n * F + k); }
+  __device__ void store(int z, int m, int n, float v) const { part[((int64_t)z * B + m) * HID + n] = v; }
+};
+// h = ReLU(Σ_chunks part + b1), chunks in fixed order.
+__global__ void k_fc_fwd_reduce(const float* __restrict__ part, const int32_t* __restrict__ bs, int B, int HID, int S,
+                                WSrc w, int64_t o_b, float* __restrict__ h) {
+  const int a = blockIdx.y, r = blockIdx.x;
+  if (r >= bs[a]) return;
+  for (int n = threadIdx.x; n < HID; n += blockDim.x) {
+    float v = 0.f;
+    for (int c = 0; c < S; ++c) v += part[(((int64_t)a * S + c) * B + r) * HID + n];
+    v += *w.at(a, o_b + n);
+    h[((int64_t)a * B + r) * HID + n] = v > 0.f ? v : 0.f;
+  }
+}
+
 // fc1 dX: dp2 = dh·W1. rows r, cols k (F), K = HID.
 struct FcDx {
   static constexpr bool kAK = true, kBK = false;
@@ -616,7 +648,16 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
       return -1;
     n += nl;
   } else {
-    launch(FcFwd{b.p2, wa.bs, B, d.F, d.HID, w, L.o_f1w, L.o_f1b, b.h}, B, d.HID, A, st), ++n;
+    // split K when the wave is small: about 4 waves of 64-wide blocks over the GPU
+    const int nb = (d.HID + 63) / 64;
+    int S = (int)std::min<int64_t>(16, std::max<int64_t>(1, (4 * 148 + (int64_t)A * nb - 1) / ((int64_t)A * nb)));
+    while (S > 1 && (int64_t)A * S * B * d.HID > b.fc1_part_floats) --S;
+    if (S > 1) {
+      launch(FcFwdPart{b.p2, wa.bs, B, d.F, d.HID, S, w, L.o_f1w, b.fc1_part}, B, d.HID, A * S, st), ++n;
+      k_fc_fwd_reduce<<<dim3(B, A), 256, 0, st>>>(b.fc1_part, wa.bs, B, d.HID, S, w, L.o_f1b, b.h), ++n;
+    } else {
+      launch(FcFwd{b.p2, wa.bs, B, d.F, d.HID, w, L.o_f1w, L.o_f1b, b.h}, B, d.HID, A, st), ++n;
+    }
   }
   pf.end(K_FC1_FWD, f_f1, wbytes + 4.0 * S * (d.F + d.HID), st);
   const size_t hsm = sizeof(float) * (size_t)(d.NCLS * d.HID + HR * d.NCLS + HR * d.HID);
