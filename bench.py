@@ -50,6 +50,13 @@ def workload(world: int, name: str | None):
                 f"McMahan CNN, E=1, B=32"), "weak"
 
 
+def run_config(wl, desc, cohort, sizes, world):
+    """The `config` object of both arms' JSON lines (identical for ours and --impl reference)."""
+    return {"workload": desc, "clients": int(len(cohort)), "samples": int(sizes.sum()), "B": wl.B, "E": wl.E,
+            "lr": wl.lr, "parallelism": f"clients x{world}",
+            "l2": "per-round working set >> 126 MB L2 (no flush needed)"}
+
+
 def pop_for(wl):
     """Sizes of the whole population, the cohort, and data for the cohort's clients only,
     re-indexed so the library's population = the cohort's clients (ids 0..K-1)."""
@@ -278,8 +285,7 @@ def run_reference(args, world, rank):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8d laws)",
-            "config": {"workload": desc, "clients": int(len(cohort)), "samples": int(sizes.sum()), "B": wl.B,
-                       "E": wl.E, "model": wl.model},
+            "config": run_config(wl, desc, cohort, sizes, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[-1]["cores"], "kind": "oracle",
                              "sample": vals[-1]["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -393,9 +399,7 @@ def main():
                 "precision_note": "tensor-core GEMM operands tf32, fp32 accumulate; fp32 master weights, SGD, "
                                   "softmax-CE; fp64 FedAvg accumulation",
                 "data": "synthetic (seeded, SURVEY §8d laws), device-resident",
-                "config": {"workload": desc, "clients": int(len(cohort)), "samples": int(sizes.sum()),
-                           "B": wl.B, "E": wl.E, "lr": wl.lr, "model": wl.model, "parallelism": f"clients x{world}",
-                           "l2": "per-round working set >> 126 MB L2 (no flush needed)"},
+                "config": run_config(wl, desc, cohort, sizes, world),
                 "round_stats": dict({k: st[k] for k in ["round_ms", "place_ms", "stage_ms", "train_ms", "agg_ms",
                                                         "allreduce_ms", "waves", "steps_local", "kernels"]},
                                     timedelta_ms=timedelta),
