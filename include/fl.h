@@ -143,7 +143,8 @@ fl_status fl_place_plan(int32_t policy, const int64_t* cohort_ids, int64_t n_coh
  * QR).  It is accepted if a >= 0 and it predicts > 0 over [min x, max x];
  * otherwise the fallback is the line a·x + d with a >= 0, else the mean.
  * coef_out[4] = (a, b, c, d); *kind_out = 0 Eq. 3, 1 line, 2 constant (nullable);
- * *mse_out = mean squared residual (nullable).  FL_ERR_INVALID if n < 4 or x < 1. */
+ * *mse_out = mean squared residual (nullable).  FL_ERR_INVALID if n < 4, any x < 1, or any
+ * x / y not finite. */
 fl_status fl_lb_fit(const double* x, const double* y, int64_t n, double* coef_out, int32_t* kind_out,
                     double* mse_out);
 

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cmath>
 #include <numeric>
 #include <vector>
 
@@ -173,7 +174,7 @@ int lb_fit(const double* x, const double* y, int64_t n, double* coef, double* ms
   if (n < 4 || !x || !y || !coef) return -1;
   double xmin = x[0], xmax = x[0], ymean = 0;
   for (int64_t i = 0; i < n; ++i) {
-    if (!(x[i] >= 1.0)) return -1;
+    if (!(x[i] >= 1.0) || !std::isfinite(x[i]) || !std::isfinite(y[i])) return -1;
     xmin = std::min(xmin, x[i]);
     xmax = std::max(xmax, x[i]);
     ymean += y[i];

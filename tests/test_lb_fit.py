@@ -147,6 +147,10 @@ def test_library_fit_matches_oracle():
         assert e1 == pytest.approx(e0, rel=1e-6, abs=1e-12)
     with pytest.raises(fl.FLError):
         fl.fl_lb_fit([1, 2, 3], [1, 2, 3])
+    with pytest.raises(fl.FLError):  # non-finite records are rejected, not fitted
+        fl.fl_lb_fit([1, 2, 3, 4], [1.0, np.nan, 3.0, 4.0])
+    with pytest.raises(fl.FLError):
+        fl.fl_lb_fit([1, 2, np.inf, 4], [1.0, 2.0, 3.0, 4.0])
 
 
 def test_library_lb_gpu_plan_bit_exact():
