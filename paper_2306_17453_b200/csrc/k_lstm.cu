@@ -767,7 +767,9 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
   int n = 0;
   static const bool g128 = env_knob("FL_LSTM_GEMM64", 0) == 0;
   auto gemm = [&](const GemmArgs& g) {
-    if (g128)
+    // small waves: 128x128 tiles would leave most SMs idle; the 64x64 kernel is bit-identical
+    const int64_t b128 = (int64_t)((g.N + G2_T - 1) / G2_T) * ((g.M + G2_T - 1) / G2_T) * A;
+    if (g128 && b128 >= 2 * 148)
       launch_pdl(wa.pdl, k_lstm_gemm128, dim3((g.N + G2_T - 1) / G2_T, (g.M + G2_T - 1) / G2_T, A), 256, 0, st, g);
     else
       launch_pdl(wa.pdl, k_lstm_gemm, dim3((g.N + 63) / 64, (g.M + 63) / 64, A), 256, 0, st, g);
