@@ -4,13 +4,13 @@ client-updates/s and FedAvg round time).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2|C3|...]
 
-Workload: N=1 -> BASELINE configs[1] (C2: 100 CIFAR-shaped
-clients, log-normal sizes 10..2000, McMahan CNN, E=1, B=32).  N>1 -> weak scaling: a
-cohort of 100·N clients drawn from a 10,000-client population with the same size law
-(C2's per-GPU load on every GPU, C3's population), one NCCL allreduce per round.
+Workload: at every N, BASELINE configs[2] = C3, the north-star round (1,000
+of 10,000 CIFAR-shaped clients, log-normal sizes 10..2000, McMahan CNN, E=2, B=32), placed
+across the N GPUs by the library (strong scaling; one NCCL allreduce of [S‖N] per round at
+N>1).  At N=1 the line also carries configs[1] (C2: 100 clients, E=1) as its `c2` object.
 A step = one whole round (place -> pack -> local SGD of every client -> fused FedAvg
 accumulation -> allreduce -> finalize), inputs resident in HBM.  The per-round working
-set (client models 100 x 8.6 MB + activations) exceeds the 126 MB L2, so no flush is
+set (client models K x 8.6 MB + activations) exceeds the 126 MB L2, so no flush is
 needed between steps.  For N>1 launch with torchrun (one process per GPU).
 """
 from __future__ import annotations
@@ -38,16 +38,19 @@ FLOPS_PER_SAMPLE_EPOCH = {"cnn": 101_087_232.0, "speech": 337_250_000.0, "logreg
 
 
 def workload(world: int, name: str | None):
-    if name:
-        wl = synth.preset(name)
-        if name == "C3":
-            return wl, "C3: 1,000 of 10,000 CIFAR-shaped clients, McMahan CNN, E=2, B=32 (strong scaling)", "strong"
-        return wl, f"{name}", "weak" if world == 1 else "strong"
-    if world == 1:
-        return synth.preset("C2"), "C2: 100 CIFAR-shaped clients, log-normal sizes 10-2000, McMahan CNN, E=1, B=32", "weak"
-    wl = synth.preset("C3", n_cohort=100 * world, E=1)
-    return wl, (f"C2-per-GPU weak scaling: {100 * world} of 10,000 CIFAR-shaped clients (C3 population), "
-                f"McMahan CNN, E=1, B=32"), "weak"
+    """(Workload, description, scaling).  Default at every N: BASELINE configs[2] = C3, the
+    north-star round (1,000 of 10,000 CIFAR-shaped clients, E = 2, B = 32) whose metric is
+    quoted at 1/2/4/8 GPUs -- strong scaling: the same round on N GPUs, so the driver's
+    per-N values form one curve.  configs[1] (C2, the single-GPU config) is measured beside
+    it at N = 1 (the `c2` object of the line) and with --config C2."""
+    name = name or "C3"
+    wl = synth.preset(name)
+    desc = {"C1": "C1: 10 logreg clients, 784-dim, sizes 5-50, E=1, B=5",
+            "C2": "C2: 100 CIFAR-shaped clients, log-normal sizes 10-2000, McMahan CNN, E=1, B=32",
+            "C3": "C3: 1,000 of 10,000 CIFAR-shaped clients, log-normal sizes 10-2000, McMahan CNN, E=2, B=32",
+            "C4": "C4: 2,000 speech-shaped clients (1x40x98), log-normal sizes 5-5000, conv+MLP, E=1, B=20",
+            "C5": "C5: 700 Shakespeare-shaped clients, log-normal sizes 4-4000, char-LSTM, E=1, B=4"}[name]
+    return wl, desc, ("strong" if world > 1 else "weak")
 
 
 def run_config(wl, desc, cohort, sizes, world):
@@ -193,7 +196,7 @@ def roofline(kstats, math, total_ms):
     out["kernel"] = name
     out["share_of_round"] = k["ms"] / total_ms if total_ms else None
     out["launches_per_round"] = k["launches"]
-    out["traffic"] = ncu_traffic(name)
+    out["traffic"], out["traffic_source"] = ncu_traffic(name)
     return out
 
 
@@ -208,37 +211,61 @@ def kernel_table(kstats, math):
 
 
 def ncu_traffic(kernel_class):
-    """dram bytes per launch of this class from the committed ncu --set full summary, if any."""
+    """DRAM bytes per launch of this class (dram__bytes_read.sum + dram__bytes_write.sum) from the
+    committed ncu --set full capture of that kernel (profiles/ncu_traffic.json records which
+    capture); None if the class was not captured."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        return json.load(open(p)).get(kernel_class)
+        d = json.load(open(p))
     except Exception:
-        return None
+        return None, None
+    v = d.get(kernel_class)
+    return v, (d.get("_source") if v is not None else None)
 
 
-def cpu_baseline(wl, sizes, x, y, theta, budget_samples, threads=0):
-    """The oracle, as it stands, on a bounded random sample of the workload's clients:
-    samples/s of local SGD, converted to client-updates/s with the workload's mean
-    client size (aggregation cost is negligible next to training on the CPU)."""
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(wl, sizes, x, y, theta, budget_samples, threads=0, seed=1):
+    """The oracle, as it stands, on a bounded random sample of the workload's clients.
+
+    The sample holds at least 2 clients per host thread (so every thread has work; the oracle
+    runs one OpenMP task per client) and ~budget_samples samples, issued largest-first.
+    client-updates/s = (sample samples/s) / (mean client samples per round); `cores` = the
+    threads that actually had a client.  A second, single-thread timing of the first client
+    is reported as `single_thread`."""
     import oracle
-    rng = np.random.default_rng(1)
+    threads = threads or cpu_threads()
+    rng = np.random.default_rng(seed)
     order = rng.permutation(len(sizes))
     pick, tot = [], 0
     for c in order:
-        if tot >= budget_samples:
+        if tot >= budget_samples and len(pick) >= 2 * threads:
             break
         pick.append(int(c))
         tot += int(sizes[c])
+    pick = sorted(pick, key=lambda c: -int(sizes[c]))
     pop_off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    mean_client = float(np.mean(sizes)) * wl.E
     t0 = time.perf_counter()
     _, used = oracle.train_clients(wl.model, theta, x, y, pop_off, np.array(pick), wl.B, wl.E, wl.lr, threads=threads)
     dt = time.perf_counter() - t0
-    samples_per_s = tot * wl.E / dt
-    mean_client = float(np.mean(sizes)) * wl.E
-    return {"value": samples_per_s / mean_client, "unit": UNIT, "cores": int(used), "kind": "oracle",
-            "sample": f"{len(pick)} random clients of the cohort ({tot} samples x E={wl.E}) trained by the fp64 "
-                      f"oracle in {dt:.1f} s; client-updates/s = samples/s / mean client size ({mean_client:.1f})",
-            "seconds": dt}
+    value = tot * wl.E / dt / mean_client
+    small = min(pick, key=lambda c: int(sizes[c]))
+    t1 = time.perf_counter()
+    oracle.train_clients(wl.model, theta, x, y, pop_off, np.array([small]), wl.B, wl.E, wl.lr, threads=1)
+    dt1 = time.perf_counter() - t1
+    return {"value": value, "unit": UNIT, "cores": int(min(used, len(pick))), "kind": "oracle",
+            "sample": f"{len(pick)} random clients of the cohort ({tot} samples x E={wl.E}), largest first, trained "
+                      f"by the fp64 oracle on {min(used, len(pick))} host threads in {dt:.1f} s; client-updates/s = "
+                      f"samples/s / mean client samples per round ({mean_client:.1f})",
+            "seconds": dt, "host_threads": int(threads),
+            "single_thread": {"value": int(sizes[small]) * wl.E / dt1 / mean_client, "unit": UNIT, "cores": 1,
+                              "sample": f"1 client ({int(sizes[small])} samples x E={wl.E}) in {dt1:.2f} s"}}
 
 
 def dist_setup():
@@ -262,14 +289,28 @@ def allmax(v, world):
     return float(t.item())
 
 
+def allmax_list(vs, world):
+    if world == 1:
+        return list(vs)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v) for v in vs], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
 
 
+def pct(v, q):
+    return float(np.percentile(np.asarray(v, dtype=np.float64), q))
+
+
 def run_reference(args, world, rank):
-    """The oracle (the only reference this tier has) on the host cores."""
+    """The oracle (the only reference this tier has) on the host cores; rank 0 only."""
     if rank != 0:
         return
     wl, desc, scaling = workload(args.gpus, args.config)
@@ -277,7 +318,7 @@ def run_reference(args, world, rank):
     theta = synth.init_params(wl.model)
     vals = []
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(wl, sizes, x, y, theta, budget_samples=args.ref_samples)
+        cb = cpu_baseline(wl, sizes, x, y, theta, budget_samples=args.ref_samples, seed=1 + i)
         if i >= args.warmup:
             vals.append(cb)
     v = statistics.median(c["value"] for c in vals)
@@ -287,10 +328,36 @@ def run_reference(args, world, rank):
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8d laws)",
             "config": run_config(wl, desc, cohort, sizes, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[-1]["cores"], "kind": "oracle",
-                             "sample": vals[-1]["sample"]},
+                             "sample": vals[-1]["sample"] + f"; median of {args.steps} such samples"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "gpu_launches": 0}
+            "gpu_launches": 0,
+            "note": "each step trains a bounded random sample of the cohort's clients on the host cores and "
+                    "converts samples/s to client-updates/s; ms_per_step is the implied whole-round time"}
     print(json.dumps(line), flush=True)
+
+
+def timed_rounds(ctx, cohort, steps, rnd, world, stream, clk=None):
+    """K rounds queued back to back on the ctx stream, bracketed by barrier + synchronize;
+    one CUDA event between consecutive rounds gives the per-round device times.  Returns
+    (total ms max over ranks, per-round ms max over ranks, next round index)."""
+    import torch
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    barrier(world)
+    torch.cuda.synchronize()
+    if clk:
+        clk.mark_start()
+    evs[0].record(stream)
+    for i in range(steps):
+        ctx.fl_round(cohort, round_index=rnd, stats=False)
+        rnd += 1
+        evs[i + 1].record(stream)
+    torch.cuda.synchronize()
+    if clk:
+        clk.mark_end()
+    barrier(world)
+    per = allmax_list([evs[i].elapsed_time(evs[i + 1]) for i in range(steps)], world)
+    total = allmax(evs[0].elapsed_time(evs[-1]), world)
+    return total, per, rnd
 
 
 def main():
@@ -299,10 +366,11 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=None)
+    ap.add_argument("--config", default=None, help="C1..C5 (default C3, BASELINE configs[2])")
     ap.add_argument("--math", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c2", action="store_true", help="skip the configs[1] (C2) measurement at N = 1")
     ap.add_argument("--cpu-samples", type=int, default=400)
     ap.add_argument("--ref-samples", type=int, default=200)
     args = ap.parse_args()
@@ -335,48 +403,34 @@ def main():
         ctx.fl_round(cohort, round_index=rnd, stats=False)
         rnd += 1
     torch.cuda.synchronize()
-    barrier(world)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(list(range(world)) if rank == 0 else [local]) as clk:
-        barrier(world)
-        torch.cuda.synchronize()
-        clk.mark_start()
-        e0.record(stream)
-        for _ in range(args.steps):
-            ctx.fl_round(cohort, round_index=rnd, stats=False)
-            rnd += 1
-        e1.record(stream)
-        torch.cuda.synchronize()
-        clk.mark_end()
-        barrier(world)
-    ms_total = allmax(e0.elapsed_time(e1), world)
-    st = ctx.fl_get_stats()
-    # "timedelta workers": slowest minus fastest rank's training time of the last round
-    timedelta = allmax(st["train_ms"], world) + allmax(-st["train_ms"], world)
+        ms_total, per_step, rnd = timed_rounds(ctx, cohort, args.steps, rnd, world, stream, clk)
+    clocks = clk.summary()
+    # one more round with stats: max-over-ranks round time and "timedelta workers"
+    st = ctx.fl_round(cohort, round_index=rnd)
+    rnd += 1
     ms_step = ms_total / args.steps
     value = len(cohort) * args.steps / (ms_total * 1e-3)
-    clocks = clk.summary()
-    # per-kernel device time of one extra (profiled) round, for the roofline
+    # per-kernel device time of one extra (profiled, serialised) round, for the roofline
     ctx.fl_set_profiling(True)
     st_p = ctx.fl_round(cohort, round_index=rnd)
     rnd += 1
     kstats = ctx.fl_get_kernel_stats()
     ctx.fl_set_profiling(False)
     roof = roofline(kstats, args.math, st_p["round_ms"])
-    ctx.close()  # the e2e context below needs the memory (C4: ~60 GB of activations per context)
+    ctx.close()
     del xd, yd
     torch.cuda.empty_cache()
     # e2e: the public API with HOST buffers; H2D of this rank's cohort rows and D2H of θ_new per step
     e2e = None
     if not args.no_e2e:
-        ctx2 = fl.fl_round_init(cfg if world == 1 else cfg, sizes, x, y, theta, on_device=False)
+        ctx2 = fl.fl_round_init(cfg, sizes, x, y, theta, on_device=False)
         for _ in range(2):
             ctx2.fl_place(cohort)
             ctx2.fl_train_clients(0)
             ctx2.fl_aggregate(want_params=True)
         barrier(world)
         t0 = time.perf_counter()
-        h2d = 0
         for i in range(args.steps):
             ctx2.fl_place(cohort)
             ctx2.fl_train_clients(i)
@@ -387,6 +441,27 @@ def main():
                "h2d_bytes_per_step": int(s2["h2d_bytes"]), "d2h_bytes_per_step": int(4 * ctx2.P),
                "ms_per_step": t_e2e / args.steps, "timer": "host wall clock around the public API calls"}
         ctx2.close()
+    # configs[1] (C2, 100 clients, single GPU) beside the C3 line at N = 1
+    c2 = None
+    if world == 1 and args.config is None and not args.no_c2:
+        wl2 = synth.preset("C2")
+        s2z, x2, y2, co2 = pop_for(wl2)
+        th2 = synth.init_params("cnn")
+        cfg2 = fl.Config(model="cnn", batch_size=wl2.B, local_epochs=wl2.E, lr=wl2.lr, device=local, math=args.math)
+        x2d, y2d = torch.from_numpy(x2).cuda(), torch.from_numpy(y2).cuda()
+        ctx3 = fl.fl_round_init(cfg2, s2z, x2d, y2d, th2)
+        r2 = 0
+        for _ in range(args.warmup):
+            ctx3.fl_round(co2, round_index=r2, stats=False)
+            r2 += 1
+        tot2, per2, r2 = timed_rounds(ctx3, co2, max(args.steps, 10), r2, 1, torch.cuda.ExternalStream(ctx3.stream))
+        k2 = max(args.steps, 10)
+        c2 = {"workload": "C2 (BASELINE configs[1]): 100 CIFAR-shaped clients, log-normal sizes 10-2000, E=1, B=32",
+              "value": len(co2) * k2 / (tot2 * 1e-3), "unit": UNIT, "ms_per_step": tot2 / k2,
+              "step_ms": {"median": statistics.median(per2), "p10": pct(per2, 10), "p90": pct(per2, 90)},
+              "steps": k2}
+        ctx3.close()
+        del x2d, y2d
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(wl, sizes, x, y, theta, args.cpu_samples)
@@ -394,17 +469,20 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None,
-                # speech and LSTM run FP32 SIMT kernels; CNN/logreg GEMMs TF32
-                "dtype": "f32" if (args.math == 1 or wl.model in ("lstm", "speech")) else "tf32",
+                "step_ms": {"median": statistics.median(per_step), "p10": pct(per_step, 10),
+                            "p90": pct(per_step, 90), "max_over_ranks": True},
+                # speech and LSTM run FP32 SIMT kernels; CNN GEMMs TF32
+                "dtype": "f32" if (args.math == 1 or wl.model in ("lstm", "speech", "logreg")) else "tf32",
                 "precision_note": "tensor-core GEMM operands tf32, fp32 accumulate; fp32 master weights, SGD, "
                                   "softmax-CE; fp64 FedAvg accumulation",
                 "data": "synthetic (seeded, SURVEY §8d laws), device-resident",
                 "config": run_config(wl, desc, cohort, sizes, world),
-                "round_stats": dict({k: st[k] for k in ["round_ms", "place_ms", "stage_ms", "train_ms", "agg_ms",
-                                                        "allreduce_ms", "waves", "steps_local", "kernels"]},
-                                    timedelta_ms=timedelta),
+                "round_stats": {k: st[k] for k in ["round_ms", "round_ms_max", "place_ms", "stage_ms", "train_ms",
+                                                   "train_end_ms_min", "train_end_ms_max", "timedelta_ms",
+                                                   "agg_ms", "allreduce_ms", "waves", "steps_local",
+                                                   "clients_local", "kernels"]},
                 "kernels": kernel_table(kstats, args.math),
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "c2": c2,
                 "gpu_launches": int(st["kernels"]) * args.steps}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define FL_ABI_VERSION 1u
+#define FL_ABI_VERSION 2u
 
 typedef enum {
   FL_OK = 0,
@@ -80,7 +80,10 @@ typedef struct {
   int64_t min_samples;      /* clients with n < min_samples are rejected (P:447 exclusion, reading A6); >= 1 */
   int32_t rank, world_size; /* one process per GPU; 0 <= rank < world_size */
   int32_t device;           /* CUDA ordinal of this rank */
-  const uint8_t* nccl_unique_id; /* 128 bytes from fl_nccl_unique_id() on rank 0; NULL iff world_size == 1 */
+  const uint8_t* nccl_unique_id; /* 128 bytes from fl_nccl_unique_id() on rank 0; required if world_size > 1.
+                                    With world_size == 1 a non-NULL id creates a 1-rank communicator and
+                                    fl_aggregate takes the multi-rank path (partial [S‖N] -> ncclAllReduce ->
+                                    finalize) on one GPU; NULL: the fused single-GPU accumulate+finalize. */
   int32_t math;             /* 0: tensor cores (TF32, tcgen05) where built; 1: FP32 SIMT everywhere */
   void* stream;             /* optional borrowed cudaStream_t; NULL: the ctx creates its own */
 } fl_config;
@@ -108,14 +111,19 @@ typedef struct {
   double stage_ms;      /* cohort gather / host->device staging */
   double train_ms;      /* local SGD of this rank's clients (device) */
   double agg_ms;        /* fused per-GPU accumulation + (NCCL reduce) + finalize */
-  double allreduce_ms;  /* NCCL part of agg_ms (0 when world_size == 1) */
-  double client_updates_per_s; /* clients_total / round_ms (this rank's clock) */
+  double allreduce_ms;  /* NCCL part of agg_ms (0 without a communicator) */
+  double client_updates_per_s; /* clients_total / round_ms_max */
   int64_t clients_total, clients_local;
   int64_t samples_total, samples_local;
   int64_t steps_local;  /* Σ E·m over this rank's clients */
   int64_t waves;        /* max E·m over this rank's clients (critical path in SGD steps) */
   int64_t h2d_bytes;    /* host->device bytes copied this round */
   int64_t kernels;      /* kernel launches this round */
+  double train_end_ms;  /* fl_round entry to the end of this rank's local SGD (device) */
+  /* Over ranks (all-gathered through the communicator; equal to this rank's values without one): */
+  double round_ms_max;  /* the round time: max over ranks of round_ms */
+  double train_end_ms_min, train_end_ms_max;
+  double timedelta_ms;  /* "timedelta workers": train_end_ms_max − train_end_ms_min */
 } fl_round_stats;
 
 uint32_t fl_abi_version(void);
@@ -180,7 +188,9 @@ fl_status fl_aggregate(fl_ctx* ctx, float* out_params, int64_t* out_total_sample
 
 /* fl_place + fl_train_clients + fl_aggregate, timed; stats nullable.  Asynchronous
  * with respect to the host except for the stats event reads (it synchronises the
- * ctx stream when stats != NULL). */
+ * ctx stream when stats != NULL).  With a communicator, stats != NULL makes the call
+ * gather every rank's times (round_ms_max, timedelta_ms): all ranks must then pass
+ * stats != NULL for that round. */
 fl_status fl_round(fl_ctx* ctx, const int64_t* cohort_ids, int64_t n_cohort, int32_t policy,
                    const double* lb_coef, int32_t round_index, fl_round_stats* stats);
 
@@ -214,7 +224,8 @@ fl_status fl_set_global_params(fl_ctx* ctx, const float* params);
 fl_status fl_set_timing_records(fl_ctx* ctx, int32_t on);
 fl_status fl_get_client_times(fl_ctx* ctx, int64_t* ids, int64_t* m, double* t_ms, int64_t* n_local);
 
-/* Stats of the last fl_round. */
+/* Stats of the last fl_round.  With a communicator this is a collective call (the
+ * over-ranks fields are all-gathered): every rank must call it. */
 fl_status fl_get_stats(fl_ctx* ctx, fl_round_stats* out);
 
 /* Per-kernel-class device time of the last round, for roofline reports.  Off by default:

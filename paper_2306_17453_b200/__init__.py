@@ -24,7 +24,7 @@ STATUS = {0: "FL_OK", 1: "FL_ERR_INVALID", 2: "FL_ERR_STATE", 3: "FL_ERR_OOM", 4
           6: "FL_ERR_EMPTY", 7: "FL_ERR_UNSUPPORTED"}
 MODEL = {"logreg": 0, "cnn": 1, "speech": 2, "lstm": 3}
 POLICY = {"bu": 0, "lb": 1, "rr": 2, "srr": 3, "lb_gpu": 4}
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # Symbols include/fl.h declares (checked by tests/test_abi.py).
 EXPORTS = ["fl_abi_version", "fl_n_params", "fl_place_plan", "fl_pack_plan", "fl_nccl_unique_id", "fl_round_init",
@@ -57,7 +57,9 @@ class fl_round_stats(C.Structure):
                 ("train_ms", C.c_double), ("agg_ms", C.c_double), ("allreduce_ms", C.c_double),
                 ("client_updates_per_s", C.c_double), ("clients_total", C.c_int64), ("clients_local", C.c_int64),
                 ("samples_total", C.c_int64), ("samples_local", C.c_int64), ("steps_local", C.c_int64),
-                ("waves", C.c_int64), ("h2d_bytes", C.c_int64), ("kernels", C.c_int64)]
+                ("waves", C.c_int64), ("h2d_bytes", C.c_int64), ("kernels", C.c_int64),
+                ("train_end_ms", C.c_double), ("round_ms_max", C.c_double), ("train_end_ms_min", C.c_double),
+                ("train_end_ms_max", C.c_double), ("timedelta_ms", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -138,6 +138,9 @@ struct Nccl {
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*getVersion)(int*) = nullptr;
   const char* (*errStr)(ncclResult_t) = nullptr;
   bool load() {
     if (h) return true;
@@ -152,7 +155,10 @@ struct Nccl {
     allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
     commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
     errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
-    return getUniqueId && commInitRank && allReduce && commDestroy;
+    allGather = (decltype(allGather))dlsym(h, "ncclAllGather");
+    commCount = (decltype(commCount))dlsym(h, "ncclCommCount");
+    getVersion = (decltype(getVersion))dlsym(h, "ncclGetVersion");
+    return getUniqueId && commInitRank && allReduce && commDestroy && allGather;
   }
 };
 Nccl g_nccl;
@@ -192,6 +198,7 @@ struct fl_ctx {
   bool have_plan = false, trained = false, failed = false;
   std::vector<int64_t> plan_ids, plan_off, local_ids;  // local_ids in plan order
   std::vector<int64_t> exec;                           // exec position -> index into local_ids
+  std::vector<int64_t> exec_ids;                       // client id of exec position e (last trained round)
   std::vector<int64_t> steps_exec, n_exec, pseg;
   int64_t N_total = 0, N_local = 0, K_total = 0;
 
@@ -218,15 +225,20 @@ struct fl_ctx {
   LstmBufs lb;
   int64_t cb_slots_cap = 0, cb_part_cap = 0;
 
-  // pinned host staging of the per-round tables
-  char* h_tab = nullptr;
-  size_t h_tab_cap = 0;
-  double* h_N = nullptr;
+  // pinned host staging of the per-round tables: a ring of two buffers, so issuing round r
+  // waits (ev_tab[r % 2]) only for the table copies of round r - 2
+  char* h_tab[2] = {nullptr, nullptr};
+  size_t h_tab_cap[2] = {0, 0};
+  bool tab_pending[2] = {false, false};
+  cudaEvent_t ev_tab[2] = {nullptr, nullptr};
+  int tab_i = 0;
+  double tab_wait_ms = 0.0;
+  // per-rank [round_ms, train_end_ms] gathered over the communicator for the round stats
+  double* h_rstat = nullptr;  // pinned [2·world]
+  double* d_rstat = nullptr;  // device [2 + 2·world]
 
   cudaEvent_t ev_entry = nullptr, ev_start = nullptr, ev_staged = nullptr, ev_trained = nullptr,
-              ev_agg0 = nullptr, ev_acc1 = nullptr, ev_ar0 = nullptr, ev_ar1 = nullptr, ev_end = nullptr,
-              ev_tab = nullptr;
-  bool tab_pending = false;
+              ev_agg0 = nullptr, ev_acc1 = nullptr, ev_ar0 = nullptr, ev_ar1 = nullptr, ev_end = nullptr;
   double place_ms = 0.0;
   int64_t kernels = 0, h2d = 0, train_launches = 0;
   fl_round_stats stats{};
@@ -360,10 +372,12 @@ void fl_round_destroy(fl_ctx* c) {
                   c->lb.dX, c->lb.E, c->lb.dE, c->lb.dhT};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  if (c->h_tab) cudaFreeHost(c->h_tab);
-  if (c->h_N) cudaFreeHost(c->h_N);
+  for (int i = 0; i < 2; ++i)
+    if (c->h_tab[i]) cudaFreeHost(c->h_tab[i]);
+  if (c->h_rstat) cudaFreeHost(c->h_rstat);
+  if (c->d_rstat) cudaFree(c->d_rstat);
   cudaEvent_t evs[] = {c->ev_entry, c->ev_start, c->ev_staged, c->ev_trained, c->ev_agg0,
-                       c->ev_acc1, c->ev_ar0, c->ev_ar1, c->ev_end, c->ev_tab};
+                       c->ev_acc1, c->ev_ar0, c->ev_ar1, c->ev_end, c->ev_tab[0], c->ev_tab[1]};
   for (cudaEvent_t e : evs)
     if (e) cudaEventDestroy(e);
   if (c->host_registered) cudaHostUnregister((void*)c->x);
@@ -391,7 +405,7 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   if (cfg->abi_version != FL_ABI_VERSION) return FL_ERR_INVALID;
   if (cfg->batch_size < 1 || cfg->local_epochs < 1 || !(cfg->lr >= 0.f) || cfg->min_samples < 1) return FL_ERR_INVALID;
   if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) return FL_ERR_INVALID;
-  if (cfg->world_size > 1 && !cfg->nccl_unique_id) return FL_ERR_INVALID;
+  if (cfg->world_size > 1 && !cfg->nccl_unique_id) return FL_ERR_INVALID;  // world 1 + id: 1-rank comm
   if (fl_n_params(cfg->model) == 0) return FL_ERR_INVALID;
   if (n_params != fl_n_params(cfg->model)) return FL_ERR_INVALID;
   if (!model_supported(cfg->model)) return FL_ERR_UNSUPPORTED;
@@ -434,7 +448,7 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
     c->own_stream = true;
   }
   cudaEvent_t* evs[] = {&c->ev_entry, &c->ev_start, &c->ev_staged, &c->ev_trained, &c->ev_agg0,
-                        &c->ev_acc1, &c->ev_ar0, &c->ev_ar1, &c->ev_end, &c->ev_tab};
+                        &c->ev_acc1, &c->ev_ar0, &c->ev_ar1, &c->ev_end, &c->ev_tab[0], &c->ev_tab[1]};
   for (cudaEvent_t* e : evs) CK(cudaEventCreate(e));
   if (const char* ng = getenv("FL_GROUPS")) c->ngroups = std::max(1, atoi(ng));
   if (const char* ns = getenv("FL_SOLO")) c->nsolo = std::max(0, atoi(ns));
@@ -466,19 +480,29 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   CK(cudaMalloc(&c->d_canon_of, sizeof(int64_t) * Pp));
   CK(cudaMalloc(&c->d_canon, sizeof(float) * P));
   CK(cudaMalloc(&c->d_S, sizeof(double) * (Pp + 1)));
-  CK(cudaMallocHost(&c->h_N, sizeof(double)));
+  CK(cudaMallocHost(&c->h_rstat, sizeof(double) * 2 * cfg->world_size));
+  CK(cudaMalloc(&c->d_rstat, sizeof(double) * (2 + 2 * cfg->world_size)));
   CK(cudaMemcpyAsync(c->d_canon_of, c->L.canon_of.data(), sizeof(int64_t) * Pp, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(c->d_canon, global_params, sizeof(float) * P, cudaMemcpyHostToDevice, c->st));
   canon_to_internal(c->d_canon, c->d_canon_of, Pp, c->d_theta, c->st);
   CKL();
   CK(cudaStreamSynchronize(c->st));
-  if (cfg->world_size > 1) {
+  // a communicator whenever a unique id is given: world_size > 1, or world_size == 1 to run
+  // the multi-rank aggregation path (partial -> allreduce -> finalize) on one GPU
+  if (cfg->nccl_unique_id) {
     if (!g_nccl.load()) return set_err(c, FL_ERR_NCCL, "cannot dlopen libnccl.so.2");
     ncclUniqueId id;
     memcpy(id.internal, cfg->nccl_unique_id, 128);
     ncclResult_t r = g_nccl.commInitRank(&c->comm, cfg->world_size, id, cfg->rank);
     if (r != ncclSuccess)
       return set_err(c, FL_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.errStr ? g_nccl.errStr(r) : "?");
+    int nranks = -1, ver = 0;
+    if (g_nccl.commCount) g_nccl.commCount(c->comm, &nranks);
+    if (g_nccl.getVersion) g_nccl.getVersion(&ver);
+    fprintf(stderr, "[fl] NCCL %d comm ready: rank %d of %d (comm nranks %d) on device %d (%s)\n", ver,
+            cfg->rank, cfg->world_size, nranks, cfg->device, prop.name);
+    if (nranks != cfg->world_size)
+      return set_err(c, FL_ERR_NCCL, "communicator has %d ranks, expected %d", nranks, cfg->world_size);
   }
   return FL_OK;
 }
@@ -508,6 +532,7 @@ fl_status fl_place(fl_ctx* c, const int64_t* cohort_ids, int64_t n_cohort, int32
   for (int64_t i = 0; i < n_cohort; ++i) c->N_total += c->n_samples[(size_t)cohort_ids[i]];
   c->have_plan = true;
   c->trained = false;
+  c->rec_valid = false;  // records describe the previous plan's clients
   if (out_ids) std::copy(c->plan_ids.begin(), c->plan_ids.end(), out_ids);
   if (out_off) std::copy(c->plan_off.begin(), c->plan_off.end(), out_off);
   c->place_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -544,6 +569,8 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       for (int64_t e = NS + r; e < K; e += NR) ex2.push_back(c->exec[(size_t)e]), ++gsize[(size_t)(NS + r)];
     c->exec.swap(ex2);
   }
+  c->exec_ids.resize((size_t)K);
+  for (int64_t e = 0; e < K; ++e) c->exec_ids[(size_t)e] = c->local_ids[(size_t)c->exec[(size_t)e]];
   c->steps_exec.resize((size_t)K);
   c->n_exec.resize((size_t)K);
   c->pseg.assign((size_t)K + 1, 0);
@@ -623,17 +650,22 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   // pinned table layout: src_row[R] i64 | n[K] i64 | slot_off[W+1] i64 | sidx i32 | bs i32 | steps[K] i32
   size_t need = sizeof(int64_t) * (size_t)(R + K + ws.n_waves + 1) +
                 sizeof(int32_t) * (size_t)(n_sidx + n_bs + K + n_bs + ws.n_waves) + 64;
-  if (c->tab_pending) {
-    CK(cudaEventSynchronize(c->ev_tab));
-    c->tab_pending = false;
+  const int ti = c->tab_i;
+  c->tab_i ^= 1;
+  c->tab_wait_ms = 0.0;
+  if (c->tab_pending[ti]) {  // round r - 2's table copies (normally long done): not placement time
+    auto w0 = std::chrono::steady_clock::now();
+    CK(cudaEventSynchronize(c->ev_tab[ti]));
+    c->tab_pending[ti] = false;
+    c->tab_wait_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
   }
-  if (need > c->h_tab_cap) {
-    if (c->h_tab) cudaFreeHost(c->h_tab);
-    c->h_tab = nullptr;
-    CK(cudaMallocHost(&c->h_tab, need * 2));
-    c->h_tab_cap = need * 2;
+  if (need > c->h_tab_cap[ti]) {
+    if (c->h_tab[ti]) cudaFreeHost(c->h_tab[ti]);
+    c->h_tab[ti] = nullptr;
+    CK(cudaMallocHost(&c->h_tab[ti], need * 2));
+    c->h_tab_cap[ti] = need * 2;
   }
-  int64_t* h_src = (int64_t*)c->h_tab;
+  int64_t* h_src = (int64_t*)c->h_tab[ti];
   int64_t* h_n = h_src + R;
   int64_t* h_soff = h_n + K;
   int32_t* h_sidx = (int32_t*)(h_soff + ws.n_waves + 1);
@@ -769,7 +801,8 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
     }
     if (!b.c1wt_g) CK(cudaMalloc(&b.c1wt_g, sizeof(float) * C1WT_FLOATS));
   }
-  c->place_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  c->place_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() -
+                 c->tab_wait_ms;
 
   // ---- device work, stream-ordered
   cudaStream_t st = c->st;
@@ -783,8 +816,8 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   CK(cudaMemcpyAsync(ws.d_bs, h_bs, sizeof(int32_t) * n_bs, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(c->d_steps, h_steps, sizeof(int32_t) * K, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(ws.d_bpre, h_bpre, sizeof(int32_t) * (n_bs + ws.n_waves), cudaMemcpyHostToDevice, st));
-  CK(cudaEventRecord(c->ev_tab, st));
-  c->tab_pending = true;
+  CK(cudaEventRecord(c->ev_tab[ti], st));
+  c->tab_pending[ti] = true;
   h2d += (int64_t)(sizeof(int64_t) * (R + K + ws.n_waves + 1) + sizeof(int32_t) * (n_sidx + 2 * n_bs + K + ws.n_waves));
   // stage the cohort's samples: device population -> gather; host population -> H2D copies,
   // chunk by chunk on the copy stream (the previous round has released xpack once st reaches
@@ -989,8 +1022,8 @@ fl_status fl_aggregate(fl_ctx* c, float* out_params, int64_t* out_total_samples)
   CK(cudaEventRecord(c->ev_agg0, st));
   int64_t n = 0;
   c->prof.begin(st);
-  const double agg_bytes = 4.0 * (double)Pp * (double)(K + 1) + (c->cfg.world_size == 1 ? 4.0 : 8.0) * (double)Pp;
-  if (c->cfg.world_size == 1) {
+  const double agg_bytes = 4.0 * (double)Pp * (double)(K + 1) + (c->comm ? 8.0 : 4.0) * (double)Pp;
+  if (!c->comm) {
     n += fedavg_accum_final(c->d_slots, Pp, c->d_n, (int)K, Pp, c->d_theta, (double)c->N_total, c->d_theta, st);
     CKL();
     c->prof.end(K_FEDAVG, 3.0 * (double)Pp * K, agg_bytes, st);
@@ -998,12 +1031,12 @@ fl_status fl_aggregate(fl_ctx* c, float* out_params, int64_t* out_total_samples)
     CK(cudaEventRecord(c->ev_ar0, st));
     CK(cudaEventRecord(c->ev_ar1, st));
   } else {
-    n += fedavg_accum_partial(c->d_slots, Pp, c->d_n, (int)K, Pp, c->d_theta, c->d_S, st);
+    // [S_g ‖ N_g]: N_g travels as a kernel argument (no pinned host scalar that a queued
+    // next round could overwrite before an asynchronous copy reads it)
+    n += fedavg_accum_partial(c->d_slots, Pp, c->d_n, (int)K, Pp, c->d_theta, (double)c->N_local, c->d_S, st);
     CKL();
     c->prof.end(K_FEDAVG, 3.0 * (double)Pp * K, agg_bytes, st);
     CK(cudaEventRecord(c->ev_acc1, st));
-    *c->h_N = (double)c->N_local;
-    CK(cudaMemcpyAsync(c->d_S + Pp, c->h_N, sizeof(double), cudaMemcpyHostToDevice, st));
     CK(cudaEventRecord(c->ev_ar0, st));
     ncclResult_t r = g_nccl.allReduce(c->d_S, c->d_S, (size_t)(Pp + 1), ncclFloat64, ncclSum, c->comm, st);
     if (r != ncclSuccess) return set_err(c, FL_ERR_NCCL, "ncclAllReduce: %s", g_nccl.errStr ? g_nccl.errStr(r) : "?");
@@ -1034,9 +1067,31 @@ static double ev_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
-static void fill_stats(fl_ctx* c, fl_round_stats* s) {
+// Per-rank device times of the last round; with a communicator, [round_ms, train_end_ms] of
+// every rank are all-gathered (8·2·world bytes on the ctx stream) for the max-over-ranks round
+// time and the "timedelta workers" statistic.  Collective when a
+// communicator exists: every rank must call it.
+static fl_status fill_stats(fl_ctx* c, fl_round_stats* s) {
   memset(s, 0, sizeof *s);
   s->round_ms = ev_ms(c->ev_entry, c->ev_end);
+  s->train_end_ms = ev_ms(c->ev_entry, c->ev_trained);
+  s->round_ms_max = s->round_ms;
+  s->train_end_ms_min = s->train_end_ms_max = s->train_end_ms;
+  if (c->comm) {
+    const int W = c->cfg.world_size;
+    const double mine[2] = {s->round_ms, s->train_end_ms};
+    CK(cudaMemcpyAsync(c->d_rstat, mine, sizeof mine, cudaMemcpyHostToDevice, c->st));  // pageable: staged now
+    ncclResult_t r = g_nccl.allGather(c->d_rstat, c->d_rstat + 2, 2, ncclFloat64, c->comm, c->st);
+    if (r != ncclSuccess) return set_err(c, FL_ERR_NCCL, "ncclAllGather: %s", g_nccl.errStr ? g_nccl.errStr(r) : "?");
+    CK(cudaMemcpyAsync(c->h_rstat, c->d_rstat + 2, sizeof(double) * 2 * W, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    for (int w = 0; w < W; ++w) {
+      s->round_ms_max = std::max(s->round_ms_max, c->h_rstat[2 * w]);
+      s->train_end_ms_min = std::min(s->train_end_ms_min, c->h_rstat[2 * w + 1]);
+      s->train_end_ms_max = std::max(s->train_end_ms_max, c->h_rstat[2 * w + 1]);
+    }
+  }
+  s->timedelta_ms = s->train_end_ms_max - s->train_end_ms_min;
   s->place_ms = c->place_ms;
   s->stage_ms = ev_ms(c->ev_start, c->ev_staged);
   s->train_ms = ev_ms(c->ev_staged, c->ev_trained);
@@ -1050,7 +1105,8 @@ static void fill_stats(fl_ctx* c, fl_round_stats* s) {
   s->waves = c->ws.n_waves;
   s->h2d_bytes = c->h2d;
   s->kernels = c->kernels;
-  s->client_updates_per_s = s->round_ms > 0 ? (double)c->K_total / (s->round_ms * 1e-3) : 0.0;
+  s->client_updates_per_s = s->round_ms_max > 0 ? (double)c->K_total / (s->round_ms_max * 1e-3) : 0.0;
+  return FL_OK;
 }
 
 fl_status fl_round(fl_ctx* c, const int64_t* cohort_ids, int64_t n_cohort, int32_t policy, const double* lb_coef,
@@ -1067,7 +1123,8 @@ fl_status fl_round(fl_ctx* c, const int64_t* cohort_ids, int64_t n_cohort, int32
   if (s != FL_OK) return s;
   if (stats) {
     CK(cudaEventSynchronize(c->ev_end));
-    fill_stats(c, &c->stats);
+    s = fill_stats(c, &c->stats);
+    if (s != FL_OK) return s;
     *stats = c->stats;
   }
   return FL_OK;
@@ -1104,8 +1161,11 @@ fl_status fl_get_client_times(fl_ctx* c, int64_t* ids, int64_t* m, double* t_ms,
 
 fl_status fl_get_stats(fl_ctx* c, fl_round_stats* out) {
   if (!c || !out) return FL_ERR_INVALID;
+  if (c->failed) return FL_ERR_STATE;
+  CK(cudaSetDevice(c->cfg.device));
   CK(cudaEventSynchronize(c->ev_end));
-  fill_stats(c, &c->stats);
+  fl_status s = fill_stats(c, &c->stats);
+  if (s != FL_OK) return s;
   *out = c->stats;
   return FL_OK;
 }
@@ -1168,9 +1228,9 @@ fl_status fl_get_local_plan(fl_ctx* c, int64_t* ids, int64_t* seg_off, int64_t* 
 fl_status fl_get_client_params(fl_ctx* c, int64_t client_id, float* out) {
   if (!c || !out) return FL_ERR_INVALID;
   if (c->failed) return FL_ERR_STATE;
-  int64_t e = -1;
-  for (size_t i = 0; i < c->exec.size(); ++i)
-    if (c->local_ids[(size_t)c->exec[i]] == client_id) e = (int64_t)i;
+  int64_t e = -1;  // exec position in the last trained round (fl_place does not change it)
+  for (size_t i = 0; i < c->exec_ids.size(); ++i)
+    if (c->exec_ids[i] == client_id) e = (int64_t)i;
   if (e < 0 || !c->d_slots) return set_err(c, FL_ERR_INVALID, "client %lld not trained on this rank", (long long)client_id);
   CK(cudaSetDevice(c->cfg.device));
   internal_to_canon(c->d_slots + e * c->L.P_pad, c->d_canon_of, c->L.P_pad, c->d_canon, c->st);

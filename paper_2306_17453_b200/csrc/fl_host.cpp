@@ -21,7 +21,15 @@ static inline int64_t n_batches(int64_t n, int64_t B) { return (n + B - 1) / B; 
 // Eq. 3 y = a·x + b·log(c·x) + d, clamped to a positive floor.
 double eq3_cost(const double* coef, double m) {
   double y = coef[0] * m + coef[1] * log(coef[2] * m) + coef[3];
-  return y < 1e-12 ? 1e-12 : y;
+  return !(y >= 1e-12) ? 1e-12 : y;  // NaN-safe clamp
+}
+
+// Eq. 3 needs c > 0 (log(c·m)) and finite coefficients; anything else would make
+// every load comparison false and silently put the whole cohort on one worker.
+static bool eq3_coef_ok(const double* coef) {
+  for (int i = 0; i < 4; ++i)
+    if (!std::isfinite(coef[i])) return false;
+  return coef[2] > 0.0;
 }
 
 int place(int policy, const int64_t* cohort, int64_t K, const int64_t* n_samples, int64_t n_clients,
@@ -29,7 +37,7 @@ int place(int policy, const int64_t* cohort, int64_t K, const int64_t* n_samples
   if (policy == FL_PLACE_LB_GPU) return place_lb_gpu(cohort, K, n_samples, n_clients, B, G, lb, out_ids, out_off);
   if (G < 1 || B < 1 || K < 0 || K > n_clients) return FL_ERR_INVALID;
   if (policy < FL_PLACE_BU || policy > FL_PLACE_SRR) return FL_ERR_INVALID;
-  if (policy == FL_PLACE_LB && !lb) return FL_ERR_INVALID;
+  if (policy == FL_PLACE_LB && (!lb || !eq3_coef_ok(lb))) return FL_ERR_INVALID;
   std::vector<char> seen((size_t)n_clients, 0);
   for (int64_t i = 0; i < K; ++i) {
     int64_t c = cohort[i];
@@ -84,6 +92,8 @@ int place(int policy, const int64_t* cohort, int64_t K, const int64_t* n_samples
 int place_lb_gpu(const int64_t* cohort, int64_t K, const int64_t* n_samples, int64_t n_clients, int64_t B,
                  int64_t G, const double* coef, int64_t* out_ids, int64_t* out_off) {
   if (G < 1 || B < 1 || K < 0 || K > n_clients || !coef) return FL_ERR_INVALID;
+  for (int64_t w = 0; w < G; ++w)
+    if (!eq3_coef_ok(coef + 4 * w)) return FL_ERR_INVALID;
   std::vector<char> seen((size_t)n_clients, 0);
   int64_t mmax = 1;
   for (int64_t i = 0; i < K; ++i) {

@@ -243,7 +243,7 @@ int internal_to_canon(const float* internal, const int64_t* canon_of, int64_t P_
 int fedavg_accum_final(const float* slots, int64_t stride, const int64_t* n, int K, int64_t P,
                        const float* theta_g, double N, float* out, cudaStream_t st);
 int fedavg_accum_partial(const float* slots, int64_t stride, const int64_t* n, int K, int64_t P,
-                         const float* theta_g, double* S, cudaStream_t st);
+                         const float* theta_g, double N_local, double* S, cudaStream_t st);
 int fedavg_finalize(const double* S, int64_t P, const float* theta_g, const double* Ndev, float* out,
                     cudaStream_t st);
 

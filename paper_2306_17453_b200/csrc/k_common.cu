@@ -34,6 +34,9 @@ template <bool FINAL>
 __global__ void __launch_bounds__(256) k_fedavg4(const float* __restrict__ slots, int64_t stride,
                                                  const int64_t* __restrict__ n, int K, int64_t P4,
                                                  const float* theta_g, double N, float* out, double* S) {
+  // partial (world > 1): S[4·P4] = N_g, written by the kernel itself so no host value has
+  // to outlive an asynchronous copy (N is N_local here)
+  if (!FINAL && blockIdx.x == 0 && threadIdx.x == 0) S[4 * P4] = N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P4; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 g = reinterpret_cast<const float4*>(theta_g)[i];
     const double gx = g.x, gy = g.y, gz = g.z, gw = g.w;
@@ -79,6 +82,7 @@ __global__ void __launch_bounds__(256) k_fedavg4(const float* __restrict__ slots
 template <bool FINAL>
 __global__ void k_fedavg1(const float* __restrict__ slots, int64_t stride, const int64_t* __restrict__ n, int K,
                           int64_t P, const float* theta_g, double N, float* out, double* S) {
+  if (!FINAL && blockIdx.x == 0 && threadIdx.x == 0) S[P] = N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     const double g = theta_g[i];
     double a = 0.0;
@@ -101,14 +105,15 @@ int fedavg_accum_final(const float* slots, int64_t stride, const int64_t* n, int
   return 1;
 }
 
+// S[0..P) = Σ_k n_k(θ_k − θ_g) and S[P] = N_local (the [S_g ‖ N_g] vector of the allreduce).
 int fedavg_accum_partial(const float* slots, int64_t stride, const int64_t* n, int K, int64_t P,
-                         const float* theta_g, double* S, cudaStream_t st) {
+                         const float* theta_g, double N_local, double* S, cudaStream_t st) {
   bool vec = (P % 4 == 0) && (stride % 4 == 0) && ((uintptr_t)slots % 16 == 0) && ((uintptr_t)theta_g % 16 == 0);
   if (vec) {
     int64_t P4 = P / 4;
-    k_fedavg4<false><<<grid_for(P4, 256, 1 << 20), 256, 0, st>>>(slots, stride, n, K, P4, theta_g, 1.0, nullptr, S);
+    k_fedavg4<false><<<grid_for(P4, 256, 1 << 20), 256, 0, st>>>(slots, stride, n, K, P4, theta_g, N_local, nullptr, S);
   } else {
-    k_fedavg1<false><<<grid_for(P, 256), 256, 0, st>>>(slots, stride, n, K, P, theta_g, 1.0, nullptr, S);
+    k_fedavg1<false><<<grid_for(P, 256), 256, 0, st>>>(slots, stride, n, K, P, theta_g, N_local, nullptr, S);
   }
   return 1;
 }

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version_and_param_counts():
-    assert fl.fl_abi_version() == 1
+    assert fl.fl_abi_version() == fl.ABI_VERSION == 2
     for m in ["logreg", "cnn", "speech", "lstm"]:
         assert fl.fl_n_params(m) == oracle.n_params(m)
     assert fl.fl_n_params(17) == 0
@@ -96,3 +96,18 @@ def test_no_cpu_fallback():
         fl.fl_round_init(fl.Config(model="logreg", batch_size=2, lr=0.1), sizes, x, y,
                          np.zeros(7850, np.float32))
     assert e.value.status == fl.FL_ERR_CUDA
+
+
+def test_lb_rejects_invalid_coefficients():
+    """Eq. 3 needs c > 0 and finite coefficients (log(c·m)); anything else used to
+    make every load comparison false and put the whole cohort on worker 0."""
+    sizes = np.arange(1, 7, dtype=np.int64) * 10
+    for bad in ([1, 1, -1, 0], [1, 1, 0, 0], [np.nan, 1, 1, 0], [1, np.inf, 1, 0]):
+        with pytest.raises(fl.FLError) as e:
+            fl.fl_place_plan("lb", range(6), sizes, 4, 2, bad)
+        assert e.value.status == fl.FL_ERR_INVALID
+        with pytest.raises(fl.FLError) as e:
+            fl.fl_place_plan("lb_gpu", range(6), sizes, 4, 2, [1, 1, 1, 0] + list(bad))
+        assert e.value.status == fl.FL_ERR_INVALID
+    ids, off = fl.fl_place_plan("lb", range(6), sizes, 4, 2, [1, 1, 1, 0])
+    assert list(off) == [0, 3, 6]
