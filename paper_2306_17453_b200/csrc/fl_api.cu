@@ -249,11 +249,6 @@ struct fl_ctx {
   // streams in total alias onto the device's 8 hardware queues and serialise.
   int ngroups = 2;  // round-robin groups (FL_GROUPS)
   int nsolo = 4;    // longest clients given their own high-priority group (FL_SOLO)
-  // PDL only for waves of at most this many clients (FL_PDL_MAXA; default all). With the
-  // trigger at the end of each CTA it helps every wave (C2 19.98 -> 19.18 ms, one 2000-sample
-  // client 9.3 -> 7.6 ms); an early trigger parked dependent CTAs on smem and starved the
-  // concurrent streams (C2 22 ms).
-  int pdl_max_a = 1 << 30;
   // SMs the bulk groups' persistent kernels leave free for the solo (critical-path) streams
   // when solo groups exist (FL_RESERVE_SMS; measured: 64 -> C2 -3%; after the 8-warp fc1
   // backward 32 is C2-neutral and 4% faster on a 400-client C3-law cohort)
@@ -452,7 +447,6 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   for (cudaEvent_t* e : evs) CK(cudaEventCreate(e));
   if (const char* ng = getenv("FL_GROUPS")) c->ngroups = std::max(1, atoi(ng));
   if (const char* ns = getenv("FL_SOLO")) c->nsolo = std::max(0, atoi(ns));
-  if (const char* pm = getenv("FL_PDL_MAXA")) c->pdl_max_a = atoi(pm);
   if (const char* ss = getenv("FL_SOLO_SMS")) c->solo_sms = std::max(8, std::min(148, atoi(ss)));
   if (const char* rs = getenv("FL_RESERVE_SMS")) c->reserve_sms = std::max(0, std::min(120, atoi(rs)));
   c->nsolo = std::min(c->nsolo, std::max(0, 8 - c->ngroups));
@@ -463,7 +457,7 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   int prio_lo = 0, prio_hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   for (int g = 0; g < nstreams; ++g) {
-    const bool hi = (g < c->nsolo) != (getenv("FL_BULK_PRIO") != nullptr);  // FL_BULK_PRIO: bulk groups high instead
+    const bool hi = g < c->nsolo;  // the critical-path (solo) streams run at high priority
     CK(cudaStreamCreateWithPriority(&c->gstream[(size_t)g], cudaStreamNonBlocking, hi ? prio_hi : prio_lo));
     CK(cudaEventCreateWithFlags(&c->ev_join[(size_t)g], cudaEventDisableTiming));
   }
@@ -956,7 +950,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
           for (int32_t a = 0; a < ws.A[(size_t)k]; ++a) sum_bs += h_bs[ws.bs_off[(size_t)k] + a];
           WaveArgs wa{ws.A[(size_t)k], (int)B, t == 0, ws.d_sidx + ws.slot_off[(size_t)k],
                       ws.d_bs + ws.bs_off[(size_t)k], c->cfg.lr, sum_bs, &c->prof, c->cfg.math == 0,
-                      ws.gn[(size_t)g], ws.A[(size_t)k] <= c->pdl_max_a, ws.d_bpre + ws.bs_off[(size_t)k] + k,
+                      ws.gn[(size_t)g], true, ws.d_bpre + ws.bs_off[(size_t)k] + k,
                       (ws.gsolo[(size_t)g] || c->reserve_sms == 0) ? c->solo_sms : 148 - c->reserve_sms};
           int nl = cnn_wave_simt(L, wa, c->d_xpack, c->d_ypack, c->d_theta, c->d_slots + base * L.P_pad,
                                  gv[(size_t)g], gst[(size_t)g]);

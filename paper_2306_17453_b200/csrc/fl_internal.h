@@ -215,13 +215,10 @@ int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64
 bool fc1_tc_supported(const Layout& L, int B);
 int fc1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p2,
                int64_t slots, float* h, float* part, int64_t part_floats, cudaStream_t st, int* launches);
-int fc1_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dh,
-              const float* p2, const uint8_t* am2, int64_t slots, float* dY2, cudaStream_t st);
+// fused fc1 dX (+ pool2/ReLU backward -> dY2) + dW + SGD: one W1 read and one write per client step
 int fc1_bwd_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wclients_src, float* slots_w,
                int64_t wclients_dst, const float* dh, const float* p2, const uint8_t* am2, int64_t slots, float* dY2,
                cudaStream_t st);
-int fc1_dw_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wclients_src, float* slots_w,
-              int64_t wclients_dst, const float* dh, const float* p2, int64_t slots, cudaStream_t st);
 int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p1,
                  int64_t slots, float* p2, uint8_t* am2, cudaStream_t st);
 // conv2 dX + ReLU' of pool1 -> dp1m [S][16][16][32] (the pool1 routing is fused into conv1's dW)

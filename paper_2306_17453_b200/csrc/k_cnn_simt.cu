@@ -518,75 +518,9 @@ __global__ void __launch_bounds__(256) k_head_sgd(const float* __restrict__ h, c
   }
 }
 
-// Classifier head of one client per block: logits = h·W2ᵀ + b2, softmax-CE (mean over
-// |b|, reading A9), dz = (p − onehot)/|b|, dh = (dz·W2) ⊙ [h > 0], then SGD on W2, b2.
-__global__ void __launch_bounds__(512) k_head(const float* __restrict__ h, const int32_t* __restrict__ ypack,
-                                              const int32_t* __restrict__ sidx, const int32_t* __restrict__ bs,
-                                              int B, int HID, int NCLS, WSrc w, int64_t o_w, int64_t o_b,
-                                              float* dst, int64_t P_pad, float lr, float* __restrict__ dh) {
-  extern __shared__ float sm[];
-  const int z = blockIdx.x, b = bs[z];
-  if (b == 0) return;
-  float* Ws = sm;                    // [NCLS][HID]
-  float* bias = Ws + NCLS * HID;     // [NCLS]
-  float* dz = bias + NCLS;           // [B][NCLS]
-  float* hs = dz + B * NCLS;         // [b][HID]: this client's fc1 activations, staged once
-  const float* W = w.at(z, o_w);
-  for (int e = threadIdx.x; e < NCLS * HID; e += blockDim.x) Ws[e] = W[e];
-  for (int e = threadIdx.x; e < NCLS; e += blockDim.x) bias[e] = *w.at(z, o_b + e);
-  const float* hz = h + (int64_t)z * B * HID;
-  for (int e = threadIdx.x; e < b * HID; e += blockDim.x) hs[e] = hz[e];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int idx = warp; idx < b * NCLS; idx += nw) {
-    const int r = idx / NCLS, q = idx - r * NCLS;
-    const float* hr = hs + r * HID;
-    float s = 0.f;
-    for (int n = lane; n < HID; n += 32) s = fmaf(Ws[q * HID + n], hr[n], s);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) dz[r * NCLS + q] = s + bias[q];
-  }
-  __syncthreads();
-  if (threadIdx.x < b) {
-    const int r = threadIdx.x;
-    float* zr = dz + r * NCLS;
-    const int y = ypack[sidx[z * B + r]];
-    float mx = zr[0];
-    for (int q = 1; q < NCLS; ++q) mx = fmaxf(mx, zr[q]);
-    float s = 0.f;
-    for (int q = 0; q < NCLS; ++q) s += expf(zr[q] - mx);
-    const float inv = 1.f / (float)b;
-    for (int q = 0; q < NCLS; ++q) zr[q] = (expf(zr[q] - mx) / s - (q == y ? 1.f : 0.f)) * inv;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < b * HID; e += blockDim.x) {
-    const int r = e / HID, n = e - r * HID;
-    float s = 0.f;
-    for (int q = 0; q < NCLS; ++q) s = fmaf(Ws[q * HID + n], dz[r * NCLS + q], s);
-    dh[((int64_t)z * B + r) * HID + n] = hs[e] > 0.f ? s : 0.f;
-  }
-  // rows past the batch are zero, so batch-padded tensor-core GEMMs over K = rows add nothing
-  for (int e = b * HID + threadIdx.x; e < B * HID; e += blockDim.x) dh[(int64_t)z * B * HID + e] = 0.f;
-  float* Wd = dst + (int64_t)z * P_pad;
-  for (int e = threadIdx.x; e < NCLS * HID; e += blockDim.x) {
-    const int q = e / HID, n = e - q * HID;
-    float g = 0.f;
-    for (int r = 0; r < b; ++r) g = fmaf(dz[r * NCLS + q], hs[r * HID + n], g);
-    Wd[o_w + e] = Ws[e] - lr * g;
-  }
-  if (threadIdx.x < NCLS) {
-    const int q = threadIdx.x;
-    float g = 0.f;
-    for (int r = 0; r < b; ++r) g += dz[r * NCLS + q];
-    Wd[o_b + q] = bias[q] - lr * g;
-  }
-}
-
 template <class Op>
 void launch(const Op& op, int Mmax, int Nmax, int Z, cudaStream_t st) {
-  static const bool t64 = env_knob("FL_SIMT_TILE64", 0) != 0;  // 64 x 64 everywhere (bit-identical)
-  const bool nm = !t64 && Mmax <= 32, nn = !t64 && Nmax <= 32;
+  const bool nm = Mmax <= 32, nn = Nmax <= 32;
   dim3 grid((Mmax + (nm ? 31 : 63)) / (nm ? 32 : 64), (Nmax + (nn ? 31 : 63)) / (nn ? 32 : 64), Z);
   if (nm && nn) k_gemm<Op, 32, 32><<<grid, NT, 0, st>>>(op);
   else if (nm) k_gemm<Op, 32, 64><<<grid, NT, 0, st>>>(op);
@@ -673,39 +607,22 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
                                                           slots, L.P_pad, wa.lr), ++n;
   pf.end(K_HEAD, 3.0 * f_f2, 8.0 * A * d.NCLS * d.HID + 8.0 * S * d.HID, st);
   // ---- backward (each layer's dX reads W before its dW epilogue overwrites it)
-  static const bool fc1_fused = [] {
-    const char* e = getenv("FL_FC1_FUSED");
-    return !(e && e[0] == '0');
-  }();
-  if (tcf && fc1_fused) {  // one W1 pass: dX (+ pool2/ReLU backward -> dY2), dW, SGD
-    pf.begin(st);
+  pf.begin(st);
+  if (tcf) {  // one W1 pass: dX (+ pool2/ReLU backward -> dY2), dW, SGD
     if (fc1_bwd_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, slots, wa.wclients, b.dh, b.p2, b.am2, b.slots, b.dY2,
                    st) < 0)
       return -1;
     ++n;
     pf.end(K_FC1_DW, 2.0 * f_f1, 2.0 * wbytes + 4.0 * S * (d.F + d.HID) + S * hw1 * d.C2 * (9.0 / 4.0), st);
   } else {
+    launch(FcDx{b.dh, wa.bs, B, d.F, d.HID, w, L.o_f1w, b.dp2}, B, d.F, A, st), ++n;
+    pf.end(K_FC1_DX, f_f1, wbytes + 4.0 * S * (d.F + d.HID), st);
     pf.begin(st);
-    if (tcf) {  // fused: dp2 -> pool2/ReLU backward -> dY2 in the epilogue
-      if (fc1_dx_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, b.dh, b.p2, b.am2, b.slots, b.dY2, st) < 0) return -1;
-      ++n;
-      pf.end(K_FC1_DX, f_f1, wbytes + 4.0 * S * (d.F + d.HID) + S * hw1 * d.C2 * (9.0 / 4.0), st);
-    } else {
-      launch(FcDx{b.dh, wa.bs, B, d.F, d.HID, w, L.o_f1w, b.dp2}, B, d.F, A, st), ++n;
-      pf.end(K_FC1_DX, f_f1, wbytes + 4.0 * S * (d.F + d.HID), st);
-      pf.begin(st);
-      k_unpool<<<dim3(4, A * B), 256, 0, st>>>(b.dp2, b.p2, b.am2, d.H1, d.W1, d.C2, B, wa.bs, b.dY2), ++n;
-      pf.end(K_UNPOOL2, 0, S * hw1 * d.C2 * (4.0 + 9.0 / 4.0), st);
-    }
+    k_unpool<<<dim3(4, A * B), 256, 0, st>>>(b.dp2, b.p2, b.am2, d.H1, d.W1, d.C2, B, wa.bs, b.dY2), ++n;
+    pf.end(K_UNPOOL2, 0, S * hw1 * d.C2 * (4.0 + 9.0 / 4.0), st);
     pf.begin(st);
-    if (tcf) {
-      if (fc1_dw_tc(L, wa, w.base, wa.first ? 1 : wa.wclients, slots, wa.wclients, b.dh, b.p2, b.slots, st) < 0)
-        return -1;
-      ++n;
-    } else {
-      launch(FcDwSgd{b.dh, b.p2, wa.bs, B, d.F, d.HID, w, slots, L.P_pad, L.o_f1w, L.o_f1b, wa.lr}, d.HID, d.F + 1, A,
-             st), ++n;
-    }
+    launch(FcDwSgd{b.dh, b.p2, wa.bs, B, d.F, d.HID, w, slots, L.P_pad, L.o_f1w, L.o_f1b, wa.lr}, d.HID, d.F + 1, A,
+           st), ++n;
     pf.end(K_FC1_DW, f_f1, 2.0 * wbytes + 4.0 * S * (d.F + d.HID), st);
   }
   pf.begin(st);

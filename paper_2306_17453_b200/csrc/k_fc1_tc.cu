@@ -3,7 +3,7 @@
 // weight gradient with the SGD step fused in its epilogue.
 //
 // fc1 holds 97% of the CNN's parameters, so every client step streams its 8 MB weight
-// matrix three times (forward, dX, dW read + write); these kernels are HBM-bound by design
+// matrix twice (forward; fused dX + dW: one read + one write); HBM-bound by design
 // and the batch (|b| <= 32) rides in the MMA N dimension ("swap AB"):
 //   forward  D[n][r]  = Σ_k W1[n][k] p2[r][k]      A = W1 tile   (K-major, SW128)
 //                                                   B = p2 rows   (K-major, SW128)
@@ -13,7 +13,7 @@
 //            epilogue: dp2 -> dY2 through pool2's argmax and ReLU' (writes every dY2 cell).
 //   dW+SGD   D[n][k]  = Σ_r dh[r][n] p2[r][k]      A = dhᵀ, B = p2ᵀ (both MN-major), K = |b|
 //            epilogue: W1 <- W1 − η·D (θ_g read on the first wave), b1 from Σ_r dh.
-// Rows r >= |b| of a client's slots are zero in dh (k_head writes them) and finite in p2,
+// Rows r >= |b| of a client's slots are zero in dh (k_head_fwd writes them) and finite in p2,
 // so padding the batch to 32 never changes a sum.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -140,232 +140,7 @@ __global__ void k_fc1_fwd_reduce(const float* __restrict__ part, const int32_t* 
   h[((int64_t)a * B + r) * HID + n] = s > 0.f ? s : 0.f;
 }
 
-// ------------------------------------------------------------------ dX (+ pool2 backward)
-constexpr int DX_A = 4 * 32 * 128, DX_B = NB * 128, DX_STAGE = DX_A + DX_B, DX_NST = 4;
-constexpr int DX_BAR = DX_NST * DX_STAGE, DX_SMEM = DX_BAR + 128 + 1024;
-
-struct DxArgs {
-  const int32_t* bs;
-  int B, HID, F, wmul;
-  int H2, W2, C2;           // pooled map (dp2 index k = (h*W2 + w)*C2 + c)
-  const float* p2;
-  const uint8_t* am2;
-  float* dY2;               // [S][2*H2][2*W2][C2]
-};
-
-__global__ void __launch_bounds__(192, 1)
-    k_fc1_dx_tc(const __grid_constant__ CUtensorMap mapWt, const __grid_constant__ CUtensorMap mapDh, DxArgs p) {
-  constexpr uint32_t IDESC = tc::idesc_tf32(128, NB, 1, 0);
-  const int a = blockIdx.y, mt = blockIdx.x;
-  const int bs = p.bs[a];
-  if (bs == 0) return;
-  const int nkb = p.HID / 32;
-  // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
-  // would stall other streams' kernels) or touching anything it writes.
-  pdl_wait();
-  extern __shared__ uint8_t smem_raw[];
-  // align by pointer arithmetic on the shared array (an integer round trip would turn every
-  // epilogue access into a generic LD/ST instead of LDS/STS)
-  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + DX_BAR);
-  uint64_t* empty = full + DX_NST;
-  uint64_t* tfull = empty + DX_NST;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0) {
-    if (lane == 0) {
-      tc::prefetch_tmap(&mapWt);
-      tc::prefetch_tmap(&mapDh);
-      for (int i = 0; i < DX_NST; ++i) {
-        tc::mbar_init(full + i, 1);
-        tc::mbar_init(empty + i, 1);
-      }
-      tc::mbar_init(tfull, 1);
-      tc::fence_mbar_init();
-    }
-    __syncwarp();
-    tc::tmem_alloc<32>(tslot);
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tbase = *tslot;
-  if (warp == 0) {
-    if (tc::elect_one()) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int st = kb % DX_NST, ph = (kb / DX_NST) & 1;
-        tc::mbar_wait(empty + st, ph ^ 1);
-        uint8_t* sa = smem + st * DX_STAGE;
-        tc::mbar_expect_tx(full + st, DX_STAGE);
-        // W1ᵀ tile: 4 chunks of 32 k (MN) x 32 n rows (K), chunk stride 4096 B
-        tc::tma_load_4d(sa, &mapWt, full + st, 0, 32 * kb, 4 * mt, a * p.wmul);
-        tc::tma_load_3d(sa + DX_A, &mapDh, full + st, 32 * kb, a * p.B, 0);
-      }
-    }
-  } else if (warp == 1) {
-    if (tc::elect_one()) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int st = kb % DX_NST, ph = (kb / DX_NST) & 1;
-        tc::mbar_wait(full + st, ph);
-        tc::tc_fence_after();
-        const uint32_t sa = tc::smem_u32(smem + st * DX_STAGE), sb = sa + DX_A;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          tc::mma_tf32(tbase, tc::sdesc(sa + k * 1024, 4096, 512, tc::kSW128_32B),
-                       tc::sdesc(sb + k * 32, 0, 1024, tc::kSW128), IDESC, (kb | k) != 0);
-        tc::mma_commit(empty + st);
-      }
-      tc::mma_commit(tfull);
-    }
-  } else {
-    const int qd = warp & 3, k = mt * 128 + qd * 32 + lane;  // dp2 index (h, w, c)
-    // the pool2 state of this column does not depend on the MMA: fetch it while it runs
-    bool pos[NB];
-    uint8_t amr[NB];
-#pragma unroll
-    for (int r = 0; r < NB; ++r) {
-      const int64_t s = (int64_t)a * p.B + r;
-      pos[r] = r < bs ? p.p2[s * p.F + k] > 0.f : false;
-      amr[r] = r < bs ? p.am2[s * p.F + k] : 0;
-    }
-    tc::mbar_wait(tfull, 0);
-    tc::tc_fence_after();
-    float v[NB];
-    tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16), *reinterpret_cast<float(*)[16]>(v));
-    tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + 16, *reinterpret_cast<float(*)[16]>(v + 16));
-    const int c = k % p.C2, pw = (k / p.C2) % p.W2, ph = k / (p.C2 * p.W2);
-    const int W1 = 2 * p.W2, H1 = 2 * p.H2;
-#pragma unroll
-    for (int r = 0; r < NB; ++r) {
-      if (r >= bs) break;
-      const int64_t s = (int64_t)a * p.B + r;
-      const float g = pos[r] ? v[r] : 0.f;  // ReLU'(pooled) = ReLU'(argmax)
-      const int am = amr[r];
-      float* d = p.dY2 + ((s * H1 + 2 * ph) * W1 + 2 * pw) * p.C2 + c;
-      d[0] = am == 0 ? g : 0.f;
-      d[p.C2] = am == 1 ? g : 0.f;
-      d[(int64_t)W1 * p.C2] = am == 2 ? g : 0.f;
-      d[(int64_t)W1 * p.C2 + p.C2] = am == 3 ? g : 0.f;
-    }
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  pdl_trigger();  // late trigger: a dependent kernel's CTAs park on SM resources until it runs
-  if (warp == 0) tc::tmem_dealloc<32>(tbase);
-}
-
-// ------------------------------------------------------------------ dW + SGD
-// One CTA: a 128 (n) x 256 (k) tile of W1.  The tile (128 KB) is brought into shared
-// memory by TMA alongside the operands, updated there by the epilogue warps
-// (W <- W − η·D, 16-byte accesses in the SW128 pattern, conflict-free), and written back
-// by TMA: the HBM stream is one bulk read and one bulk write of W1 per client step.
-constexpr int DW_N = 128;  // 128 x 128 W1 tile: ~97 KB smem, two CTAs per SM overlap load / MMA / store
-constexpr int DW_A = 4 * NB * 128, DW_B = (DW_N / 32) * NB * 128;  // 16 KB + 32 KB
-constexpr int DW_W = (DW_N / 32) * 128 * 128;                        // 8 chunks of [128 n][32 k] = 128 KB
-constexpr int DW_BAR = DW_W + DW_A + DW_B, DW_SMEM = DW_BAR + 64 + 1024;
-
-struct DwArgs {
-  const int32_t* bs;
-  int B, HID, F, ntiles, wmul;
-  const float* bsrc;   // client 0 bias (θ_g on the first wave); client a at + a*bstride
-  int64_t bstride;
-  float* bdst;         // slot 0 bias; client a at + a*P_pad
-  int64_t P_pad;
-  const float* dh;     // [S][HID]
-  float lr;
-};
-
-__global__ void __launch_bounds__(192, 1)
-    k_fc1_dw_tc(const __grid_constant__ CUtensorMap mapDh, const __grid_constant__ CUtensorMap mapX,
-                const __grid_constant__ CUtensorMap mapWsrc, const __grid_constant__ CUtensorMap mapWdst, DwArgs p) {
-  constexpr uint32_t IDESC = tc::idesc_tf32(128, DW_N, 1, 1);
-  const int a = blockIdx.y, mt = blockIdx.x / p.ntiles, nt = blockIdx.x % p.ntiles;
-  const int bs = p.bs[a];
-  if (bs == 0) return;
-  // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
-  // would stall other streams' kernels) or touching anything it writes.
-  pdl_wait();
-  extern __shared__ uint8_t smem_raw[];
-  // align by pointer arithmetic on the shared array (an integer round trip would turn every
-  // epilogue access into a generic LD/ST instead of LDS/STS)
-  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sw = smem;                  // W tile
-  uint8_t* sa = smem + DW_W;           // dhᵀ
-  uint8_t* sbp = sa + DW_A;            // p2ᵀ
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + DW_BAR);
-  uint64_t* tfull = full + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0) {
-    if (lane == 0) {
-      tc::mbar_init(full, 1);
-      tc::mbar_init(tfull, 1);
-      tc::fence_mbar_init();
-    }
-    __syncwarp();
-    tc::tmem_alloc<DW_N>(tslot);
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tbase = *tslot;
-  if (warp == 0) {
-    if (tc::elect_one()) {
-      tc::mbar_expect_tx(full, DW_W + DW_A + DW_B);
-      tc::tma_load_3d(sa, &mapDh, full, 0, a * p.B, 4 * mt);                   // dhᵀ: 4 chunks of 32 n
-      tc::tma_load_3d(sbp, &mapX, full, 0, a * p.B, (DW_N / 32) * nt);         // p2ᵀ: 8 chunks of 32 k
-      for (int j = 0; j < DW_N / 32; ++j)                                       // W tile, 8 x [128 n][32 k]
-        tc::tma_load_3d(sw + j * 16384, &mapWsrc, full, nt * DW_N + 32 * j, 128 * mt, a * p.wmul);
-    }
-  } else if (warp == 1) {
-    if (tc::elect_one()) {
-      tc::mbar_wait(full, 0);
-      tc::tc_fence_after();
-      const uint32_t ua = tc::smem_u32(sa), ub = tc::smem_u32(sbp);
-#pragma unroll
-      for (int k = 0; k < 4; ++k)  // K = 32 batch slots
-        tc::mma_tf32(tbase, tc::sdesc(ua + k * 1024, NB * 128, 512, tc::kSW128_32B),
-                     tc::sdesc(ub + k * 1024, NB * 128, 512, tc::kSW128_32B), IDESC, k != 0);
-      tc::mma_commit(tfull);
-    }
-  } else {
-    const int qd = warp & 3, row = qd * 32 + lane, n = mt * 128 + row;
-    tc::mbar_wait(full, 0);  // W tile landed (MMA completion implies it, but be explicit)
-    tc::mbar_wait(tfull, 0);
-    tc::tc_fence_after();
-    for (int j = 0; j < DW_N / 32; ++j) {
-      float v[32];
-      tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + 32 * j, *reinterpret_cast<float(*)[16]>(v));
-      tc::tmem_ld16(tbase + ((uint32_t)(qd * 32) << 16) + 32 * j + 16, *reinterpret_cast<float(*)[16]>(v + 16));
-      uint8_t* rowp = sw + j * 16384 + row * 128;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {  // 16-byte piece q of the row sits at (q ^ row%8) (SW128)
-        float4* w4 = reinterpret_cast<float4*>(rowp + ((q ^ (row & 7)) << 4));
-        float4 w = *w4;
-        w.x -= p.lr * v[4 * q];
-        w.y -= p.lr * v[4 * q + 1];
-        w.z -= p.lr * v[4 * q + 2];
-        w.w -= p.lr * v[4 * q + 3];
-        *w4 = w;
-      }
-    }
-    tc::fence_async_smem();  // generic-proxy writes -> TMA store
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (warp == 2 && tc::elect_one()) {
-      for (int j = 0; j < DW_N / 32; ++j) tc::tma_store_3d(&mapWdst, sw + j * 16384, nt * DW_N + 32 * j, 128 * mt, a);
-      tc::tma_store_commit_wait();
-    }
-    if (nt == 0) {  // bias: Σ_r dh[r][n]
-      float g = 0.f;
-      for (int r = 0; r < bs; ++r) g += p.dh[((int64_t)a * p.B + r) * p.HID + n];
-      p.bdst[(int64_t)a * p.P_pad + n] = p.bsrc[(int64_t)a * p.bstride * p.wmul + n] - p.lr * g;
-    }
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  pdl_trigger();  // late trigger: a dependent kernel's CTAs park on SM resources until it runs
-  if (warp == 0) tc::tmem_dealloc<DW_N>(tbase);
-}
+constexpr int DW_N = 128;  // W1 tile width in k (fc1_tc_supported requires F % DW_N == 0)
 
 // ------------------------------------------------------------------ fused dX + dW + SGD
 // Persistent over (client, 128-column k panel of W1) tiles; a panel is streamed in 4 chunks
@@ -667,56 +442,6 @@ int fc1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t 
                                                                        wbase + L.o_f1b, L.P_pad, wmul, h);
     *launches = 2;
   }
-  return cudaGetLastError() == cudaSuccess ? 1 : -1;
-}
-
-// dX: dh -> dp2 -> (pool2/ReLU backward) -> dY2
-int fc1_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dh,
-              const float* p2, const uint8_t* am2, int64_t slots, float* dY2, cudaStream_t st) {
-  const CnnDims& d = L.d;
-  CUtensorMap mw, md;
-  // W1 viewed as (k_in 32, n HID, k_out F/32, client): box {32, 32, 4, 1} = 4 MN chunks x 32 n rows
-  uint64_t dw[4] = {32, (uint64_t)d.HID, (uint64_t)d.F / 32, (uint64_t)wclients};
-  uint64_t sw[3] = {(uint64_t)d.F * 4, 128, (uint64_t)L.P_pad * 4};
-  uint32_t bw[4] = {32, 32, 4, 1};
-  uint64_t dd[3] = {(uint64_t)d.HID, (uint64_t)slots, 1};
-  uint64_t sd[2] = {(uint64_t)d.HID * 4, (uint64_t)d.HID * 4 * slots};
-  uint32_t bd[3] = {32, NB, 1};
-  if (!tmap_encode(&mw, wbase + L.o_f1w, 4, dw, sw, bw, 2) || !tmap_encode(&md, dh, 3, dd, sd, bd, 1)) return -1;
-  static bool attr = false;
-  set_smem(k_fc1_dx_tc, DX_SMEM, attr);
-  DxArgs p{wa.bs, wa.B, d.HID, d.F, wa.first ? 0 : 1, d.H2, d.W2, d.C2, p2, am2, dY2};
-  launch_pdl(wa.pdl, k_fc1_dx_tc, dim3(d.F / 128, wa.A), 192, DX_SMEM, st, mw, md, p);
-  return cudaGetLastError() == cudaSuccess ? 1 : -1;
-}
-
-// dW + SGD on W1, b1
-int fc1_dw_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wclients_src, float* slots_w,
-              int64_t wclients_dst, const float* dh, const float* p2, int64_t slots, cudaStream_t st) {
-  const CnnDims& d = L.d;
-  CUtensorMap mh, mx, mws, mwd;
-  // dhᵀ: (n_in 32, slot, n_out HID/32), box {32, 32 slots, 4}
-  uint64_t dh3[3] = {32, (uint64_t)slots, (uint64_t)d.HID / 32};
-  uint64_t sh3[2] = {(uint64_t)d.HID * 4, 128};
-  uint32_t bh3[3] = {32, NB, 4};
-  uint64_t dx3[3] = {32, (uint64_t)slots, (uint64_t)d.F / 32};
-  uint64_t sx3[2] = {(uint64_t)d.F * 4, 128};
-  uint32_t bx3[3] = {32, NB, DW_N / 32};
-  // W1 of every client (or θ_g): (k F, n HID, client), box {32 k, 128 n, 1}, SW128
-  uint64_t dws[3] = {(uint64_t)d.F, (uint64_t)d.HID, (uint64_t)wclients_src};
-  uint64_t dwd[3] = {(uint64_t)d.F, (uint64_t)d.HID, (uint64_t)wclients_dst};
-  uint64_t sww[2] = {(uint64_t)d.F * 4, (uint64_t)L.P_pad * 4};
-  uint32_t bww[3] = {32, 128, 1};
-  if (!tmap_encode(&mh, dh, 3, dh3, sh3, bh3, 2) || !tmap_encode(&mx, p2, 3, dx3, sx3, bx3, 2) ||
-      !tmap_encode(&mws, wsrc + L.o_f1w, 3, dws, sww, bww, 1) ||
-      !tmap_encode(&mwd, slots_w + L.o_f1w, 3, dwd, sww, bww, 1))
-    return -1;
-  static bool attr = false;
-  set_smem(k_fc1_dw_tc, DW_SMEM, attr);
-  const int ntiles = d.F / DW_N, mtiles = d.HID / 128;
-  DwArgs p{wa.bs, wa.B, d.HID, d.F, ntiles, wa.first ? 0 : 1, wsrc + L.o_f1b, L.P_pad, slots_w + L.o_f1b,
-           L.P_pad, dh, wa.lr};
-  launch_pdl(wa.pdl, k_fc1_dw_tc, dim3(mtiles * ntiles, wa.A), 192, DW_SMEM, st, mh, mx, mws, mwd, p);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

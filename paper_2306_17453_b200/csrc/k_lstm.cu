@@ -71,122 +71,17 @@ struct RecArgs {
   float* dpre;         // bwd: [S][T][LG] gradient of the gate pre-activations
 };
 
-// Forward recurrence of one layer for one client (cluster of CL = 16 CTAs, 4·RPC = 256 threads each).
-// Thread (rl, kq) = (tid / 4, tid % 4) accumulates gate row rl over k-quarter kq for all 4
-// batch rows with 16 independent FMA chains (float4 loads of W and h); the 4 threads of a row
-// combine with two shuffles.  The next step's input projection is prefetched during the step.
+// Forward recurrence of one layer for one client: a cluster of CL = 16 CTAs, FT threads each.
 constexpr int FT = 4 * RPC;  // thread (row, k-quarter)
 constexpr int NOWN = 4 * UPC;  // cell-owner threads: (batch row, unit)
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(FT, 2) k_lstm_fwd(RecArgs p) {
-  pdl_wait();
-  cg::cluster_group cl = cg::this_cluster();
-  const int c = (int)cl.block_rank(), a = blockIdx.x / CL, tid = threadIdx.x;
-  extern __shared__ float sm[];
-  float* Wr = sm;                  // [RPC][WPF]
-  float* hb = sm + LH * WPB;       // [2][4][LH] h_{t-1} of the 4 batch rows (ping-pong)
-  float* gs = hb + 2 * 4 * LH;     // [4][RPC] activated gates of this CTA's rows
-  uint64_t* hbar = reinterpret_cast<uint64_t*>(sm + LH * WPB + 2 * 4 * LH + 4 * RPC + 2 * CL * 4 * UPC);  // [2]
-  {
-    const float* W = p.wsrc + (int64_t)a * p.wstride + p.o_whh;
-    for (int e = tid; e < RPC * LH / 4; e += FT) {
-      const int rl = e / (LH / 4), k4 = e - rl * (LH / 4);
-      *reinterpret_cast<float4*>(Wr + rl * WPF + 4 * k4) =
-          __ldg(reinterpret_cast<const float4*>(W + (int64_t)grow_of(rl, c) * LH) + k4);
-    }
-  }
-  for (int e = tid; e < 2 * 4 * LH; e += FT) hb[e] = 0.f;
-  const int cb = tid / UPC, cu = tid % UPC, unit = UPC * c + cu;  // cell owned by threads < NOWN
-  const int64_t cs = (int64_t)a * p.B + cb;
-  float cst = 0.f;
-  if (tid < NOWN) {
-    p.C[cs * (LT + 1) * LH + unit] = 0.f;
-    p.H[cs * (LT + 1) * LH + unit] = 0.f;
-  }
-  const int rl = tid >> 2, kh = tid & 3, gr = grow_of(rl, c);
-  const int64_t s0 = (int64_t)a * p.B;
-  const float* xr = p.xp + s0 * LT * LG + gr;  // batch row b, step t at xr + (b*LT + t)*LG
-  float xn[4];
-#pragma unroll
-  for (int b = 0; b < 4; ++b) xn[b] = kh == 0 ? xr[(int64_t)b * LT * LG] : 0.f;
-  if (tid == 0) {
-    tc::mbar_init(hbar, 1);
-    tc::mbar_init(hbar + 1, 1);
-    tc::fence_mbar_init();
-  }
-  // this cell's h slot and the barriers, mapped into each peer's shared memory at the store
-  const uint32_t lh = tc::smem_u32(hb + cb * LH + unit), lb = tc::smem_u32(hbar);
-  cl.sync();
-  const bool tg = rl / UPC == 2;  // the cell-candidate gate uses tanh
-  float sv[6];
-  for (int t = 0; t < LT; ++t) {
-    const int cur = t & 1, nxt = cur ^ 1;
-    if (tid == 0 && t + 1 < LT) tc::mbar_expect_tx(hbar + nxt, XCH_BYTES);  // h_t lands in buffer nxt
-    if (t > 0) tc::mbar_wait(hbar + cur, ((t - 1) >> 1) & 1);                // h_{t-1} from all CL CTAs
-    float acc[4] = {xn[0], xn[1], xn[2], xn[3]};
-    if (kh == 0 && t + 1 < LT)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) xn[b] = xr[((int64_t)b * LT + t + 1) * LG];
-    // the 4 threads of a row take interleaved float4 columns (k = 16j + 4kq): their loads of the
-    // same W row and of h fall in distinct banks
-    const float* w = Wr + rl * WPF + 4 * kh;
-    const float* h = hb + cur * 4 * LH + 4 * kh;
-    float ax[4] = {0.f, 0.f, 0.f, 0.f}, ay[4] = {0.f, 0.f, 0.f, 0.f}, az[4] = {0.f, 0.f, 0.f, 0.f},
-          aw[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-    for (int k = 0; k < LH; k += 16) {
-      const float4 wv = *reinterpret_cast<const float4*>(w + k);
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const float4 hv = *reinterpret_cast<const float4*>(h + b * LH + k);
-        ax[b] = fmaf(wv.x, hv.x, ax[b]);
-        ay[b] = fmaf(wv.y, hv.y, ay[b]);
-        az[b] = fmaf(wv.z, hv.z, az[b]);
-        aw[b] = fmaf(wv.w, hv.w, aw[b]);
-      }
-    }
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      acc[b] += (ax[b] + ay[b]) + (az[b] + aw[b]);
-      acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], 1);
-      acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], 2);
-    }
-    if (kh == 0)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) gs[b * RPC + rl] = tg ? tanhf(acc[b]) : sigm(acc[b]);
-    __syncthreads();
-    if (tid < NOWN) {
-      const float ig = gs[cb * RPC + cu], fg = gs[cb * RPC + UPC + cu], gg = gs[cb * RPC + 2 * UPC + cu],
-                  og = gs[cb * RPC + 3 * UPC + cu];
-      cst = fg * cst + ig * gg;                 // c_t = f c_{t-1} + i g
-      const float hv = og * tanhf(cst);         // h_t = o tanh(c_t)
-      if (t + 1 < LT)
-#pragma unroll
-        for (int r = 0; r < CL; ++r) st_async_f32(mapa_u32(lh + nxt * 4 * LH * 4, r), hv, mapa_u32(lb + nxt * 8, r));
-      sv[0] = cst, sv[1] = hv, sv[2] = ig, sv[3] = fg, sv[4] = gg, sv[5] = og;
-    }
-    __syncthreads();  // gs is rewritten by the next step
-    // No cluster barrier per step: a CTA cannot run ahead into a buffer still being read,
-    // because its next step needs every CTA's h_t, which each sends only after reading h_{t-1}.
-    if (tid < NOWN) {
-      p.C[(cs * (LT + 1) + t + 1) * LH + unit] = sv[0];
-      p.H[(cs * (LT + 1) + t + 1) * LH + unit] = sv[1];
-      float* g = p.G + (cs * LT + t) * LG + unit;
-      g[0] = sv[2];
-      g[LH] = sv[3];
-      g[2 * LH] = sv[4];
-      g[3 * LH] = sv[5];
-    }
-  }
-  cl.sync();  // no CTA exits while a peer may still address its shared memory
-}
-
 // Forward recurrence, register-resident variant: W_hh is constant over the T steps, so each
 // thread keeps its 4-row x 16-column segment of the CTA's slice in registers for the whole
 // sequence.  Thread (rg, ks) = (tid / 16, tid % 16) owns rows 4·rg .. 4·rg+3 and columns
 // {4·ks + 64·j + u}; per step it reads 16 float4 of h_{t-1} (each feeds 4 rows, 16 FMAs) and
 // the 16 partial (row, batch) sums of a row group are reduce-scattered over its 16 lanes
 // with 15 shuffles (fixed butterfly order); lane ks then owns (row, batch) j = bitrev4(ks).
-// Shared-memory traffic per step is a quarter of k_lstm_fwd's (which re-reads h for every row).
+// Shared-memory traffic per step is a quarter of a shared-memory-resident W_hh's (which re-reads h for
+// every row; round 1, removed).
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(FT, 2) k_lstm_fwd_reg(RecArgs p) {
   pdl_wait();
   cg::cluster_group cl = cg::this_cluster();
@@ -387,7 +282,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2) k_lstm_bwd(
 #pragma unroll
       for (int src = 0; src < CL; ++src) s += part[((pb * CL + src) * 4 + cb) * UPC + cu];
       dhr = s;
-      float* d = p.dpre + (cs * LT + t) * LG + unit;  // stored after the barrier (see k_lstm_fwd)
+      float* d = p.dpre + (cs * LT + t) * LG + unit;  // stored after the barrier (see k_lstm_fwd_reg)
       d[0] = sd[0];
       d[LH] = sd[1];
       d[2 * LH] = sd[2];
@@ -752,11 +647,9 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
   const float lr = wa.lr;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_lstm_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, REC_SMEM);
     cudaFuncSetAttribute(k_lstm_fwd_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, REC_SMEM);
     cudaFuncSetAttribute(k_lstm_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, REC_SMEM);
     if (CL > 8) {  // 16-CTA clusters are a non-portable size
-      cudaFuncSetAttribute(k_lstm_fwd, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaFuncSetAttribute(k_lstm_fwd_reg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaFuncSetAttribute(k_lstm_bwd, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     }
@@ -765,11 +658,10 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
   }
   const int64_t S_T1 = (int64_t)(LT + 1) * LH;  // per-slot stride of H / C
   int n = 0;
-  static const bool g128 = env_knob("FL_LSTM_GEMM64", 0) == 0;
   auto gemm = [&](const GemmArgs& g) {
     // small waves: 128x128 tiles would leave most SMs idle; the 64x64 kernel is bit-identical
     const int64_t b128 = (int64_t)((g.N + G2_T - 1) / G2_T) * ((g.M + G2_T - 1) / G2_T) * A;
-    if (g128 && b128 >= 2 * 148)
+    if (b128 >= 2 * 148)
       launch_pdl(wa.pdl, k_lstm_gemm128, dim3((g.N + G2_T - 1) / G2_T, (g.M + G2_T - 1) / G2_T, A), 256, 0, st, g);
     else
       launch_pdl(wa.pdl, k_lstm_gemm, dim3((g.N + 63) / 64, (g.M + 63) / 64, A), 256, 0, st, g);
@@ -780,8 +672,7 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
   EmbArgs ea{xpack, wa.sidx, wbase, wstride, q.emb, q.wih[0], q.bih[0], q.bhh[0], B, b.E, b.xp};
   launch_pdl(wa.pdl, k_lstm_embed, dim3(A * B), 256, 0, st, ea), ++n;
   RecArgs r0{wbase, wstride, q.whh[0], B, b.xp, b.G0, b.C0, b.H0, nullptr, 0, nullptr};
-  static const bool fwd_reg = env_knob("FL_LSTM_FWD_SMEM", 0) == 0;
-  auto fwd = fwd_reg ? k_lstm_fwd_reg : k_lstm_fwd;
+  auto fwd = k_lstm_fwd_reg;
   launch_pdl(wa.pdl, fwd, dim3(A * CL), FT, REC_SMEM, st, r0), ++n;
   // layer-1 input projection: xp[s][t] = W_ih1 · H0[s][t+1] + b_ih1 + b_hh1
   {
