@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define FL_ABI_VERSION 2u
+#define FL_ABI_VERSION 3u
 
 typedef enum {
   FL_OK = 0,
@@ -86,7 +86,26 @@ typedef struct {
                                     finalize) on one GPU; NULL: the fused single-GPU accumulate+finalize. */
   int32_t math;             /* 0: tensor cores (TF32, tcgen05) where built; 1: FP32 SIMT everywhere */
   void* stream;             /* optional borrowed cudaStream_t; NULL: the ctx creates its own */
+  /* SM partition of this rank (a CUDA green context; heterogeneous-worker emulation):
+   *   0: the whole GPU;  s > 0: the first partition of >= s SMs of cfg.device;
+   *   s < 0: the remainder after splitting off the first partition of >= -s SMs (so two ranks
+   *   configured s and -s share a GPU on disjoint SMs).  Every stream of the ctx is created in
+   *   the partition; persistent grids are sized to its SM count.  FL_ERR_INVALID with a
+   *   borrowed stream; FL_ERR_CUDA if the driver cannot split. */
+  int32_t sm_count;
+  /* Cross-rank aggregation (world_size > 1), the paper's server-traffic question (P:73, P:221-222,
+   * §4.3):
+   *   FL_AGG_NCCL (0): per-GPU fused partial [S_g ‖ N_g] -> ncclAllReduce -> finalize;
+   *   FL_AGG_PEER (1): one kernel per rank over peer memory: the fused fp64 partial S_g, then
+   *     this rank's slice of Σ_g S_g read from every peer, θ_new = fp32(θ_g + S/N) stored into
+   *     every rank's θ_g (reduce-scatter + finalize + all-gather, no NCCL); needs fl_peer_connect;
+   *   FL_AGG_UNAGGREGATED (2): the ablation without partial aggregation: every rank ships each
+   *     client model θ_k (fp32) to rank 0 (the "server GPU"), which averages all
+   *     of them and stores θ_new into every rank; needs fl_peer_connect. */
+  int32_t agg_mode;
 } fl_config;
+
+typedef enum { FL_AGG_NCCL = 0, FL_AGG_PEER = 1, FL_AGG_UNAGGREGATED = 2 } fl_agg_mode;
 
 /* The client population, client-id order.  Sample rows of client k
  * are rows [Σ_{j<k} n_j, Σ_{j<=k} n_j) of x / y.
@@ -124,6 +143,9 @@ typedef struct {
   double round_ms_max;  /* the round time: max over ranks of round_ms */
   double train_end_ms_min, train_end_ms_max;
   double timedelta_ms;  /* "timedelta workers": train_end_ms_max − train_end_ms_min */
+  int64_t xfer_bytes;   /* bytes this rank sent to other ranks' memory in the aggregation
+                           (peer / unaggregated modes; NCCL: 8·(P_pad+1)·2·(W−1)/W, ring estimate) */
+  int32_t sm_count;     /* SMs this rank's kernels may use (its green-context partition) */
 } fl_round_stats;
 
 uint32_t fl_abi_version(void);
@@ -242,6 +264,23 @@ typedef struct {
 } fl_kernel_stats;
 fl_status fl_set_profiling(fl_ctx* ctx, int32_t on);
 fl_status fl_get_kernel_stats(fl_ctx* ctx, int32_t kind, fl_kernel_stats* out);
+
+/* ---- peer-memory aggregation (agg_mode FL_AGG_PEER / FL_AGG_UNAGGREGATED) ----------- */
+/* A rank's peer blob: FL_PEER_BLOB_BYTES opaque bytes (process id, device, CUDA IPC handles and
+ * addresses of this ctx's partial buffer S, θ_g, signal words and the unaggregated receive
+ * buffer).  Every rank exports one; the caller all-gathers them (e.g. torch.distributed) and
+ * passes the array [world_size][FL_PEER_BLOB_BYTES] in rank order to fl_peer_connect, which maps
+ * the peers' buffers (IPC across processes, plain pointers for ranks in one process) and enables
+ * peer access across devices.  Ranks sharing one device must run on disjoint SM partitions
+ * (sm_count), because the aggregation kernel of one rank waits on the device for its peers';
+ * FL_ERR_INVALID otherwise.  Such a process should run with CUDA_MODULE_LOADING=EAGER (a lazily
+ * loaded kernel variant can stall behind a spinning peer) and CUDA_DEVICE_MAX_CONNECTIONS=32 (the
+ * ranks' streams otherwise share 8 hardware queues and serialise).  fl_peer_export needs the largest cohort size this rank will
+ * aggregate as a server (max_clients, for the unaggregated receive buffer; ignored elsewhere).
+ * Collective in effect: a round's fl_aggregate completes only when every rank ran its own. */
+#define FL_PEER_BLOB_BYTES 512
+fl_status fl_peer_export(fl_ctx* ctx, int64_t max_clients, uint8_t* out_blob);
+fl_status fl_peer_connect(fl_ctx* ctx, const uint8_t* blobs, int32_t world_size);
 
 /* The cudaStream_t the ctx launches on (for the caller's event timing). */
 void* fl_get_stream(fl_ctx* ctx);

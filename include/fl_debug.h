@@ -9,6 +9,8 @@
  *   "p1" f32 [S][H1][W1][C1]  "am1" u8 same   "p2" f32 [S][H2][W2][C2]  "am2" u8 same
  *   "h" / "dh" f32 [S][HID]   "dp2" f32 [S][F] "dY2" f32 [S][H1][W1][C2]
  *   "dp1" f32 [S][H1][W1][C1] "dY1" f32 [S][H0][W0][C1]
+ * "sig" (any model): the ctx's peer signal words uint64 [(8 + 1)·T] (ready[8][T], done[T]),
+ * copied without waiting for the ctx stream (to inspect a peer aggregation in flight).
  * bytes is the caller's buffer size; copies min(bytes, buffer size).  Synchronous.
  * FL_ERR_INVALID for an unknown name or a non-CNN context.
  */

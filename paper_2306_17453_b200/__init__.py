@@ -24,14 +24,16 @@ STATUS = {0: "FL_OK", 1: "FL_ERR_INVALID", 2: "FL_ERR_STATE", 3: "FL_ERR_OOM", 4
           6: "FL_ERR_EMPTY", 7: "FL_ERR_UNSUPPORTED"}
 MODEL = {"logreg": 0, "cnn": 1, "speech": 2, "lstm": 3}
 POLICY = {"bu": 0, "lb": 1, "rr": 2, "srr": 3, "lb_gpu": 4}
-ABI_VERSION = 2
+ABI_VERSION = 3
+AGG_MODE = {"nccl": 0, "peer": 1, "unaggregated": 2}
+PEER_BLOB_BYTES = 512
 
 # Symbols include/fl.h declares (checked by tests/test_abi.py).
 EXPORTS = ["fl_abi_version", "fl_n_params", "fl_place_plan", "fl_pack_plan", "fl_nccl_unique_id", "fl_round_init",
            "fl_place", "fl_train_clients", "fl_aggregate", "fl_round", "fl_fedavg_vectors", "fl_get_local_plan",
            "fl_get_client_params", "fl_get_global_params", "fl_set_global_params", "fl_get_stats",
            "fl_set_profiling", "fl_get_kernel_stats", "fl_get_stream", "fl_last_error", "fl_round_destroy", "fl_debug_read",
-           "fl_lb_fit", "fl_set_timing_records", "fl_get_client_times"]
+           "fl_lb_fit", "fl_set_timing_records", "fl_get_client_times", "fl_peer_export", "fl_peer_connect"]
 
 
 class FLError(RuntimeError):
@@ -44,7 +46,8 @@ class fl_config(C.Structure):
     _fields_ = [("abi_version", C.c_uint32), ("model", C.c_int32), ("batch_size", C.c_int32),
                 ("local_epochs", C.c_int32), ("lr", C.c_float), ("shuffle", C.c_int32), ("seed", C.c_uint64),
                 ("min_samples", C.c_int64), ("rank", C.c_int32), ("world_size", C.c_int32), ("device", C.c_int32),
-                ("nccl_unique_id", C.c_void_p), ("math", C.c_int32), ("stream", C.c_void_p)]
+                ("nccl_unique_id", C.c_void_p), ("math", C.c_int32), ("stream", C.c_void_p),
+                ("sm_count", C.c_int32), ("agg_mode", C.c_int32)]
 
 
 class fl_population(C.Structure):
@@ -59,7 +62,8 @@ class fl_round_stats(C.Structure):
                 ("samples_total", C.c_int64), ("samples_local", C.c_int64), ("steps_local", C.c_int64),
                 ("waves", C.c_int64), ("h2d_bytes", C.c_int64), ("kernels", C.c_int64),
                 ("train_end_ms", C.c_double), ("round_ms_max", C.c_double), ("train_end_ms_min", C.c_double),
-                ("train_end_ms_max", C.c_double), ("timedelta_ms", C.c_double)]
+                ("train_end_ms_max", C.c_double), ("timedelta_ms", C.c_double), ("xfer_bytes", C.c_int64),
+                ("sm_count", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -109,6 +113,8 @@ def lib():
             "fl_lb_fit": (C.c_int, [vp, vp, i64, vp, vp, vp]),
             "fl_set_timing_records": (C.c_int, [vp, i32]),
             "fl_get_client_times": (C.c_int, [vp, vp, vp, vp, vp]),
+            "fl_peer_export": (C.c_int, [vp, i64, vp]),
+            "fl_peer_connect": (C.c_int, [vp, vp, i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -198,6 +204,8 @@ class Config:
     nccl_unique_id: bytes | None = None
     math: int = 0
     stream: int | None = None
+    sm_count: int = 0      # green-context SM partition (include/fl.h): 0 whole GPU, s>0 first part, s<0 remainder
+    agg_mode: str = "nccl"  # "nccl" | "peer" | "unaggregated" (include/fl.h fl_agg_mode)
 
 
 class Ctx:
@@ -213,7 +221,8 @@ class Ctx:
             self._keep.append(uid)
         c = fl_config(ABI_VERSION, MODEL[cfg.model], cfg.batch_size, cfg.local_epochs, cfg.lr, cfg.shuffle,
                       cfg.seed & 0xFFFFFFFFFFFFFFFF, cfg.min_samples, cfg.rank, cfg.world_size, cfg.device,
-                      C.addressof(uid) if uid is not None else None, cfg.math, cfg.stream)
+                      C.addressof(uid) if uid is not None else None, cfg.math, cfg.stream, cfg.sm_count,
+                      AGG_MODE[cfg.agg_mode])
         n_samples = _i64(n_samples)
         if on_device is None:
             on_device = not isinstance(x, np.ndarray)
@@ -333,6 +342,19 @@ class Ctx:
         self._check(lib().fl_get_client_times(self._h, _ptr(ids), _ptr(m), _ptr(t), C.byref(n)),
                     "fl_get_client_times")
         return ids, m, t
+
+    def fl_peer_export(self, max_clients=0) -> bytes:
+        """This rank's peer blob (FL_PEER_BLOB_BYTES opaque bytes) for fl_peer_connect."""
+        buf = (C.c_uint8 * PEER_BLOB_BYTES)()
+        self._check(lib().fl_peer_export(self._h, int(max_clients), C.addressof(buf)), "fl_peer_export")
+        return bytes(buf)
+
+    def fl_peer_connect(self, blobs):
+        """blobs: every rank's fl_peer_export bytes, in rank order."""
+        if len(blobs) != self.cfg.world_size or any(len(b) != PEER_BLOB_BYTES for b in blobs):
+            raise FLError(FL_ERR_INVALID, "fl_peer_connect: one blob of PEER_BLOB_BYTES per rank")
+        arr = (C.c_uint8 * (PEER_BLOB_BYTES * len(blobs))).from_buffer_copy(b"".join(blobs))
+        self._check(lib().fl_peer_connect(self._h, C.addressof(arr), len(blobs)), "fl_peer_connect")
 
     def fl_get_stats(self):
         st = fl_round_stats()

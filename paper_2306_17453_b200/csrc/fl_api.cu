@@ -4,8 +4,10 @@
 // local client as waves of grouped kernels (a4-a7) -> fused fp64 accumulation (K1) ->
 // NCCL allreduce of [S ‖ N] across ranks (a9) -> finalize (K2).  PAPER.md §4.1-4.4,
 // Eq. 1-2; SURVEY.md §3.3.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <unistd.h>
 #include <nccl.h>  // types only; the library is dlopen'ed when world_size > 1
 #include <stdarg.h>
 #include <stdint.h>
@@ -173,6 +175,67 @@ cudaError_t grow_dev(T*& p, int64_t& cap, int64_t need) {
   cap = e == cudaSuccess ? n : 0;
   return e;
 }
+// Green contexts (CUDA driver API through the runtime's entry-point table, no -lcuda):
+// an SM partition of the device whose streams only run on its SMs (include/fl.h sm_count).
+template <class F>
+F drv(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return nullptr;
+  return (F)fn;
+}
+struct GreenPart {
+  CUgreenCtx g = nullptr;
+  int sms = 0;
+  CUresult (*stream_create)(CUstream*, CUgreenCtx, unsigned, int) = nullptr;
+};
+// s > 0: the first partition of >= s SMs; s < 0: the remainder after splitting off >= -s SMs
+bool green_partition(int device, int s, GreenPart* out, std::string* err) {
+  auto devGet = drv<CUresult (*)(CUdevice*, int)>("cuDeviceGet");
+  auto getRes = drv<CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType)>("cuDeviceGetDevResource");
+  auto split = drv<CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned)>(
+      "cuDevSmResourceSplitByCount");
+  auto gen = drv<CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned)>("cuDevResourceGenerateDesc");
+  auto gcreate = drv<CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned)>("cuGreenCtxCreate");
+  out->stream_create = drv<CUresult (*)(CUstream*, CUgreenCtx, unsigned, int)>("cuGreenCtxStreamCreate");
+  if (!devGet || !getRes || !split || !gen || !gcreate || !out->stream_create) {
+    *err = "driver has no green-context entry points";
+    return false;
+  }
+  CUdevice dev;
+  CUdevResource all, part, rem;
+  unsigned nb = 1;
+  CUresult r;
+  if ((r = devGet(&dev, device)) != CUDA_SUCCESS || (r = getRes(dev, &all, CU_DEV_RESOURCE_TYPE_SM)) != CUDA_SUCCESS ||
+      (r = split(&part, &nb, &all, &rem, 0, (unsigned)(s > 0 ? s : -s))) != CUDA_SUCCESS || nb != 1) {
+    *err = "cannot split the device's SMs (CUresult " + std::to_string((int)r) + ")";
+    return false;
+  }
+  CUdevResource* use = s > 0 ? &part : &rem;
+  if (use->sm.smCount == 0) {
+    *err = "empty SM partition";
+    return false;
+  }
+  CUdevResourceDesc desc;
+  if ((r = gen(&desc, use, 1)) != CUDA_SUCCESS || (r = gcreate(&out->g, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM)) != CUDA_SUCCESS) {
+    *err = "cuGreenCtxCreate failed (CUresult " + std::to_string((int)r) + ")";
+    return false;
+  }
+  out->sms = (int)use->sm.smCount;
+  return true;
+}
+
+// peer blob (include/fl.h FL_PEER_BLOB_BYTES): what a rank tells the others about its buffers
+struct PeerBlob {
+  uint64_t magic;
+  int32_t pid, device, sm_count, world, rank, T;
+  int64_t P_pad, recv_cap;
+  uint64_t ptr[4];                 // S, theta, sig, recv (valid in the exporting process)
+  cudaIpcMemHandle_t h[4];
+};
+static_assert(sizeof(PeerBlob) <= FL_PEER_BLOB_BYTES, "peer blob too large");
+constexpr uint64_t kPeerMagic = 0x464c50454552310aull;  // "FLPEER1\n"
+constexpr int64_t kPeerTile = 8192;                    // parameters per aggregation tile
 }  // namespace
 
 struct fl_ctx {
@@ -269,6 +332,24 @@ struct fl_ctx {
   cudaStream_t cst = nullptr;
   cudaStream_t pst = nullptr;  // high-priority pack stream: a pack kernel waiting for SMs never stalls the copies
   std::vector<cudaEvent_t> ev_chunk, ev_copy;
+  // SM partition (cfg.sm_count): green context whose streams run on n_sms SMs only
+  GreenPart green;
+  int n_sms = 148;
+  // peer-memory aggregation (FL_AGG_PEER / FL_AGG_UNAGGREGATED)
+  bool peer_on = false;
+  PeerArgs peer{};
+  std::vector<void*> ipc_opened;             // peer buffers mapped with cudaIpcOpenMemHandle
+  unsigned long long* d_sig = nullptr;       // [(FL_MAX_PEERS + 1) · T] signal words
+  int peer_T = 0;
+  float* d_recv = nullptr;                   // server (rank 0) receive buffer, unaggregated mode
+  int64_t recv_cap = 0;
+  int64_t* d_dst_row = nullptr;              // [K] receive row of each exec slot (unaggregated)
+  int64_t dst_cap = 0;
+  int64_t* d_nplan = nullptr;                // server: [K_total] n of each received row
+  int64_t nplan_cap = 0;
+  unsigned int* d_ctr = nullptr;             // last-CTA counters of the push / broadcast kernels
+  unsigned long long agg_seq = 0;
+  int64_t xfer_bytes = 0;
 };
 
 // ---------------------------------------------------------------- error helpers
@@ -367,6 +448,10 @@ void fl_round_destroy(fl_ctx* c) {
                   c->lb.dX, c->lb.E, c->lb.dE, c->lb.dhT};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  void* pptrs[] = {c->d_sig, c->d_recv, c->d_dst_row, c->d_nplan, c->d_ctr};
+  for (void* p : pptrs)
+    if (p) cudaFree(p);
   for (int i = 0; i < 2; ++i)
     if (c->h_tab[i]) cudaFreeHost(c->h_tab[i]);
   if (c->h_rstat) cudaFreeHost(c->h_rstat);
@@ -390,6 +475,10 @@ void fl_round_destroy(fl_ctx* c) {
   if (c->cst) cudaStreamDestroy(c->cst);
   if (c->pst) cudaStreamDestroy(c->pst);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+  if (c->green.g) {
+    auto gdestroy = drv<CUresult (*)(CUgreenCtx)>("cuGreenCtxDestroy");
+    if (gdestroy) gdestroy(c->green.g);
+  }
   delete c;
 }
 
@@ -400,7 +489,11 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   if (cfg->abi_version != FL_ABI_VERSION) return FL_ERR_INVALID;
   if (cfg->batch_size < 1 || cfg->local_epochs < 1 || !(cfg->lr >= 0.f) || cfg->min_samples < 1) return FL_ERR_INVALID;
   if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) return FL_ERR_INVALID;
-  if (cfg->world_size > 1 && !cfg->nccl_unique_id) return FL_ERR_INVALID;  // world 1 + id: 1-rank comm
+  if (cfg->agg_mode < FL_AGG_NCCL || cfg->agg_mode > FL_AGG_UNAGGREGATED) return FL_ERR_INVALID;
+  if (cfg->world_size > FL_MAX_PEERS && cfg->agg_mode != FL_AGG_NCCL) return FL_ERR_INVALID;
+  // NCCL aggregation across ranks needs the communicator's id (world 1 + id: a 1-rank comm)
+  if (cfg->world_size > 1 && cfg->agg_mode == FL_AGG_NCCL && !cfg->nccl_unique_id) return FL_ERR_INVALID;
+  if (cfg->sm_count != 0 && cfg->stream) return FL_ERR_INVALID;  // a borrowed stream cannot be partitioned
   if (fl_n_params(cfg->model) == 0) return FL_ERR_INVALID;
   if (n_params != fl_n_params(cfg->model)) return FL_ERR_INVALID;
   if (!model_supported(cfg->model)) return FL_ERR_UNSUPPORTED;
@@ -437,9 +530,25 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   CK(cudaGetDeviceProperties(&prop, cfg->device));
   if (prop.major != 10) return set_err(c, FL_ERR_CUDA, "device %s is sm_%d%d; this build targets sm_100a", prop.name,
                                        prop.major, prop.minor);
+  c->n_sms = prop.multiProcessorCount;
+  if (cfg->sm_count != 0) {
+    std::string why;
+    if (!green_partition(cfg->device, cfg->sm_count, &c->green, &why))
+      return set_err(c, FL_ERR_CUDA, "sm_count %d: %s", cfg->sm_count, why.c_str());
+    c->n_sms = c->green.sms;
+  }
+  // every stream of the ctx lives in its SM partition (a green-context stream) when one is set
+  auto make_stream = [&](cudaStream_t* s, int prio) -> cudaError_t {
+    if (c->green.g)
+      return c->green.stream_create((CUstream*)s, c->green.g, CU_STREAM_NON_BLOCKING, prio) == CUDA_SUCCESS
+                 ? cudaSuccess
+                 : cudaErrorInvalidResourceHandle;
+    return cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, prio);
+  };
+  c->solo_sms = c->n_sms;
   if (cfg->stream) c->st = (cudaStream_t)cfg->stream;
   else {
-    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    CK(make_stream(&c->st, 0));
     c->own_stream = true;
   }
   cudaEvent_t* evs[] = {&c->ev_entry, &c->ev_start, &c->ev_staged, &c->ev_trained, &c->ev_agg0,
@@ -447,8 +556,9 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   for (cudaEvent_t* e : evs) CK(cudaEventCreate(e));
   if (const char* ng = getenv("FL_GROUPS")) c->ngroups = std::max(1, atoi(ng));
   if (const char* ns = getenv("FL_SOLO")) c->nsolo = std::max(0, atoi(ns));
-  if (const char* ss = getenv("FL_SOLO_SMS")) c->solo_sms = std::max(8, std::min(148, atoi(ss)));
+  if (const char* ss = getenv("FL_SOLO_SMS")) c->solo_sms = std::max(8, std::min(c->n_sms, atoi(ss)));
   if (const char* rs = getenv("FL_RESERVE_SMS")) c->reserve_sms = std::max(0, std::min(120, atoi(rs)));
+  c->reserve_sms = c->reserve_sms * c->n_sms / 148;  // the same share of a smaller partition
   c->nsolo = std::min(c->nsolo, std::max(0, 8 - c->ngroups));
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   const int nstreams = c->nsolo + c->ngroups;
@@ -458,12 +568,12 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   for (int g = 0; g < nstreams; ++g) {
     const bool hi = g < c->nsolo;  // the critical-path (solo) streams run at high priority
-    CK(cudaStreamCreateWithPriority(&c->gstream[(size_t)g], cudaStreamNonBlocking, hi ? prio_hi : prio_lo));
+    CK(make_stream(&c->gstream[(size_t)g], hi ? prio_hi : prio_lo));
     CK(cudaEventCreateWithFlags(&c->ev_join[(size_t)g], cudaEventDisableTiming));
   }
   if (!c->pop_dev) {
-    CK(cudaStreamCreateWithFlags(&c->cst, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithPriority(&c->pst, cudaStreamNonBlocking, prio_hi));
+    CK(make_stream(&c->cst, 0));
+    CK(make_stream(&c->pst, prio_hi));
     // borrowed host population: pin it so per-round staging copies run at full PCIe rate
     size_t xb = (size_t)c->pop_off.back() * (size_t)c->L.D_in * sizeof(float);
     if (cudaHostRegister((void*)c->x, xb, cudaHostRegisterReadOnly) == cudaSuccess) c->host_registered = true;
@@ -476,6 +586,11 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   CK(cudaMalloc(&c->d_S, sizeof(double) * (Pp + 1)));
   CK(cudaMallocHost(&c->h_rstat, sizeof(double) * 2 * cfg->world_size));
   CK(cudaMalloc(&c->d_rstat, sizeof(double) * (2 + 2 * cfg->world_size)));
+  c->peer_T = (int)((Pp + kPeerTile - 1) / kPeerTile);
+  CK(cudaMalloc(&c->d_sig, sizeof(unsigned long long) * (FL_MAX_PEERS + 1) * c->peer_T));
+  CK(cudaMemset(c->d_sig, 0, sizeof(unsigned long long) * (FL_MAX_PEERS + 1) * c->peer_T));
+  CK(cudaMalloc(&c->d_ctr, sizeof(unsigned int) * 2));
+  CK(cudaMemset(c->d_ctr, 0, sizeof(unsigned int) * 2));
   CK(cudaMemcpyAsync(c->d_canon_of, c->L.canon_of.data(), sizeof(int64_t) * Pp, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(c->d_canon, global_params, sizeof(float) * P, cudaMemcpyHostToDevice, c->st));
   canon_to_internal(c->d_canon, c->d_canon_of, Pp, c->d_theta, c->st);
@@ -951,7 +1066,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
           WaveArgs wa{ws.A[(size_t)k], (int)B, t == 0, ws.d_sidx + ws.slot_off[(size_t)k],
                       ws.d_bs + ws.bs_off[(size_t)k], c->cfg.lr, sum_bs, &c->prof, c->cfg.math == 0,
                       ws.gn[(size_t)g], true, ws.d_bpre + ws.bs_off[(size_t)k] + k,
-                      (ws.gsolo[(size_t)g] || c->reserve_sms == 0) ? c->solo_sms : 148 - c->reserve_sms};
+                      (ws.gsolo[(size_t)g] || c->reserve_sms == 0) ? c->solo_sms : c->n_sms - c->reserve_sms};
           int nl = cnn_wave_simt(L, wa, c->d_xpack, c->d_ypack, c->d_theta, c->d_slots + base * L.P_pad,
                                  gv[(size_t)g], gst[(size_t)g]);
           if (nl < 0)
@@ -976,7 +1091,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
         int64_t sum_bs = 0;
         for (int32_t a = 0; a < ws.A[(size_t)k]; ++a) sum_bs += h_bs[ws.bs_off[(size_t)k] + a];
         WaveArgs wa{ws.A[(size_t)k], (int)B, k == 0, ws.d_sidx + ws.slot_off[(size_t)k], ws.d_bs + ws.bs_off[(size_t)k],
-                    c->cfg.lr, sum_bs, &c->prof, true, K, true, ws.d_bpre + ws.bs_off[(size_t)k] + k, 148};
+                    c->cfg.lr, sum_bs, &c->prof, true, K, true, ws.d_bpre + ws.bs_off[(size_t)k] + k, c->n_sms};
         c->prof.begin(st);
         const int nl = lstm_wave(L, wa, reinterpret_cast<const uint8_t*>(c->d_xpack), c->d_ypack, c->d_theta,
                                  c->d_slots, c->lb, st);
@@ -1017,7 +1132,61 @@ fl_status fl_aggregate(fl_ctx* c, float* out_params, int64_t* out_total_samples)
   int64_t n = 0;
   c->prof.begin(st);
   const double agg_bytes = 4.0 * (double)Pp * (double)(K + 1) + (c->comm ? 8.0 : 4.0) * (double)Pp;
-  if (!c->comm) {
+  const int W = c->cfg.world_size;
+  const int mode = c->cfg.agg_mode;
+  if (mode != FL_AGG_NCCL && W > 1 && !c->peer_on)
+    return set_err(c, FL_ERR_STATE, "agg_mode %d needs fl_peer_connect first", mode);
+  c->xfer_bytes = 0;
+  if (c->peer_on && mode == FL_AGG_PEER) {
+    // one cooperative kernel: partial, reduce-scatter over peer memory, finalize, all-gather
+    PeerArgs a = c->peer;
+    a.slots = c->d_slots, a.stride = Pp, a.n = c->d_n, a.K = (int)K, a.N = (double)c->N_total;
+    a.seq = ++c->agg_seq;
+    CK(cudaEventRecord(c->ev_acc1, st));
+    CK(cudaEventRecord(c->ev_ar0, st));
+    if (fedavg_peer(a, c->n_sms, st) < 0) return set_err(c, FL_ERR_CUDA, "k_fedavg_peer launch failed");
+    ++n;
+    CKL();
+    CK(cudaEventRecord(c->ev_ar1, st));
+    c->prof.end(K_FEDAVG, 3.0 * (double)Pp * K, agg_bytes, st);
+    const int64_t t0 = peer_slice_begin(a.me, a.T, W), t1 = peer_slice_begin(a.me + 1, a.T, W);
+    const int64_t slice = std::min<int64_t>(Pp, t1 * kPeerTile) - std::min<int64_t>(Pp, t0 * kPeerTile);
+    c->xfer_bytes = (int64_t)(W - 1) * slice * 12;  // pull 8 B of every peer's S, push 4 B of θ_new
+  } else if (c->peer_on && mode == FL_AGG_UNAGGREGATED) {
+    // the ablation: every client model to the server (rank 0), which averages all of them
+    const int r = c->cfg.rank;
+    const int64_t Kt = c->K_total;
+    if (c->peer.r[0].recv == nullptr || Kt > c->recv_cap)
+      return set_err(c, FL_ERR_INVALID, "unaggregated: server receive buffer holds %lld models, cohort has %lld",
+                     (long long)c->recv_cap, (long long)Kt);
+    std::vector<int64_t> dst((size_t)K);
+    for (int64_t e = 0; e < K; ++e) dst[(size_t)e] = c->plan_off[(size_t)r] + c->exec[(size_t)e];
+    CK(grow_dev(c->d_dst_row, c->dst_cap, K));
+    if (K) CK(cudaMemcpyAsync(c->d_dst_row, dst.data(), sizeof(int64_t) * K, cudaMemcpyHostToDevice, st));
+    const unsigned long long seq = ++c->agg_seq;
+    CK(cudaEventRecord(c->ev_acc1, st));
+    CK(cudaEventRecord(c->ev_ar0, st));
+    n += unagg_push(c->d_slots, Pp, c->d_dst_row, (int)K, Pp / 4, c->peer.r[0].recv, c->peer.r[0].sig, r, seq,
+                    c->d_ctr, c->n_sms, st);
+    if (r != 0) {
+      c->xfer_bytes = K * Pp * 4;
+      n += wait_flags(c->d_sig + (int64_t)W * c->peer_T, 0, 1, 1, seq, st);  // θ_new from the server
+    } else {
+      std::vector<int64_t> np((size_t)Kt);
+      for (int64_t i = 0; i < Kt; ++i) np[(size_t)i] = c->n_samples[(size_t)c->plan_ids[(size_t)i]];
+      CK(grow_dev(c->d_nplan, c->nplan_cap, Kt));
+      CK(cudaMemcpyAsync(c->d_nplan, np.data(), sizeof(int64_t) * Kt, cudaMemcpyHostToDevice, st));
+      n += wait_flags(c->d_sig, 0, W, 1, seq, st);  // every rank's models have landed
+      n += fedavg_accum_final(c->d_recv, Pp, c->d_nplan, (int)Kt, Pp, c->d_theta, (double)c->N_total, c->d_theta, st);
+      PeerArgs a = c->peer;
+      a.seq = seq;
+      n += unagg_bcast(a, c->d_ctr + 1, c->n_sms, st);
+      c->xfer_bytes = (int64_t)(W - 1) * Pp * 4;
+    }
+    CKL();
+    CK(cudaEventRecord(c->ev_ar1, st));
+    c->prof.end(K_FEDAVG, 3.0 * (double)Pp * Kt, 4.0 * (double)Pp * (double)(Kt + 1) + 4.0 * (double)Pp, st);
+  } else if (!c->comm) {
     n += fedavg_accum_final(c->d_slots, Pp, c->d_n, (int)K, Pp, c->d_theta, (double)c->N_total, c->d_theta, st);
     CKL();
     c->prof.end(K_FEDAVG, 3.0 * (double)Pp * K, agg_bytes, st);
@@ -1037,6 +1206,7 @@ fl_status fl_aggregate(fl_ctx* c, float* out_params, int64_t* out_total_samples)
     CK(cudaEventRecord(c->ev_ar1, st));
     n += fedavg_finalize(c->d_S, Pp, c->d_theta, c->d_S + Pp, c->d_theta, st);
     CKL();
+    c->xfer_bytes = W > 1 ? (int64_t)(2.0 * (W - 1) / W * 8.0 * (double)(Pp + 1)) : 0;  // ring estimate
   }
   CK(cudaEventRecord(c->ev_end, st));
   c->kernels += n;
@@ -1099,6 +1269,8 @@ static fl_status fill_stats(fl_ctx* c, fl_round_stats* s) {
   s->waves = c->ws.n_waves;
   s->h2d_bytes = c->h2d;
   s->kernels = c->kernels;
+  s->xfer_bytes = c->xfer_bytes;
+  s->sm_count = c->n_sms;
   s->client_updates_per_s = s->round_ms_max > 0 ? (double)c->K_total / (s->round_ms_max * 1e-3) : 0.0;
   return FL_OK;
 }
@@ -1121,6 +1293,101 @@ fl_status fl_round(fl_ctx* c, const int64_t* cohort_ids, int64_t n_cohort, int32
     if (s != FL_OK) return s;
     *stats = c->stats;
   }
+  return FL_OK;
+}
+
+fl_status fl_peer_export(fl_ctx* c, int64_t max_clients, uint8_t* out_blob) {
+  if (!c || !out_blob || max_clients < 0) return FL_ERR_INVALID;
+  if (c->failed) return FL_ERR_STATE;
+  if (c->cfg.agg_mode == FL_AGG_NCCL) return set_err(c, FL_ERR_INVALID, "agg_mode is NCCL: nothing to export");
+  CK(cudaSetDevice(c->cfg.device));
+  const int64_t Pp = c->L.P_pad;
+  if (c->cfg.agg_mode == FL_AGG_UNAGGREGATED && c->cfg.rank == 0 && max_clients > c->recv_cap) {
+    if (c->d_recv) cudaFree(c->d_recv);
+    c->d_recv = nullptr;
+    c->recv_cap = 0;
+    CK(cudaMalloc(&c->d_recv, sizeof(float) * (size_t)(max_clients * Pp)));
+    c->recv_cap = max_clients;
+  }
+  PeerBlob b;
+  memset(&b, 0, sizeof b);
+  b.magic = kPeerMagic;
+  b.pid = (int32_t)getpid();
+  b.device = c->cfg.device;
+  b.sm_count = c->cfg.sm_count;
+  b.world = c->cfg.world_size;
+  b.rank = c->cfg.rank;
+  b.T = c->peer_T;
+  b.P_pad = Pp;
+  b.recv_cap = c->recv_cap;
+  void* ptrs[4] = {c->d_S, c->d_theta, c->d_sig, c->d_recv};
+  for (int i = 0; i < 4; ++i) {
+    b.ptr[i] = (uint64_t)(uintptr_t)ptrs[i];
+    if (ptrs[i]) CK(cudaIpcGetMemHandle(&b.h[i], ptrs[i]));
+  }
+  memset(out_blob, 0, FL_PEER_BLOB_BYTES);
+  memcpy(out_blob, &b, sizeof b);
+  return FL_OK;
+}
+
+fl_status fl_peer_connect(fl_ctx* c, const uint8_t* blobs, int32_t world) {
+  if (!c || !blobs) return FL_ERR_INVALID;
+  if (c->failed) return FL_ERR_STATE;
+  if (c->cfg.agg_mode == FL_AGG_NCCL) return set_err(c, FL_ERR_INVALID, "agg_mode is NCCL");
+  if (world != c->cfg.world_size) return set_err(c, FL_ERR_INVALID, "%d blobs for world_size %d", world, c->cfg.world_size);
+  if (c->peer_on) return set_err(c, FL_ERR_STATE, "already connected");
+  std::vector<PeerBlob> b((size_t)world);
+  for (int j = 0; j < world; ++j) {
+    memcpy(&b[(size_t)j], blobs + (size_t)j * FL_PEER_BLOB_BYTES, sizeof(PeerBlob));
+    const PeerBlob& x = b[(size_t)j];
+    if (x.magic != kPeerMagic || x.rank != j || x.world != world || x.T != c->peer_T || x.P_pad != c->L.P_pad)
+      return set_err(c, FL_ERR_INVALID, "peer blob %d does not match this ctx (rank, world, model)", j);
+  }
+  const int me = c->cfg.rank, pid = (int)getpid();
+  if (b[(size_t)me].pid != pid || b[(size_t)me].ptr[1] != (uint64_t)(uintptr_t)c->d_theta)
+    return set_err(c, FL_ERR_INVALID, "blob %d is not this ctx's", me);
+  for (int j = 0; j < world; ++j)
+    for (int i = j + 1; i < world; ++i)
+      if (b[(size_t)j].device == b[(size_t)i].device) {
+        // a rank's aggregation kernel waits on the device for its peers: ranks sharing a GPU
+        // must run concurrently, i.e. in one process on disjoint SM partitions
+        if (b[(size_t)j].pid != b[(size_t)i].pid || b[(size_t)j].sm_count == 0 || b[(size_t)i].sm_count == 0)
+          return set_err(c, FL_ERR_INVALID, "ranks %d and %d share device %d: they must be contexts of one process "
+                         "with SM partitions (sm_count)", j, i, b[(size_t)j].device);
+      }
+  CK(cudaSetDevice(c->cfg.device));
+  if (peer_preload() != 0) return set_err(c, FL_ERR_CUDA, "cannot load the peer-aggregation kernels");
+  PeerArgs a{};
+  a.W = world, a.me = me, a.T = c->peer_T, a.P4 = c->L.P_pad / 4, a.tile4 = kPeerTile / 4;
+  for (int j = 0; j < world; ++j) {
+    const PeerBlob& x = b[(size_t)j];
+    void* p[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (x.pid == pid) {
+      for (int i = 0; i < 4; ++i) p[i] = (void*)(uintptr_t)x.ptr[i];
+      if (x.device != c->cfg.device) {
+        int can = 0;
+        CK(cudaDeviceCanAccessPeer(&can, c->cfg.device, x.device));
+        if (!can) return set_err(c, FL_ERR_CUDA, "no peer access from device %d to %d", c->cfg.device, x.device);
+        cudaError_t e = cudaDeviceEnablePeerAccess(x.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+        cudaGetLastError();
+      }
+    } else {
+      for (int i = 0; i < 4; ++i) {
+        if (!x.ptr[i]) continue;
+        if (i == 3 && !(j == 0 && c->cfg.agg_mode == FL_AGG_UNAGGREGATED)) continue;
+        CK(cudaIpcOpenMemHandle(&p[i], x.h[i], cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_opened.push_back(p[i]);
+      }
+    }
+    a.r[j] = PeerRank{(double*)p[0], (float*)p[1], (unsigned long long*)p[2], (float*)p[3]};
+  }
+  if (c->cfg.agg_mode == FL_AGG_UNAGGREGATED) {
+    if (!a.r[0].recv) return set_err(c, FL_ERR_INVALID, "server (rank 0) exported no receive buffer (max_clients)");
+    c->recv_cap = b[0].recv_cap;
+  }
+  c->peer = a;
+  c->peer_on = true;
   return FL_OK;
 }
 
@@ -1258,6 +1525,13 @@ fl_status fl_set_global_params(fl_ctx* c, const float* params) {
 
 fl_status fl_debug_read(fl_ctx* c, const char* name, void* host, int64_t bytes) {
   if (!c || !name || !host || bytes < 0) return FL_ERR_INVALID;
+  if (strcmp(name, "sig") == 0) {  // peer signal words, read without synchronising the ctx stream
+    CK(cudaSetDevice(c->cfg.device));
+    CK(cudaMemcpy(host, c->d_sig,
+                  (size_t)std::min<int64_t>(bytes, sizeof(unsigned long long) * (FL_MAX_PEERS + 1) * c->peer_T),
+                  cudaMemcpyDeviceToHost));
+    return FL_OK;
+  }
   if (c->L.model != FL_MODEL_CNN_CIFAR && c->L.model != FL_MODEL_CNN_SPEECH) return FL_ERR_INVALID;
   const CnnBufs& b = c->cb;
   const CnnDims& d = c->L.d;

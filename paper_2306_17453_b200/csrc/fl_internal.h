@@ -244,6 +244,43 @@ int fedavg_accum_partial(const float* slots, int64_t stride, const int64_t* n, i
 int fedavg_finalize(const double* S, int64_t P, const float* theta_g, const double* Ndev, float* out,
                     cudaStream_t st);
 
+// ---- cross-rank aggregation over peer memory (k_peer.cu)
+constexpr int FL_MAX_PEERS = 8;
+struct PeerRank {
+  double* S;                // [P_pad] fp64 partial of that rank
+  float* theta;             // [P_pad] θ_g of that rank (internal layout)
+  unsigned long long* sig;  // [(W + 1) · T] words: ready[W][T], done[T] (round sequence numbers)
+  float* recv;              // rank 0 only: unaggregated receive buffer [max_clients][P_pad]
+};
+struct PeerArgs {
+  PeerRank r[FL_MAX_PEERS];
+  int W, me, T;             // ranks, this rank, parameter tiles
+  int64_t P4, tile4;        // P_pad / 4, float4s per tile
+  const float* slots;       // this rank's client models [K][stride]
+  int64_t stride;
+  const int64_t* n;         // [K] weights (samples)
+  int K;
+  double N;                 // Σ n over the whole cohort (every rank knows it from the plan)
+  unsigned long long seq;   // this round's sequence number (> every earlier one)
+};
+// tiles [peer_slice_begin(j), peer_slice_begin(j + 1)) are owned (reduced) by rank j
+__host__ __device__ inline int peer_slice_begin(int j, int T, int W) { return (int)(((int64_t)j * T) / W); }
+__host__ __device__ inline int peer_owner(int t, int T, int W) {
+  int j = (int)(((int64_t)t * W) / T);
+  while (j + 1 < W && peer_slice_begin(j + 1, T, W) <= t) ++j;
+  while (j > 0 && peer_slice_begin(j, T, W) > t) --j;
+  return j;
+}
+int fedavg_peer(const PeerArgs& p, int sms, cudaStream_t st);
+int peer_preload();    // load the protocol's kernels eagerly (lazy loading + spinning peers can deadlock)
+int fedavg_preload();
+int unagg_push(const float* slots, int64_t stride, const int64_t* dst_row, int K, int64_t P4, float* recv,
+               unsigned long long* server_sig, int me, unsigned long long seq, unsigned int* done_ctr, int sms,
+               cudaStream_t st);
+int wait_flags(const unsigned long long* sig, int j0, int j1, int64_t stride, unsigned long long seq,
+               cudaStream_t st);
+int unagg_bcast(const PeerArgs& p, unsigned int* done_ctr, int sms, cudaStream_t st);
+
 // ---------------------------------------------------------------- char-LSTM (k_lstm.cu)
 // Per-slot activations of one wave (slot s = a*B + r; B must be 4): input projections xp,
 // post-activation gates G0/G1, cell/hidden states C/H [T+1] (index 0 = zero state), gate

@@ -118,6 +118,15 @@ int fedavg_accum_partial(const float* slots, int64_t stride, const int64_t* n, i
   return 1;
 }
 
+int fedavg_preload() {
+  cudaFuncAttributes a;
+  const void* ks[] = {(const void*)k_fedavg4<true>, (const void*)k_fedavg4<false>, (const void*)k_fedavg1<true>,
+                      (const void*)k_fedavg1<false>};
+  for (const void* k : ks)
+    if (cudaFuncGetAttributes(&a, k) != cudaSuccess) return -1;
+  return 0;
+}
+
 // K2 after the cross-GPU reduce: θ_new = fp32_rn(θ_g + S/N), N = S[P] (exact in fp64).
 __global__ void k_finalize(const double* __restrict__ S, int64_t P, const float* theta_g, const double* Ndev,
                            float* out) {

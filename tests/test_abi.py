@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version_and_param_counts():
-    assert fl.fl_abi_version() == fl.ABI_VERSION == 2
+    assert fl.fl_abi_version() == fl.ABI_VERSION == 3
     for m in ["logreg", "cnn", "speech", "lstm"]:
         assert fl.fl_n_params(m) == oracle.n_params(m)
     assert fl.fl_n_params(17) == 0
