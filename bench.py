@@ -53,10 +53,10 @@ def workload(world: int, name: str | None):
     return wl, desc, ("strong" if world > 1 else "weak")
 
 
-def run_config(wl, desc, cohort, sizes, world):
+def run_config(wl, desc, cohort, sizes, world, agg="nccl"):
     """The `config` object of both arms' JSON lines (identical for ours and --impl reference)."""
     return {"workload": desc, "clients": int(len(cohort)), "samples": int(sizes.sum()), "B": wl.B, "E": wl.E,
-            "lr": wl.lr, "parallelism": f"clients x{world}",
+            "lr": wl.lr, "parallelism": f"clients x{world}", "aggregation": agg,
             "l2": "per-round working set >> 126 MB L2 (no flush needed)"}
 
 
@@ -326,7 +326,7 @@ def run_reference(args, world, rank):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8d laws)",
-            "config": run_config(wl, desc, cohort, sizes, world),
+            "config": run_config(wl, desc, cohort, sizes, world, args.agg),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[-1]["cores"], "kind": "oracle",
                              "sample": vals[-1]["sample"] + f"; median of {args.steps} such samples"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -334,6 +334,18 @@ def run_reference(args, world, rank):
             "note": "each step trains a bounded random sample of the cohort's clients on the host cores and "
                     "converts samples/s to client-updates/s; ms_per_step is the implied whole-round time"}
     print(json.dumps(line), flush=True)
+
+
+def peer_connect(ctx, world, max_clients):
+    """Exchange the ranks' peer blobs (CUDA IPC handles) over torch.distributed and connect."""
+    blob = ctx.fl_peer_export(max_clients if ctx.cfg.rank == 0 else 0)
+    if world == 1:
+        ctx.fl_peer_connect([blob])
+        return
+    import torch.distributed as dist
+    blobs = [None] * world
+    dist.all_gather_object(blobs, blob)
+    ctx.fl_peer_connect(blobs)
 
 
 def timed_rounds(ctx, cohort, steps, rnd, world, stream, clk=None):
@@ -373,6 +385,9 @@ def main():
     ap.add_argument("--no-c2", action="store_true", help="skip the configs[1] (C2) measurement at N = 1")
     ap.add_argument("--cpu-samples", type=int, default=400)
     ap.add_argument("--ref-samples", type=int, default=200)
+    ap.add_argument("--agg", default="nccl", choices=["nccl", "peer", "unaggregated"],
+                    help="cross-rank aggregation (include/fl.h agg_mode): NCCL allreduce of partials, one "
+                         "peer-memory kernel, or the unaggregated ablation (all client models to rank 0)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup()
@@ -387,16 +402,19 @@ def main():
     sizes, x, y, cohort = pop_for(wl)
     theta = synth.init_params(wl.model)
     uid = None
-    if world > 1:
+    if world > 1 and args.agg == "nccl":
         import torch.distributed as dist
         obj = [fl.fl_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     cfg = fl.Config(model=wl.model, batch_size=wl.B, local_epochs=wl.E, lr=wl.lr, shuffle=wl.shuffle, seed=wl.seed,
-                    rank=rank, world_size=world, device=local, nccl_unique_id=uid, math=args.math)
+                    rank=rank, world_size=world, device=local, nccl_unique_id=uid, math=args.math,
+                    agg_mode=args.agg)
     xd = torch.from_numpy(x).cuda()
     yd = torch.from_numpy(y).cuda()
     ctx = fl.fl_round_init(cfg, sizes, xd, yd, theta)
+    if args.agg != "nccl":
+        peer_connect(ctx, world, len(cohort))
     stream = torch.cuda.ExternalStream(ctx.stream)
     rnd = 0
     for _ in range(args.warmup):
@@ -425,6 +443,8 @@ def main():
     e2e = None
     if not args.no_e2e:
         ctx2 = fl.fl_round_init(cfg, sizes, x, y, theta, on_device=False)
+        if args.agg != "nccl":
+            peer_connect(ctx2, world, len(cohort))
         for _ in range(2):
             ctx2.fl_place(cohort)
             ctx2.fl_train_clients(0)
@@ -476,11 +496,11 @@ def main():
                 "precision_note": "tensor-core GEMM operands tf32, fp32 accumulate; fp32 master weights, SGD, "
                                   "softmax-CE; fp64 FedAvg accumulation",
                 "data": "synthetic (seeded, SURVEY §8d laws), device-resident",
-                "config": run_config(wl, desc, cohort, sizes, world),
+                "config": run_config(wl, desc, cohort, sizes, world, args.agg),
                 "round_stats": {k: st[k] for k in ["round_ms", "round_ms_max", "place_ms", "stage_ms", "train_ms",
                                                    "train_end_ms_min", "train_end_ms_max", "timedelta_ms",
                                                    "agg_ms", "allreduce_ms", "waves", "steps_local",
-                                                   "clients_local", "kernels"]},
+                                                   "clients_local", "kernels", "xfer_bytes", "sm_count"]},
                 "kernels": kernel_table(kstats, args.math),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "c2": c2,
                 "gpu_launches": int(st["kernels"]) * args.steps}
