@@ -67,7 +67,9 @@ def two_ranks(mode):
     return {"agg_ms_rank": [float(np.median([s["agg_ms"] for s in per[i]])) for i in range(2)],
             "xfer_bytes_rank": [int(per[i][-1]["xfer_bytes"]) for i in range(2)],
             "clients_rank": [int(per[i][-1]["clients_local"]) for i in range(2)],
-            "round_ms_max": float(np.median([max(per[0][k]["round_ms"], per[1][k]["round_ms"]) for k in range(ROUNDS)]))}
+            "round_ms_max": float(np.median([max(per[0][k]["round_ms"], per[1][k]["round_ms"]) for k in range(ROUNDS)])),
+            # a rank's agg_ms includes waiting for the slower rank; the later rank's is the step itself
+            "agg_after_last_train_ms": float(min(np.median([s["agg_ms"] for s in per[i]]) for i in range(2)))}
 
 
 res = {"workload": f"{CLIENTS} C3-law CIFAR clients, E=1, two ranks on 74+74 SMs of one B200; "
