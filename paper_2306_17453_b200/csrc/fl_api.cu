@@ -660,6 +660,11 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   c->exec.resize((size_t)K);
   std::iota(c->exec.begin(), c->exec.end(), 0);
   auto nb = [&](int64_t i) { return (c->n_samples[(size_t)c->local_ids[(size_t)i]] + B - 1) / B; };
+  // Slot pitch: rows reserved per active client in a wave's activation buffers.  The CNN
+  // tensor-core kernels take a client's batch as 32 MMA rows, so a smaller batch (the speech
+  // model's B = 20) rides in 32-row slots whose rows >= |b| are padding (sidx = -1).
+  const bool cnn_tc = (L.model == FL_MODEL_CNN_CIFAR || L.model == FL_MODEL_CNN_SPEECH) && c->cfg.math == 0;
+  const int64_t Bp = (cnn_tc && B < 32) ? 32 : B;
   std::stable_sort(c->exec.begin(), c->exec.end(), [&](int64_t a, int64_t b) { return nb(a) > nb(b); });
   // Groups = concurrent streams. The NS longest clients (the round's critical path) each get
   // a group of their own on a high-priority stream; the rest of the longest-first order is
@@ -750,7 +755,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       int32_t A = 0;
       while (A < n_g && c->steps_exec[(size_t)(b0 + A)] > t) ++A;  // prefix property within the group
       ws.A.push_back(A);
-      ws.slot_off.push_back(ws.slot_off.back() + (int64_t)A * B);
+      ws.slot_off.push_back(ws.slot_off.back() + (int64_t)A * Bp);
       ws.bs_off.push_back(ws.bs_off.back() + A);
     }
   }
@@ -801,11 +806,11 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
         else std::iota(perm.begin(), perm.end(), 0);
         for (int64_t j = 0; j < m; ++j) {
           const int64_t k = ws.gw0[(size_t)g] + ep * m + j;  // flat wave of this step
-          int32_t* srow = h_sidx + ws.slot_off[(size_t)k] + el * B;
+          int32_t* srow = h_sidx + ws.slot_off[(size_t)k] + el * Bp;
           int32_t bsz = 0;
-          for (int64_t r = 0; r < B; ++r) {
+          for (int64_t r = 0; r < Bp; ++r) {
             const int64_t i = j * B + r;
-            if (i < n) {
+            if (r < B && i < n) {
               srow[r] = (int32_t)prow(e, perm[(size_t)i]);
               ++bsz;
             } else {
@@ -857,8 +862,8 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   if (cnn && K > 0) {
     CnnBufs& b = c->cb;
     const CnnDims& d = L.d;
-    b.nch = (int)std::min<int64_t>(8, B);
-    const int64_t S = (int64_t)K * B;  // wave 0 has every local client active
+    b.nch = (int)std::min<int64_t>(8, Bp);
+    const int64_t S = (int64_t)K * Bp;  // wave 0 has every local client active
     if (S > c->cb_slots_cap) {
       void* old[] = {b.a1, b.p1, b.a2, b.p2, b.h, b.dh, b.am1, b.am2, b.dp2, b.dY2, b.dp1, b.dY1, b.dz};
       for (void* p : old)
@@ -1041,7 +1046,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
           gst[(size_t)g] = c->gstream[(size_t)ws.gstream[(size_t)g]];
           CK(cudaStreamWaitEvent(gst[(size_t)g], c->ev_fork, 0));
         }
-        gv[(size_t)g] = cnn_group_view(c->cb, L.d, (int)B, ws.gbase[(size_t)g], ws.gn[(size_t)g], g, c->part_group_z,
+        gv[(size_t)g] = cnn_group_view(c->cb, L.d, (int)Bp, ws.gbase[(size_t)g], ws.gn[(size_t)g], g, c->part_group_z,
                                        conv2_dw_tc_z_floats(), (int64_t)L.d.C1 * (25 * L.d.cpad + 1));
         max_w = std::max(max_w, ws.gnw[(size_t)g]);
       }
@@ -1063,7 +1068,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
           const int64_t k = ws.gw0[(size_t)g] + t, base = ws.gbase[(size_t)g];
           int64_t sum_bs = 0;
           for (int32_t a = 0; a < ws.A[(size_t)k]; ++a) sum_bs += h_bs[ws.bs_off[(size_t)k] + a];
-          WaveArgs wa{ws.A[(size_t)k], (int)B, t == 0, ws.d_sidx + ws.slot_off[(size_t)k],
+          WaveArgs wa{ws.A[(size_t)k], (int)Bp, t == 0, ws.d_sidx + ws.slot_off[(size_t)k],
                       ws.d_bs + ws.bs_off[(size_t)k], c->cfg.lr, sum_bs, &c->prof, c->cfg.math == 0,
                       ws.gn[(size_t)g], true, ws.d_bpre + ws.bs_off[(size_t)k] + k,
                       (ws.gsolo[(size_t)g] || c->reserve_sms == 0) ? c->solo_sms : c->n_sms - c->reserve_sms};

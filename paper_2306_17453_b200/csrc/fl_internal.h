@@ -199,6 +199,7 @@ bool tmap_encode(struct CUtensorMap_st* m, const void* base, int rank, const uin
 bool conv_tc_supported(const Layout& L);
 int conv2_dw_tc(const Layout& L, const WaveArgs& wa, const float* p1, const float* dY2, int64_t slots, float* part,
                 int64_t part_cap, int* g_out, cudaStream_t st);
+int conv2_dw_kps(const Layout& L);  // conv2 dW k-blocks (32 pixels: 2 rows x 16 columns) per sample
 int conv2_dw_reduce_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wsrc_stride, float* dst,
                        const float* part, int G, cudaStream_t st);
 int64_t conv2_dw_tc_part_z(int64_t max_clients);

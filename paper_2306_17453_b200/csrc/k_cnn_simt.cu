@@ -316,6 +316,127 @@ __global__ void k_unpool(const float* __restrict__ dp, const float* __restrict__
   }
 }
 
+// conv1 forward of a 1-channel input (the speech model) fused with bias + ReLU + 2x2 max-pool
+// (+ argmax, first maximum in row-major window order, reading A13): one block per active
+// sample, the zero-padded plane and the client's 32x25 filter in shared memory, thread =
+// (channel c = tid % 32, pooled cells q = tid / 32 + 8j); the pre-pool map is never stored.
+__global__ void __launch_bounds__(256) k_c1fwd_pool_1ch(const float* __restrict__ xpack,
+                                                        const int32_t* __restrict__ sidx,
+                                                        const int32_t* __restrict__ bs, int B, int H0, int W0, WSrc w,
+                                                        int64_t o_w, int64_t o_b, float* __restrict__ p1,
+                                                        uint8_t* __restrict__ am1) {
+  pdl_wait();
+  extern __shared__ float xs[];  // [(H0 + 4)][(W0 + 4)] then ws [32][25], wb [32]
+  const int s = blockIdx.x, z = s / B, r = s - z * B;
+  if (r >= bs[z]) return;
+  const int H1 = H0 / 2, W1 = W0 / 2, PW = W0 + 4, NP = (H0 + 4) * PW;
+  float* ws = xs + NP;
+  float* wb = ws + 32 * 25;
+  const float* xr = xpack + (int64_t)sidx[s] * H0 * W0;
+  for (int e = threadIdx.x; e < NP; e += blockDim.x) {
+    const int yy = e / PW - 2, xx = e % PW - 2;
+    xs[e] = (yy >= 0 && yy < H0 && xx >= 0 && xx < W0) ? xr[yy * W0 + xx] : 0.f;
+  }
+  for (int e = threadIdx.x; e < 32 * 25; e += blockDim.x) ws[e] = *w.at(z, o_w + e);
+  if (threadIdx.x < 32) wb[threadIdx.x] = *w.at(z, o_b + threadIdx.x);
+  __syncthreads();
+  const int c = threadIdx.x & 31;
+  float wr[25];
+#pragma unroll
+  for (int t = 0; t < 25; ++t) wr[t] = ws[c * 25 + t];
+  const float bias = wb[c];
+  for (int q = threadIdx.x >> 5; q < H1 * W1; q += 8) {
+    const int y0 = 2 * (q / W1), x0 = 2 * (q % W1);
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float* xp = xs + (y0 + (u >> 1)) * PW + x0 + (u & 1);
+      float a = bias;
+#pragma unroll
+      for (int kh = 0; kh < 5; ++kh)
+#pragma unroll
+        for (int kw = 0; kw < 5; ++kw) a = fmaf(wr[kh * 5 + kw], xp[kh * PW + kw], a);
+      v[u] = a;
+    }
+    float bv = v[0];
+    int bi = 0;
+#pragma unroll
+    for (int u = 1; u < 4; ++u)
+      if (v[u] > bv) { bv = v[u]; bi = u; }
+    const int64_t o = ((int64_t)s * H1 * W1 + q) * 32 + c;
+    p1[o] = bv > 0.f ? bv : 0.f;
+    am1[o] = (uint8_t)bi;
+  }
+}
+
+// conv1 dW of a 1-channel input (the speech model) straight from the pooled gradient: pool1's
+// backward routes each pooled cell's (ReLU'-masked) gradient g = dp1m[s][ph][pw][c] to ONE pixel
+// (y, x) of its window (the argmax am1), so dW1[c][kh][kw] = Σ g · x[y+kh-2][x+kw-2] and
+// db1[c] = Σ g over the pooled cells: a quarter of the dense dY1 work and dY1 never exists.
+// Block (chunk ch, client a) = samples [ch·rpc, ch·rpc + rpc) of a's batch; thread = (channel
+// c = tid % 32, cell group tid / 32); the 16 groups are summed in fixed order.  Writes the
+// chunk's partial [32 c][26] (25 taps + bias) in k_dw_reduce_sgd's [A·nch] chunk layout.
+__global__ void __launch_bounds__(512) k_c1dw_pooled(const float* __restrict__ dp1m, const uint8_t* __restrict__ am1,
+                                                     const float* __restrict__ xpack, const int32_t* __restrict__ sidx,
+                                                     const int32_t* __restrict__ bs, int B, int H0, int W0, int nch,
+                                                     int rpc, float* __restrict__ part) {
+  constexpr int NG = 16, U = 8;  // cell groups (512 threads / 32 channels); cells whose loads are in flight together
+  pdl_wait();
+  extern __shared__ float xs[];  // [(H0 + 4)][(W0 + 4)] zero-padded input plane; later [NG][32][26] partials
+  const int a = blockIdx.y, ch = blockIdx.x, c = threadIdx.x & 31, gq = threadIdx.x >> 5;
+  const int r0 = ch * rpc, r1 = min(r0 + rpc, bs[a]);
+  const int H1 = H0 / 2, W1 = W0 / 2, NQ = H1 * W1, PW = W0 + 4, NP = (H0 + 4) * PW;
+  float acc[26];
+#pragma unroll
+  for (int j = 0; j < 26; ++j) acc[j] = 0.f;
+  for (int r = r0; r < r1; ++r) {
+    const int64_t s = (int64_t)a * B + r;
+    const float* xr = xpack + (int64_t)sidx[s] * H0 * W0;
+    __syncthreads();  // the previous sample's plane is no longer read
+    for (int e = threadIdx.x; e < NP; e += blockDim.x) {
+      const int yy = e / PW - 2, xx = e % PW - 2;
+      xs[e] = (yy >= 0 && yy < H0 && xx >= 0 && xx < W0) ? xr[yy * W0 + xx] : 0.f;
+    }
+    __syncthreads();
+    const float* dg = dp1m + s * NQ * 32;
+    const uint8_t* ag = am1 + s * NQ * 32;
+    for (int q0 = gq; q0 < NQ; q0 += NG * U) {
+      // issue the U cells' gradient / argmax loads before any use: the loop is latency-bound
+      float g[U];
+      int am[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + NG * u;
+        g[u] = q < NQ ? __ldg(dg + q * 32 + c) : 0.f;
+        am[u] = q < NQ ? __ldg(ag + q * 32 + c) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (g[u] == 0.f) continue;
+        const int q = q0 + NG * u;
+        const int y = 2 * (q / W1) + (am[u] >> 1), x = 2 * (q % W1) + (am[u] & 1);
+        const float* xp = xs + y * PW + x;  // padded (y + kh, x + kw) = pixel (y + kh - 2, x + kw - 2)
+#pragma unroll
+        for (int kh = 0; kh < 5; ++kh)
+#pragma unroll
+          for (int kw = 0; kw < 5; ++kw) acc[kh * 5 + kw] = fmaf(g[u], xp[kh * PW + kw], acc[kh * 5 + kw]);
+        acc[25] += g[u];
+      }
+    }
+  }
+  __syncthreads();
+  float* red = xs;  // [NG groups][32 c][26]
+#pragma unroll
+  for (int j = 0; j < 26; ++j) red[(gq * 32 + c) * 26 + j] = acc[j];
+  __syncthreads();
+  float* out = part + ((int64_t)a * nch + ch) * 32 * 26;
+  for (int e = threadIdx.x; e < 32 * 26; e += blockDim.x) {
+    float v = 0.f;
+    for (int gg = 0; gg < NG; ++gg) v += red[gg * 32 * 26 + e];  // fixed order
+    out[e] = v;
+  }
+}
+
 // Σ of the split-K partials, then fused SGD on the conv weights and bias.
 // Partials: [A*nch] chunks of rpc samples (bpre == nullptr), or the balanced split-K layout
 // (bpre != nullptr): client a's partials are z = a + c for the CTAs c0..c1 covering its k-blocks
@@ -549,6 +670,16 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     if (conv1_fwd_tc(L, wa, w.base, wa.first ? b.c1wt_g : b.c1wt, xpack, b.xrows, b.p1, b.am1, st) < 0) return -1;
     ++n;
     pf.end(K_CONV1_FWD, f_c1, 4.0 * S * hw0 * d.cin + 5.0 * S * hw1 * d.C1, st);
+  } else if (wa.use_tc && d.cin == 1 && d.C1 == 32) {  // speech: conv1 + bias + ReLU + pool in one pass
+    const size_t sm = sizeof(float) * ((d.H0 + 4) * (d.W0 + 4) + 32 * 25 + 32);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_c1fwd_pool_1ch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      attr = true;
+    }
+    launch_pdl(wa.pdl, k_c1fwd_pool_1ch, dim3(A * B), 256, sm, st, xpack, wa.sidx, wa.bs, B, d.H0, d.W0, w, L.o_c1w,
+               L.o_c1b, b.p1, b.am1), ++n;
+    pf.end(K_CONV1_FWD, f_c1, 4.0 * S * hw0 * d.cin + 5.0 * S * hw1 * d.C1, st);
   } else {
     launch(ConvFwd{xpack, wa.sidx, wa.bs, B, d.H0, d.W0, d.cpad, d.C1, w, L.o_c1w, L.o_c1b, b.a1},
            B * d.H0 * d.W0, d.C1, A, st), ++n;
@@ -651,7 +782,8 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     pf.end(K_CONV1_DW, f_c1, 4.0 * S * hw0 * d.cin + 5.0 * S * hw1 * d.C1, st);
     const int N2 = 25 * d.C1 + 1, N1 = 25 * d.cpad + 1;
     DwRed r1{b.part1, d.C1, N1, L.o_c1w, L.o_c1b, b.c1wt, g1, (int64_t)d.H0 * wa.sum_bs, d.H0, (d.C1 * N1 + 255) / 256};
-    DwRed r2{b.part2, d.C2, N2, L.o_c2w, L.o_c2b, nullptr, g2, (int64_t)8 * wa.sum_bs, 8, (d.C2 * N2 + 255) / 256};
+    const int kps2 = conv2_dw_kps(L);
+    DwRed r2{b.part2, d.C2, N2, L.o_c2w, L.o_c2b, nullptr, g2, (int64_t)kps2 * wa.sum_bs, kps2, (d.C2 * N2 + 255) / 256};
     pf.begin(st);
     launch_pdl(wa.pdl, k_dw_reduce2_sgd, dim3(r1.nblk + r2.nblk, A), 256, 0, st, r1, r2, wa.bpre, w, slots, L.P_pad,
                wa.lr), ++n;
@@ -679,8 +811,23 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     pf.end(K_CONV2_DWR, 0, 8.0 * A * d.C2 * 25 * d.C1, st);
   }
   int nch1 = b.nch, rpc1 = rpc, g1 = 0;
+  const bool pooled_c1dw = tc && !tc1 && d.cin == 1 && d.C1 == 32;  // speech: dW from dp1m + am1 directly
+  if (tc && !tc1 && !pooled_c1dw) {  // route the tensor-core dX's dp1m through pool1's argmax -> dY1
+    pf.begin(st);
+    k_unpool<<<dim3(8, A * B), 256, 0, st>>>(b.dp1, b.p1, b.am1, d.H0, d.W0, d.C1, B, wa.bs, b.dY1), ++n;
+    pf.end(K_UNPOOL1, 0, S * hw0 * d.C1 * (4.0 + 9.0 / 4.0), st);
+  }
   pf.begin(st);
-  if (tc1) {
+  if (pooled_c1dw) {
+    const size_t sm = sizeof(float) * std::max((d.H0 + 4) * (d.W0 + 4), 16 * 32 * 26);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_c1dw_pooled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      attr = true;
+    }
+    launch_pdl(wa.pdl, k_c1dw_pooled, dim3(b.nch, A), 512, sm, st, b.dp1, b.am1, xpack, wa.sidx, wa.bs, B, d.H0,
+               d.W0, b.nch, rpc, b.part1), ++n;
+  } else if (tc1) {
     if (conv1_dw_tc(L, wa, b.xplanar, b.xrows, b.dp1, b.am1, b.slots, b.part1, b.part1_tc_cap, &g1, st) < 0)
       return -1;
     ++n;
@@ -688,7 +835,8 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     launch(ConvDw{b.dY1, xpack, wa.sidx, wa.bs, B, d.H0, d.W0, d.cpad, d.C1, b.nch, rpc, b.part1}, d.C1,
            25 * d.cpad + 1, A * b.nch, st), ++n;
   }
-  pf.end(K_CONV1_DW, f_c1, tc1 ? 4.0 * S * hw0 * d.cin + 5.0 * S * hw1 * d.C1 : 4.0 * S * hw0 * (d.cin + d.C1), st);
+  pf.end(K_CONV1_DW, f_c1,
+         (tc1 || pooled_c1dw) ? 4.0 * S * hw0 * d.cin + 5.0 * S * hw1 * d.C1 : 4.0 * S * hw0 * (d.cin + d.C1), st);
   pf.begin(st);
   launch_pdl(wa.pdl, k_dw_reduce_sgd, dim3((d.C1 * (25 * d.cpad + 1) + 127) / 128, A), 128, 0, st, 
       b.part1, nch1, rpc1, wa.bs, d.C1, 25 * d.cpad + 1, w, L.o_c1w,

@@ -1,8 +1,11 @@
 // k_conv_tc.cu — 5x5 'same' convolutions of the CIFAR CNN's second layer on the 5th-gen
 // tensor cores (tcgen05.mma kind::tf32, fp32 accumulators in TMEM, operands staged by TMA).
 //
-// Implicit GEMM without an im2col buffer.  One CTA computes one sample's 16x16 output
-// plane (M = 256 pixels = two M=128 accumulators) for all output channels N.  For each
+// Implicit GEMM without an im2col buffer.  One CTA tile is one 16-pixel-wide patch of PH_
+// rows (16 or 8) of one sample's output plane (M = 16·PH_ pixels = one or two M=128
+// accumulators) for all output channels N.  CIFAR's 16x16 plane is one 16x16 patch; the
+// speech model's 20x49 plane is 3 x 4 patches of 8x16 (TMA zero-fills the copy outside the
+// image, the epilogue stores only pixels inside it).  For each
 // horizontal tap kw (and 32-channel input chunk q) TMA loads ONE shifted copy of the input
 // plane, copy[h'][x][c] = X[h'-2][x+kw-2][32q+c] for h' in [0,20), x in [0,16), with the
 // zero padding produced by TMA's out-of-bounds fill.  A pixel is a 128-byte SW128 row, so
@@ -106,13 +109,12 @@ static bool tmap_encode_uncached(CUtensorMap* m, const void* base, int rank, con
 
 namespace {
 
-constexpr int HH = 16, WW = 16;          // conv2 plane (CIFAR)
-constexpr int ROWS = (HH + 4) * WW;      // 320 pixels per shifted copy
-constexpr int A_BYTES = ROWS * 128;      // 40960
+constexpr int WW = 16;                   // patch width (pixels): one 128-B row per pixel, 16 per image row
 constexpr int NSTAGE = 2;
 
-template <int N, int NB>  // N output channels; NB = rows of one tap's B tile (N, or 32 for MN-major)
-struct ConvSmem {
+template <int N, int NB, int PH_>  // N output channels; NB = rows of one tap's B tile (N, or 32 for
+struct ConvSmem {                  // MN-major); PH_ = patch rows (16: two M-halves, 8: one)
+  static constexpr int A_BYTES = (PH_ + 4) * WW * 128;  // one shifted copy: PH_ + 4 rows x 16 pixels
   static constexpr int B_TAP = NB * 128;
   static constexpr int B_BYTES = 5 * B_TAP;
   static constexpr int STAGE = A_BYTES + B_BYTES;
@@ -128,19 +130,24 @@ struct ConvTcArgs {
   int msplit;             // tiles per sample: 1 (both M-halves) or 2 (one M-half each, small waves)
   const float* bias;      // bias of client 0; client a at bias + a*bias_stride
   int64_t bias_stride;
-  float* out;             // fwd: p2 [S][8][8][N]; dx: dp1m [S][16][16][N] (ReLU'-masked pooled gradient)
-  uint8_t* am;            // fwd: argmax [S][8][8][N]
-  const float* p1;        // dx: pooled conv1 output [S][16][16][N] (ReLU' of the window max)
-  const uint8_t* am1;     // dx: pool1 argmax [S][16][16][N]
+  float* out;             // fwd: p2 [S][H/2][W/2][N]; dx: dp1m [S][H][W][N] (ReLU'-masked pooled gradient)
+  uint8_t* am;            // fwd: argmax [S][H/2][W/2][N]
+  const float* p1;        // dx: pooled conv1 output [S][H][W][N] (ReLU' of the window max)
+  const uint8_t* am1;     // dx: pool1 argmax [S][H][W][N]
+  int H, W;               // image plane of this layer (CIFAR 16x16, speech 20x49)
+  int ph, pw;             // patches per sample along h (PH_ rows each) and w (16 columns each)
 };
 
 // N: output channels; CH: 32-channel chunks of the input; BMN: B operand MN-major;
-// FLIP: transposed conv (dX); POOL: fused bias + ReLU + max-pool epilogue.
-template <int N, int CH, int BMN, int FLIP, int POOL>
+// FLIP: transposed conv (dX); POOL: fused bias + ReLU + max-pool epilogue; PH_: patch rows.
+template <int N, int CH, int BMN, int FLIP, int POOL, int PH_>
 __global__ void __launch_bounds__(192, 1)
     k_conv5_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, ConvTcArgs p) {
   constexpr int NB = BMN ? 32 : N;
-  using S = ConvSmem<N, NB>;
+  using S = ConvSmem<N, NB, PH_>;
+  constexpr int A_BYTES = S::A_BYTES;
+  constexpr int NMH = PH_ / 8;  // M-halves (128-pixel accumulators) per patch
+  const int NP = p.ph * p.pw;   // patches per sample
   // two accumulator buffers x two M-halves x N columns
   constexpr uint32_t TMEM_COLS = (4 * N <= 32) ? 32 : (4 * N <= 64 ? 64 : (4 * N <= 128 ? 128 : 256));
   constexpr uint32_t IDESC = tc::idesc_tf32(128, N, 0, BMN);
@@ -150,11 +157,12 @@ __global__ void __launch_bounds__(192, 1)
   // (samples past a client's |b| are skipped identically by every role).  The smem stage
   // ring runs across tiles and the TMEM accumulators are double-buffered, so the loads of
   // tile i+1 and the epilogue of tile i-1 overlap the MMAs of tile i.
-  // Tile t = slot (t / msplit) and, when msplit = 2, only its M-half (t & 1): small waves
-  // spread a sample's MMAs and epilogue over two SMs (the loads are the same either way).
-  const int T = p.A * p.B * p.msplit;
+  // With msplit = 2 (16-row patches only) a tile is one M-half (t & 1): small waves spread a
+  // sample's MMAs and epilogue over two SMs (the loads are the same either way).
+  // tile t -> (slot sl, patch pt, M-half split): t = ((sl · NP) + pt) · msplit + half
+  const int T = p.A * p.B * NP * p.msplit;
   auto valid = [&](int t) {
-    const int sl = t / p.msplit;
+    const int sl = t / (p.msplit * NP);
     return (sl % p.B) < p.bs[sl / p.B];
   };
 
@@ -200,7 +208,8 @@ __global__ void __launch_bounds__(192, 1)
       int it = 0;
       for (int t = blockIdx.x; t < T; t += gridDim.x) {
         if (!valid(t)) continue;
-        const int s = t / p.msplit, a = s / p.B;  // slot index s = a*B + r
+        const int s = t / (p.msplit * NP), a = s / p.B;  // slot index s = a*B + r
+        const int pt = (t / p.msplit) % NP, y0 = (pt / p.pw) * PH_, x0 = (pt % p.pw) * WW;
         for (int kb = 0; kb < NKB; ++kb, ++it) {
           const int st = it % NSTAGE, ph = (it / NSTAGE) & 1;
           const int kw = kb / CH, q = kb % CH;
@@ -208,7 +217,7 @@ __global__ void __launch_bounds__(192, 1)
           uint8_t* sa = smem + st * S::STAGE;
           uint8_t* sb = sa + A_BYTES;
           tc::mbar_expect_tx(full + st, S::STAGE);
-          tc::tma_load_4d(sa, &mapX, full + st, 32 * q, kw - 2, -2, s);
+          tc::tma_load_4d(sa, &mapX, full + st, 32 * q, x0 + kw - 2, y0 - 2, s);
           for (int kh = 0; kh < 5; ++kh) {
             const int tap = FLIP ? (4 - kh) * 5 + (4 - kw) : kh * 5 + kw;
             tc::tma_load_4d(sb + kh * S::B_TAP, &mapW, full + st, 0, tap, BMN ? 32 * q : 0, a * p.wmul);
@@ -222,7 +231,7 @@ __global__ void __launch_bounds__(192, 1)
       int it = 0, tc_ = 0;
       for (int t = blockIdx.x; t < T; t += gridDim.x) {
         if (!valid(t)) continue;
-        const int mh0 = p.msplit == 2 ? (t & 1) : 0, mh1 = p.msplit == 2 ? mh0 + 1 : 2;
+        const int mh0 = p.msplit == 2 ? (t & 1) : 0, mh1 = p.msplit == 2 ? mh0 + 1 : NMH;
         const int buf = tc_ & 1, aph = (tc_ >> 1) & 1;
         tc::mbar_wait(aempty + buf, aph ^ 1);  // epilogue finished reading this buffer
         tc::tc_fence_after();
@@ -240,7 +249,7 @@ __global__ void __launch_bounds__(192, 1)
               const uint64_t bd = BMN ? tc::sdesc(sb + kh * S::B_TAP + k * 1024, NB * 128, 512, tc::kSW128_32B)
                                       : tc::sdesc(sb + kh * S::B_TAP + k * 32, 0, 1024, tc::kSW128);
 #pragma unroll
-              for (int mh = 0; mh < 2; ++mh) {
+              for (int mh = 0; mh < NMH; ++mh) {
                 if (mh < mh0 || mh >= mh1) continue;
                 const uint64_t ad = tc::sdesc(sa + (mh * 8 + kh) * WW * 128 + k * 32, 0, 1024, tc::kSW128);
                 tc::mma_tf32(acc0 + mh * N, ad, bd, IDESC, (kb | kh | k) != 0);
@@ -259,8 +268,9 @@ __global__ void __launch_bounds__(192, 1)
     int tc_ = 0;
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
     if (!valid(t)) continue;
-    const int s = t / p.msplit, a = s / p.B;
-    const int mh0 = p.msplit == 2 ? (t & 1) : 0, mh1 = p.msplit == 2 ? mh0 + 1 : 2;
+    const int s = t / (p.msplit * NP), a = s / p.B;
+    const int pt = (t / p.msplit) % NP, y0 = (pt / p.pw) * PH_, x0 = (pt % p.pw) * WW;
+    const int mh0 = p.msplit == 2 ? (t & 1) : 0, mh1 = p.msplit == 2 ? mh0 + 1 : NMH;
     const int buf = tc_ & 1, aph = (tc_ >> 1) & 1;
     ++tc_;
     tc::mbar_wait(afull + buf, aph);
@@ -268,9 +278,9 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t tacc = tbase + buf * 2 * N;
     const float* bias = p.bias + (int64_t)a * p.bias_stride * p.wmul;
 #pragma unroll
-    for (int mh = 0; mh < 2; ++mh) {
+    for (int mh = 0; mh < NMH; ++mh) {
       if (mh < mh0 || mh >= mh1) continue;
-      const int h = mh * 8 + (i >> 4), w = i & 15;
+      const int h = y0 + mh * 8 + (i >> 4), w = x0 + (i & 15);  // image pixel of this accumulator row
 #pragma unroll
       for (int n0 = 0; n0 < N; n0 += 16) {
         float v[16];
@@ -293,8 +303,10 @@ __global__ void __launch_bounds__(192, 1)
             pv[j] = bv > 0.f ? bv : 0.f;
             pa[j] = (uint8_t)bi;
           }
-          if ((lane & 17) == 0) {
-            const int64_t o = (((int64_t)s * 8 + (h >> 1)) * 8 + (w >> 1)) * N + n0;
+          // floor pooling: only windows inside the image (the patch may overhang it)
+          const int H2 = p.H >> 1, W2 = p.W >> 1;
+          if ((lane & 17) == 0 && (h >> 1) < H2 && (w >> 1) < W2) {
+            const int64_t o = (((int64_t)s * H2 + (h >> 1)) * W2 + (w >> 1)) * N + n0;
             float4* dst = reinterpret_cast<float4*>(p.out + o);
 #pragma unroll
             for (int j = 0; j < 4; ++j) dst[j] = make_float4(pv[4 * j], pv[4 * j + 1], pv[4 * j + 2], pv[4 * j + 3]);
@@ -308,13 +320,15 @@ __global__ void __launch_bounds__(192, 1)
           // ReLU' of pool1 fused: dp1m = dp1 where the pooled value is > 0, else 0.  The
           // routing to the window's argmax (pool1 backward) happens where dY1 is consumed
           // (conv1's dW expands it into its B operand), so dY1 is never written to HBM.
-          const int64_t o = (((int64_t)s * HH + h) * WW + w) * N + n0;
+          const int64_t o = (((int64_t)s * p.H + h) * p.W + w) * N + n0;
+          if (h < p.H && w < p.W) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 pv = *reinterpret_cast<const float4*>(p.p1 + o + 4 * j);
-            *reinterpret_cast<float4*>(p.out + o + 4 * j) =
-                make_float4(pv.x > 0.f ? v[4 * j] : 0.f, pv.y > 0.f ? v[4 * j + 1] : 0.f,
-                            pv.z > 0.f ? v[4 * j + 2] : 0.f, pv.w > 0.f ? v[4 * j + 3] : 0.f);
+            for (int j = 0; j < 4; ++j) {
+              const float4 pv = *reinterpret_cast<const float4*>(p.p1 + o + 4 * j);
+              *reinterpret_cast<float4*>(p.out + o + 4 * j) =
+                  make_float4(pv.x > 0.f ? v[4 * j] : 0.f, pv.y > 0.f ? v[4 * j + 1] : 0.f,
+                              pv.z > 0.f ? v[4 * j + 2] : 0.f, pv.w > 0.f ? v[4 * j + 3] : 0.f);
+            }
           }
         }
       }
@@ -340,18 +354,18 @@ int msplit_for(const WaveArgs& wa) {
   return (on && 2 * wa.sum_bs <= wa.sms) ? 2 : 1;
 }
 
-template <int N, int CH, int BMN, int FLIP, int POOL>
+template <int N, int CH, int BMN, int FLIP, int POOL, int PH_>
 cudaError_t launch_conv5(const CUtensorMap& mx, const CUtensorMap& mw, const ConvTcArgs& p, int A, bool pdl, int sms,
                          cudaStream_t st) {
   constexpr int NB = BMN ? 32 : N;
-  const int smem = ConvSmem<N, NB>::TOTAL;
-  auto kfn = k_conv5_tc<N, CH, BMN, FLIP, POOL>;
+  const int smem = ConvSmem<N, NB, PH_>::TOTAL;
+  auto kfn = k_conv5_tc<N, CH, BMN, FLIP, POOL, PH_>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  const int tiles = A * p.B * p.msplit;
+  const int tiles = A * p.B * p.ph * p.pw * p.msplit;
   launch_pdl(pdl, kfn, dim3(tiles < sms ? tiles : sms), 192, smem, st, mx, mw, p);
   return cudaGetLastError();
 }
@@ -366,36 +380,52 @@ bool make_w2_map(CUtensorMap* m, const Layout& L, const float* base, int64_t ncl
   return tmap_encode(m, base + L.o_c2w, 4, dims, str, box, swz);
 }
 
-// NHWC activations [S][16][16][C] with a box of one 20-row x 16-pixel x 32-channel copy.
-bool make_plane_map(CUtensorMap* m, const float* base, int C, int64_t slots) {
-  uint64_t dims[4] = {(uint64_t)C, WW, HH, (uint64_t)slots};
-  uint64_t str[3] = {(uint64_t)C * 4, (uint64_t)C * 4 * WW, (uint64_t)C * 4 * WW * HH};
-  uint32_t box[4] = {32, WW, HH + 4, 1};
+// NHWC activations [S][H][W][C] with a box of one (ph + 4)-row x 16-pixel x 32-channel copy.
+bool make_plane_map(CUtensorMap* m, const float* base, int C, int H, int W, int ph, int64_t slots) {
+  uint64_t dims[4] = {(uint64_t)C, (uint64_t)W, (uint64_t)H, (uint64_t)slots};
+  uint64_t str[3] = {(uint64_t)C * 4, (uint64_t)C * 4 * W, (uint64_t)C * 4 * W * H};
+  uint32_t box[4] = {32, WW, (uint32_t)ph + 4, 1};
   return tmap_encode(m, base, 4, dims, str, box, 1);
 }
+
+// patch rows: a single 16x16 patch covers CIFAR's plane; other planes use 8-row patches
+// (less overhang: speech's 20 rows = 3 x 8 instead of 2 x 16)
+int patch_rows(const CnnDims& d) { return (d.H1 == 16 && d.W1 == 16) ? 16 : 8; }
 
 }  // namespace
 
 bool conv_tc_supported(const Layout& L) {
-  return L.model == 1 && L.d.H1 == HH && L.d.W1 == WW && L.d.C1 == 32 && L.d.C2 == 64;
+  // conv2 of either CNN: 5x5 'same', 32 -> 64 channels, any plane at least 8 x 16
+  return (L.model == FL_MODEL_CNN_CIFAR || L.model == FL_MODEL_CNN_SPEECH) && L.d.C1 == 32 && L.d.C2 == 64 &&
+         L.d.H1 >= 8 && L.d.W1 >= 16;
 }
 
 // conv2 forward + bias + ReLU + pool on tensor cores: p1 -> p2, am2.
 int conv2_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p1,
                  int64_t slots, float* p2, uint8_t* am2, cudaStream_t st) {
+  const CnnDims& d = L.d;
+  const int ph = patch_rows(d);
   CUtensorMap mx, mw;
-  if (!make_plane_map(&mx, p1, 32, slots) || !make_w2_map(&mw, L, wbase, wclients, 64, 1)) return -1;
-  ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, msplit_for(wa), wbase + L.o_c2b, L.P_pad, p2, am2};
-  return launch_conv5<64, 1, 0, 0, 1>(mx, mw, p, wa.A, wa.pdl, wa.sms, st) == cudaSuccess ? 1 : -1;
+  if (!make_plane_map(&mx, p1, 32, d.H1, d.W1, ph, slots) || !make_w2_map(&mw, L, wbase, wclients, 64, 1)) return -1;
+  ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, ph == 16 ? msplit_for(wa) : 1, wbase + L.o_c2b, L.P_pad, p2, am2,
+               nullptr, nullptr, d.H1, d.W1, (d.H1 + ph - 1) / ph, (d.W1 + WW - 1) / WW};
+  const cudaError_t e = ph == 16 ? launch_conv5<64, 1, 0, 0, 1, 16>(mx, mw, p, wa.A, wa.pdl, wa.sms, st)
+                                 : launch_conv5<64, 1, 0, 0, 1, 8>(mx, mw, p, wa.A, wa.pdl, wa.sms, st);
+  return e == cudaSuccess ? 1 : -1;
 }
 
 // conv2 dX (transposed conv) on tensor cores: dY2 -> dp1.
 int conv2_dx_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* dY2,
                 int64_t slots, const float* p1, float* dp1m, cudaStream_t st) {
+  const CnnDims& d = L.d;
+  const int ph = patch_rows(d);
   CUtensorMap mx, mw;
-  if (!make_plane_map(&mx, dY2, 64, slots) || !make_w2_map(&mw, L, wbase, wclients, 32, 2)) return -1;
-  ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, msplit_for(wa), nullptr, 0, dp1m, nullptr, p1, nullptr};
-  return launch_conv5<32, 2, 1, 1, 0>(mx, mw, p, wa.A, wa.pdl, wa.sms, st) == cudaSuccess ? 1 : -1;
+  if (!make_plane_map(&mx, dY2, 64, d.H1, d.W1, ph, slots) || !make_w2_map(&mw, L, wbase, wclients, 32, 2)) return -1;
+  ConvTcArgs p{wa.bs, wa.A, wa.B, wa.first ? 0 : 1, ph == 16 ? msplit_for(wa) : 1, nullptr, 0, dp1m, nullptr, p1,
+               nullptr, d.H1, d.W1, (d.H1 + ph - 1) / ph, (d.W1 + WW - 1) / WW};
+  const cudaError_t e = ph == 16 ? launch_conv5<32, 2, 1, 1, 0, 16>(mx, mw, p, wa.A, wa.pdl, wa.sms, st)
+                                 : launch_conv5<32, 2, 1, 1, 0, 8>(mx, mw, p, wa.A, wa.pdl, wa.sms, st);
+  return e == cudaSuccess ? 1 : -1;
 }
 
 }  // namespace flb

@@ -5,8 +5,9 @@
 //
 // GEMM with M = (tap, c) = 800 rows, N = o = 64, K = pixels.  One CTA reduces a chunk of
 // one client's samples; all 800 rows live in TMEM at once (7 accumulators of 128 x 64 fp32
-// plus one for the bias = 512 columns), so every K-block of 32 pixels (two image rows) is
-// loaded exactly once:
+// plus one for the bias = 512 columns), so every K-block of 32 pixels (two image rows of a
+// 16-column patch: CIFAR's 16 x 16 plane has 8 per sample, speech's 20 x 49 plane 10 x 4 with
+// the columns past 49 zero-filled by TMA) is loaded exactly once:
 //   A: five shifted copies copy_kw[h'][w][c] = p1[h0-2+h'][w+kw-2][c], h' in [0,6) (TMA,
 //      zero fill at the borders); tap (kh, kw) is copy_kw shifted down by 16·kh rows.
 //      Both operands are MN-major (32-bit MN-major = SWIZZLE_128B_BASE32B layout).
@@ -44,9 +45,10 @@ constexpr int NO = 64;
 
 struct DwArgs {
   const int32_t* bpre;  // [A + 1] prefix sums of the wave's batch sizes
-  int A, B, G;          // G CTAs split the wave's U k-blocks (8 per sample) evenly
+  int A, B, G;          // G CTAs split the wave's U k-blocks (kps per sample) evenly
   int64_t U;
   float* part;          // [A + G][64 o][801]: partial of (CTA c, client a) at z = a + c
+  int kps, pw;          // k-blocks per sample = (H / 2) row pairs x pw 16-column patches
 };
 
 // Largest a in [0, A) with bpre[a] <= x (the client owning concatenated sample x).
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(192, 1)
   // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
   // would stall other streams' kernels) or touching anything it writes.
   pdl_wait();
-  const int a0 = client_of(p.bpre, p.A, u0 >> 3);
+  const int a0 = client_of(p.bpre, p.A, u0 / p.kps);
   extern __shared__ uint8_t smem_raw[];
   // align by pointer arithmetic on the shared array (an integer round trip would turn every
   // epilogue access into a generic LD/ST instead of LDS/STS)
@@ -111,19 +113,21 @@ __global__ void __launch_bounds__(192, 1)
     if (tc::elect_one()) {
       int it = 0;
       for (int a = a0; a < p.A; ++a) {
-        const int64_t kb0 = 8 * (int64_t)p.bpre[a];
-        const int64_t ss = u0 > kb0 ? u0 : kb0, se = min(u1, 8 * (int64_t)p.bpre[a + 1]);
+        const int64_t kb0 = p.kps * (int64_t)p.bpre[a];
+        const int64_t ss = u0 > kb0 ? u0 : kb0, se = min(u1, p.kps * (int64_t)p.bpre[a + 1]);
         if (ss >= u1) break;
         for (int64_t u = ss; u < se; ++u, ++it) {
           const int st = it % NST, ph = (it / NST) & 1;
-          const int kk = (int)(u - kb0), s = a * p.B + (kk >> 3), h0 = 2 * (kk & 7);
+          const int kk = (int)(u - kb0), s = a * p.B + kk / p.kps, r = kk % p.kps;
+          const int h0 = 2 * (r / p.pw), x0 = 16 * (r % p.pw);
           tc::mbar_wait(empty + st, ph ^ 1);
           uint8_t* sa = smem + st * STAGE;
           tc::mbar_expect_tx(full + st, STAGE);
 #pragma unroll
-          for (int kw = 0; kw < 5; ++kw) tc::tma_load_4d(sa + kw * COPY_BYTES, &mapX, full + st, 0, kw - 2, h0 - 2, s);
-          tc::tma_load_4d(sa + A_BYTES, &mapD, full + st, 0, 0, h0, s);
-          tc::tma_load_4d(sa + A_BYTES + 4096, &mapD, full + st, 32, 0, h0, s);
+          for (int kw = 0; kw < 5; ++kw)
+            tc::tma_load_4d(sa + kw * COPY_BYTES, &mapX, full + st, 0, x0 + kw - 2, h0 - 2, s);
+          tc::tma_load_4d(sa + A_BYTES, &mapD, full + st, 0, x0, h0, s);
+          tc::tma_load_4d(sa + A_BYTES + 4096, &mapD, full + st, 32, x0, h0, s);
         }
       }
     }
@@ -132,8 +136,8 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t ones_a = tc::smem_u32(ones);
       int it = 0, si = 0;
       for (int a = a0; a < p.A; ++a, ++si) {
-        const int64_t kb0 = 8 * (int64_t)p.bpre[a];
-        const int64_t ss = u0 > kb0 ? u0 : kb0, se = min(u1, 8 * (int64_t)p.bpre[a + 1]);
+        const int64_t kb0 = p.kps * (int64_t)p.bpre[a];
+        const int64_t ss = u0 > kb0 ? u0 : kb0, se = min(u1, p.kps * (int64_t)p.bpre[a + 1]);
         if (ss >= u1) break;
         tc::mbar_wait(tempty, (si & 1) ^ 1);  // previous segment's accumulators drained
         tc::tc_fence_after();
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(192, 1)
     const int qd = warp & 3, i = qd * 32 + lane;  // accumulator row
     int si = 0;
     for (int a = a0; a < p.A; ++a, ++si) {
-      const int64_t kb0 = 8 * (int64_t)p.bpre[a];
+      const int64_t kb0 = p.kps * (int64_t)p.bpre[a];
       if ((u0 > kb0 ? u0 : kb0) >= u1) break;
       tc::mbar_wait(tfull, si & 1);
       tc::tc_fence_after();
@@ -201,11 +205,11 @@ __global__ void __launch_bounds__(192, 1)
 
 // Σ of a client's partials (CTAs c_first..c_last, in order), then SGD on conv2.w / conv2.b.
 __global__ void k_dw2_reduce_sgd(const float* __restrict__ part, const int32_t* __restrict__ bpre, int G,
-                                 int64_t U, const float* wsrc, int64_t wstride, float* dst, int64_t P_pad,
+                                 int64_t U, int kps, const float* wsrc, int64_t wstride, float* dst, int64_t P_pad,
                                  int64_t o_w, int64_t o_b, float lr) {
   pdl_wait();  // (PDL) previous kernel's writes visible; the implicit trigger is at exit
   const int a = blockIdx.y;
-  const int64_t v0 = 8 * (int64_t)bpre[a], v1 = 8 * (int64_t)bpre[a + 1] - 1;  // the client's k-blocks
+  const int64_t v0 = kps * (int64_t)bpre[a], v1 = kps * (int64_t)bpre[a + 1] - 1;  // the client's k-blocks
   const int c0 = (int)(((v0 + 1) * G + U - 1) / U) - 1, c1 = (int)(((v1 + 1) * G + U - 1) / U) - 1;
   const float* pa = part + (int64_t)(a + c0) * NROW * NO;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < NROW * NO; e += gridDim.x * blockDim.x) {
@@ -216,12 +220,12 @@ __global__ void k_dw2_reduce_sgd(const float* __restrict__ part, const int32_t* 
   }
 }
 
-bool make_maps(CUtensorMap* mx, CUtensorMap* md, const float* p1, const float* dY2, int64_t slots) {
-  uint64_t dx[4] = {32, 16, 16, (uint64_t)slots};
-  uint64_t sx[3] = {32 * 4, 32 * 4 * 16, 32 * 4 * 256};
+bool make_maps(CUtensorMap* mx, CUtensorMap* md, const float* p1, const float* dY2, int H, int W, int64_t slots) {
+  uint64_t dx[4] = {32, (uint64_t)W, (uint64_t)H, (uint64_t)slots};
+  uint64_t sx[3] = {32 * 4, (uint64_t)32 * 4 * W, (uint64_t)32 * 4 * W * H};
   uint32_t bx[4] = {32, 16, 6, 1};
-  uint64_t dd[4] = {64, 16, 16, (uint64_t)slots};
-  uint64_t sd[3] = {64 * 4, 64 * 4 * 16, 64 * 4 * 256};
+  uint64_t dd[4] = {64, (uint64_t)W, (uint64_t)H, (uint64_t)slots};
+  uint64_t sd[3] = {64 * 4, (uint64_t)64 * 4 * W, (uint64_t)64 * 4 * W * H};
   uint32_t bd[4] = {32, 16, 2, 1};
   return tmap_encode(mx, p1, 4, dx, sx, bx, 2) && tmap_encode(md, dY2, 4, dd, sd, bd, 2);
 }
@@ -230,10 +234,12 @@ bool make_maps(CUtensorMap* mx, CUtensorMap* md, const float* p1, const float* d
 
 int conv2_dw_tc(const Layout& L, const WaveArgs& wa, const float* p1, const float* dY2, int64_t slots, float* part,
                 int64_t part_cap, int* g_out, cudaStream_t st) {
+  const CnnDims& d = L.d;
   CUtensorMap mx, md;
-  if (!make_maps(&mx, &md, p1, dY2, slots)) return -1;
+  if (!make_maps(&mx, &md, p1, dY2, d.H1, d.W1, slots)) return -1;
   // one CTA per SM (512 TMEM columns each), every CTA at least one sample of work
-  const int64_t U = 8 * wa.sum_bs;
+  const int kps = conv2_dw_kps(L), pw = (d.W1 + 15) / 16;
+  const int64_t U = (int64_t)kps * wa.sum_bs;
   // at least `mins` samples per CTA (FL_DW2_MINS): each CTA writes a whole [801][64] partial, so
   // in small waves a finer split costs more SM time and traffic than it saves in latency
   static const int mins = std::max(1, env_knob("FL_DW2_MINS", 1));
@@ -244,7 +250,7 @@ int conv2_dw_tc(const Layout& L, const WaveArgs& wa, const float* p1, const floa
     cudaFuncSetAttribute(k_conv2_dw_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     attr = true;
   }
-  DwArgs p{wa.bpre, wa.A, wa.B, G, U, part};
+  DwArgs p{wa.bpre, wa.A, wa.B, G, U, part, kps, pw};
   launch_pdl(wa.pdl, k_conv2_dw_tc, dim3(G), 192, SMEM, st, mx, md, p);
   *g_out = G;
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
@@ -252,12 +258,14 @@ int conv2_dw_tc(const Layout& L, const WaveArgs& wa, const float* p1, const floa
 
 int conv2_dw_reduce_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t wsrc_stride, float* dst,
                        const float* part, int G, cudaStream_t st) {
+  const int kps = conv2_dw_kps(L);
   launch_pdl(wa.pdl, k_dw2_reduce_sgd, dim3((NROW * NO + 255) / 256, wa.A), 256, 0, st, part, wa.bpre, G,
-             (int64_t)8 * wa.sum_bs, wsrc, wsrc_stride, dst, L.P_pad, L.o_c2w, L.o_c2b, wa.lr);
+             (int64_t)kps * wa.sum_bs, kps, wsrc, wsrc_stride, dst, L.P_pad, L.o_c2w, L.o_c2b, wa.lr);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
 int64_t conv2_dw_tc_part_z(int64_t max_clients) { return max_clients + 2 * 148; }
+int conv2_dw_kps(const Layout& L) { return (L.d.H1 / 2) * ((L.d.W1 + 15) / 16); }
 int64_t conv2_dw_tc_z_floats() { return (int64_t)NROW * NO; }
 
 }  // namespace flb

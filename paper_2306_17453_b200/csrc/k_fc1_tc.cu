@@ -172,6 +172,7 @@ struct BwArgs {
   const int32_t* bs;
   int A, B, HID, F, wmul;
   int H2, W2, C2;
+  int H1, W1;          // conv2 output plane (pool2 input): 2·H2 x 2·W2, or one odd row / column more
   const float* p2;
   const uint8_t* am2;
   float* dY2;
@@ -373,7 +374,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       tc::tc_fence_before();
       tc::mbar_arrive(dxempty + pb);
       const int cc = k % p.C2, pw = (k / p.C2) % p.W2, ph = k / (p.C2 * p.W2);
-      const int W1 = 2 * p.W2, H1 = 2 * p.H2;
+      const int W1 = p.W1, H1 = p.H1;  // a trailing odd row / column gets no gradient (floor pooling)
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         if (r0 + r >= bs) break;
@@ -407,7 +408,8 @@ void set_smem(K k, int bytes, bool& done) {
 
 bool fc1_tc_supported(const Layout& L, int B) {
   const CnnDims& d = L.d;
-  return B == NB && d.HID % 128 == 0 && d.F % DW_N == 0 && d.H1 == 2 * d.H2 && d.W1 == 2 * d.W2;
+  // B: the slot pitch (the speech model's batch of 20 rides in 32-row slots, rows >= |b| zero)
+  return B == NB && d.HID % 128 == 0 && d.F % DW_N == 0 && d.H1 / 2 == d.H2 && d.W1 / 2 == d.W2;
 }
 
 int64_t fc1_tc_part_floats(int64_t max_clients, const Layout& L) { return (max_clients + 2 * 148) * 16 * NB * L.d.HID; }
@@ -467,7 +469,7 @@ int fc1_bwd_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, int64_t w
     return -1;
   static bool attr = false;
   set_smem(k_fc1_bwd_tc, BW_SMEM, attr);
-  BwArgs p{wa.bs, wa.A, wa.B, d.HID, d.F, wa.first ? 0 : 1, d.H2, d.W2, d.C2, p2, am2, dY2,
+  BwArgs p{wa.bs, wa.A, wa.B, d.HID, d.F, wa.first ? 0 : 1, d.H2, d.W2, d.C2, d.H1, d.W1, p2, am2, dY2,
            wsrc + L.o_f1b, L.P_pad, slots_w + L.o_f1b, L.P_pad, dh, wa.lr};
   const int tiles = wa.A * (d.F / 128);
   launch_pdl(wa.pdl, k_fc1_bwd_tc, dim3(tiles < wa.sms ? tiles : wa.sms), BW_THREADS, BW_SMEM, st, mws, mwd, mdht, mx,
