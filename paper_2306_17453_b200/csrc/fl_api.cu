@@ -1096,7 +1096,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
         int64_t sum_bs = 0;
         for (int32_t a = 0; a < ws.A[(size_t)k]; ++a) sum_bs += h_bs[ws.bs_off[(size_t)k] + a];
         WaveArgs wa{ws.A[(size_t)k], (int)B, k == 0, ws.d_sidx + ws.slot_off[(size_t)k], ws.d_bs + ws.bs_off[(size_t)k],
-                    c->cfg.lr, sum_bs, &c->prof, true, K, true, ws.d_bpre + ws.bs_off[(size_t)k] + k, c->n_sms};
+                    c->cfg.lr, sum_bs, &c->prof, c->cfg.math == 0, K, true, ws.d_bpre + ws.bs_off[(size_t)k] + k, c->n_sms};
         c->prof.begin(st);
         const int nl = lstm_wave(L, wa, reinterpret_cast<const uint8_t*>(c->d_xpack), c->d_ypack, c->d_theta,
                                  c->d_slots, c->lb, st);

@@ -292,6 +292,22 @@ struct LstmBufs {
   float *dpre = nullptr, *dX = nullptr, *E = nullptr, *dE = nullptr, *dhT = nullptr;
 };
 bool lstm_layout(Layout* L);
+// char-LSTM batched GEMMs on tcgen05 (k_lstm_tc.cu): which = 1 layer-1 input projection,
+// 2 layer-1 dX, 3 W_hh1 SGD, 4 W_ih1 SGD, 6 W_hh0 SGD (see the file header)
+struct LstmTcIn {
+  int A, B, wmul;
+  int64_t slots;               // activation slots (tensor-map extent)
+  const float* wsrc;           // weights read: θ_g (first wave) or the slots
+  int64_t wstride, wclients, P_pad;
+  float* slots_w;              // weights written (client slots)
+  int64_t o_wih1, o_whh1, o_whh0, o_bih1, o_bhh1;
+  const float *H0, *H1, *dpre;
+  float *xp, *dX;
+  float lr;
+  bool pdl;
+};
+bool lstm_tc_supported(int B);
+int lstm_gemm_tc(int which, const LstmTcIn& in, cudaStream_t st);
 int64_t lstm_act_floats(int64_t S, int which);  // 0: [S][T][G] 1: [S][T+1][H] 2: [S][T][H] 3: [S][T][E] 4: [S][H]
 int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const int32_t* ypack, const float* theta_g,
               float* slots, LstmBufs& b, cudaStream_t st);

@@ -674,8 +674,19 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
   RecArgs r0{wbase, wstride, q.whh[0], B, b.xp, b.G0, b.C0, b.H0, nullptr, 0, nullptr};
   auto fwd = k_lstm_fwd_reg;
   launch_pdl(wa.pdl, fwd, dim3(A * CL), FT, REC_SMEM, st, r0), ++n;
+  // tensor-core GEMMs (TF32, k_lstm_tc.cu) unless math = 1 (FP32 SIMT everywhere)
+  const bool tc = wa.use_tc && lstm_tc_supported(B);
+  LstmTcIn ti{A, B, wa.first ? 0 : 1, b.slots, wbase, wstride, wa.first ? 1 : wa.wclients, L.P_pad, slots,
+              q.wih[1], q.whh[1], q.whh[0], q.bih[1], q.bhh[1], b.H0, b.H1, b.dpre, b.xp, b.dX, lr, wa.pdl};
+  auto tcg = [&](int which) {
+    if (lstm_gemm_tc(which, ti, st) < 0) return false;
+    ++n;
+    return true;
+  };
   // layer-1 input projection: xp[s][t] = W_ih1 · H0[s][t+1] + b_ih1 + b_hh1
-  {
+  if (tc) {
+    if (!tcg(1)) return -1;
+  } else {
     GemmArgs g{};
     g.A = Opnd{b.H0 + LH, (int64_t)B * S_T1, S_T1, LH, 0, 1, LT, 0x7fffffff};
     g.Bm = affine(wbase + q.wih[1], wstride, LH, 1);
@@ -692,7 +703,9 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
   RecArgs rb1{wbase, wstride, q.whh[1], B, nullptr, b.G1, b.C1, b.H1, b.dhT, 0, b.dpre};
   launch_pdl(wa.pdl, k_lstm_bwd, dim3(A * CL), 256, REC_SMEM, st, rb1), ++n;
   // dX of layer 1 (old W_ih1): dX[s][t][k] = Σ_n dpre[s][t][n] W_ih1[n][k]
-  {
+  if (tc) {
+    if (!tcg(2)) return -1;
+  } else {
     GemmArgs g{};
     g.A = affine(b.dpre, (int64_t)M * LG, LG, 1);
     g.Bm = affine(wbase + q.wih[1], wstride, 1, LH);
@@ -701,7 +714,10 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
     gemm(g);
   }
   // layer-1 weight gradients + SGD: W_hh1 -= η Σ dpreᵀ H1[t], W_ih1 -= η Σ dpreᵀ H0[t+1]
-  for (int which = 0; which < 2; ++which) {
+  if (tc) {
+    if (!tcg(3) || !tcg(4)) return -1;
+  }
+  for (int which = 0; which < 2 && !tc; ++which) {
     GemmArgs g{};
     g.A = Opnd{b.dpre, (int64_t)M * LG, 0, 1, (int64_t)LT * LG, LG, 0x7fffffff, LT};  // (n, m = (r, t))
     const float* hsrc = which == 0 ? b.H1 : b.H0 + LH;
@@ -725,7 +741,9 @@ int lstm_wave(const Layout& L, const WaveArgs& wa, const uint8_t* xpack, const i
     g.out = b.dE, g.o_sa = (int64_t)M * LE, g.o_r = (int64_t)LT * LE, g.o_t = LE, g.o_j = 1, g.To = LT;
     gemm(g);
   }
-  {  // W_hh0 -= η Σ dpre0ᵀ H0[t]
+  if (tc) {  // W_hh0 -= η Σ dpre0ᵀ H0[t]
+    if (!tcg(6)) return -1;
+  } else {  // W_hh0 -= η Σ dpre0ᵀ H0[t]
     GemmArgs g{};
     g.A = Opnd{b.dpre, (int64_t)M * LG, 0, 1, (int64_t)LT * LG, LG, 0x7fffffff, LT};
     g.Bm = Opnd{b.H0, (int64_t)B * S_T1, 0, 1, S_T1, LH, 0x7fffffff, LT};

@@ -320,22 +320,30 @@ def _lstm_block_errors(a, b):
     return out
 
 
-def test_lstm_round_small():
+# char-LSTM: the batched GEMMs run on tcgen05 with TF32 operands (math = 0, reading R15) and
+# in FP32 SIMT with math = 1.  FP32 trajectories stay ~2e-7 from the fp64 oracle; TF32 ones
+# ~1e-5 over a few steps (1e-3 is the north-star bar on θ after a round).
+TOL_LSTM = {0: 1e-4, 1: 1e-5}
+
+
+@pytest.mark.parametrize("math", [0, 1])
+def test_lstm_round_small(math):
     sizes = np.array([1, 3, 4, 5, 9], dtype=np.int64)
     wl = synth.preset("C5", n_pop=len(sizes), n_cohort=len(sizes))
-    out, N, ref, Nref, tk, tk_gpu, theta = run_round(wl, sizes, np.arange(len(sizes)))
+    out, N, ref, Nref, tk, tk_gpu, theta = run_round(wl, sizes, np.arange(len(sizes)), math=math)
     assert N == Nref == sizes.sum()
     for i in range(len(sizes)):
         e = np.max(np.abs(tk_gpu[i] - tk[i]))
-        assert e <= 1e-5, (i, _lstm_block_errors(tk_gpu[i], tk[i]))  # fp32 SIMT path: ~2e-7 measured
+        assert e <= TOL_LSTM[math], (i, _lstm_block_errors(tk_gpu[i], tk[i]))
     assert np.max(np.abs(out - ref)) <= TOL_ROUND
     assert np.max(np.abs(out - theta)) > 1e-4  # the round moved the model
 
 
-def test_lstm_round_two_epochs_shuffled_host_population():
+@pytest.mark.parametrize("math", [0, 1])
+def test_lstm_round_two_epochs_shuffled_host_population(math):
     sizes = np.array([2, 4, 7, 13], dtype=np.int64)
     wl = synth.preset("C5", n_pop=len(sizes), n_cohort=len(sizes), E=2, shuffle=1)
-    out, N, ref, Nref, tk, tk_gpu, theta = run_round(wl, sizes, np.arange(len(sizes)), on_device=False)
+    out, N, ref, Nref, tk, tk_gpu, theta = run_round(wl, sizes, np.arange(len(sizes)), on_device=False, math=math)
     for i in range(len(sizes)):
-        assert np.max(np.abs(tk_gpu[i] - tk[i])) <= 1e-5, (i, _lstm_block_errors(tk_gpu[i], tk[i]))
-    assert np.max(np.abs(out - ref)) <= 1e-5
+        assert np.max(np.abs(tk_gpu[i] - tk[i])) <= TOL_LSTM[math], (i, _lstm_block_errors(tk_gpu[i], tk[i]))
+    assert np.max(np.abs(out - ref)) <= TOL_LSTM[math]
