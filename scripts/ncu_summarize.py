@@ -52,7 +52,7 @@ def main():
     os.makedirs(out, exist_ok=True)
     # launch list
     L = rows(os.path.join(src, "launches.csv"))
-    shutil.copy(os.path.join(src, "launches.csv"), os.path.join(out, "launches_c2_round.csv"))
+    shutil.copy(os.path.join(src, "launches.csv"), os.path.join(out, "launches_bench_round.csv"))
     agg = collections.defaultdict(lambda: [0, 0.0])
     for d in L:
         us = float(d["Metric Value"].replace(",", "")) / (1e3 if d["Metric Unit"] == "ns" else 1.0)
@@ -94,7 +94,9 @@ def main():
         res[c] = b
         print(f"| {c} | {len(p['ids'])} | {nl} | {p['read'] / 1e6:.1f} | {p['write'] / 1e6:.1f} | {b / 1e6:.3f} MB |")
     res["_note"] = ("mean dram__bytes_read.sum + dram__bytes_write.sum per bench kernel-class launch (one per wave "
-                    "for per-wave classes), ncu over one timed C2 round of bench.py; scripts/gpu_evidence.sh")
+                    "for per-wave classes), ncu over one timed round of bench.py's default workload (C3); "
+                    "scripts/gpu_evidence.sh")
+    res["_source"] = f"{out}: ncu dram__bytes_read.sum + dram__bytes_write.sum over one timed bench round"
     json.dump(res, open(os.path.join(os.path.dirname(out.rstrip("/")), "ncu_traffic.json"), "w"), indent=1)
 
 
