@@ -6,9 +6,17 @@ if os.environ.get("_KNOB_CHILD"):
     import numpy as np, torch, statistics
     import synth, paper_2306_17453_b200 as fl
     out = {}
-    for name, wl in [("C2", synth.preset("C2")), ("C3x400", synth.preset("C3", n_pop=400, n_cohort=400, E=1))]:
-        sizes = synth.client_sizes(wl)
-        _, x, y = synth.population(wl, sizes)
+    sets = os.environ.get("KNOB_SETS", "C2,C3x400").split(",")
+    cfgs = {"C2": synth.preset("C2"), "C3x400": synth.preset("C3", n_pop=400, n_cohort=400, E=1), "C3": synth.preset("C3")}
+    for name in sets:
+        wl = cfgs[name]
+        if name == "C3":  # the bench workload: the cohort's 1,000 clients of the 10,000 population
+            sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+            from bench import pop_for
+            sizes, x, y, _ = pop_for(wl)
+        else:
+            sizes = synth.client_sizes(wl)
+            _, x, y = synth.population(wl, sizes)
         ctx = fl.fl_round_init(fl.Config(model="cnn", batch_size=32, lr=wl.lr), sizes, torch.from_numpy(x).cuda(),
                                torch.from_numpy(y).cuda(), synth.init_params("cnn"))
         ids = np.arange(len(sizes))

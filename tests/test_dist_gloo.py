@@ -164,3 +164,53 @@ def test_lb_loop_two_ranks_heterogeneous():
     lb_gap = abs(loads[2][0] - loads[2][1]) / max(loads[2])
     assert lb_gap < 0.1 < rr_gap, (loads, rr_gap, lb_gap)
     assert res[0][4] == pytest.approx(abs(loads[2][0] - loads[2][1]))
+
+
+# ------------------------------------------------------------------ peer-memory blob exchange (f3)
+class _BlobCtx:
+    """Stands in for a rank's fl_ctx: fl_peer_export returns a rank-stamped blob (the real one
+    carries CUDA IPC handles), fl_peer_connect records what it was given."""
+
+    def __init__(self, rank):
+        self.cfg = type("C", (), {"rank": rank})()
+        self.got = None
+        self.max_clients = None
+
+    def fl_peer_export(self, max_clients=0):
+        self.max_clients = max_clients
+        return bytes([self.cfg.rank]) * fl.PEER_BLOB_BYTES
+
+    def fl_peer_connect(self, blobs):
+        self.got = blobs
+
+
+def _blob_worker(rank, world, port, q):
+    try:
+        import bench
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        ctx = _BlobCtx(rank)
+        bench.peer_connect(ctx, world, max_clients=1000)
+        q.put((rank, [b[0] for b in ctx.got], [len(b) for b in ctx.got], ctx.max_clients))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, "error", repr(e), None))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_peer_blob_exchange_two_ranks():
+    """bench.peer_connect all-gathers every rank's blob in rank order; only the server (rank 0)
+    asks for a receive buffer (the unaggregated ablation ships client models to it)."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_blob_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    for rank, order, lens, maxc in res:
+        assert order == [0, 1], (rank, order)
+        assert lens == [fl.PEER_BLOB_BYTES] * world
+        assert maxc == (1000 if rank == 0 else 0)
