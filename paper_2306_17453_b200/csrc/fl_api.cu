@@ -831,9 +831,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   CK(grow_dev(c->d_slots, c->slots_cap, std::max<int64_t>(K, 1) * L.P_pad));
   CK(grow_dev(c->d_xpack, c->xpack_cap, std::max<int64_t>(R, 1) * L.D_pack));
   // shifted planar copies of the input exist only for the tensor-core conv1 dW
-  // shifted planar copies of the input were the tensor-core conv1 dW's A operand; conv1's dW
-  // now runs from the pooled gradient (k_c1dw_pooled4) and needs only the packed input
-  const bool want_planar = false;
+  const bool want_planar = L.model == FL_MODEL_CNN_CIFAR && c->cfg.math == 0 && conv1_tc_supported(L);
   if (want_planar)
     CK(grow_dev(c->cb.xplanar, c->cb.xplanar_cap, (c->xpack_cap / L.D_pack) * 16 * L.d.H0 * (L.d.W0 + 4)));
   CK(grow_dev(c->d_ypack, c->ypack_cap, R));

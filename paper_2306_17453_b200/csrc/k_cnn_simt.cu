@@ -437,108 +437,6 @@ __global__ void __launch_bounds__(512) k_c1dw_pooled(const float* __restrict__ d
   }
 }
 
-// conv1 dW of the CIFAR CNN (3 channels padded to 4, 32 x 32 input, 32 filters) from the pooled
-// gradient, in the balanced split-K layout of the wave (the same partials as a tensor-core dW
-// would write, reduced by k_dw_reduce2_sgd): a unit = one pooled row (16 cells) of one sample,
-// the wave's U = 16·Σ|b| units split evenly over G CTAs, CTA c writing one partial per client
-// segment of its range at z = a + c.  Pool1's backward sends each pooled cell's gradient
-// g = dp1m[ph][pw][o] (ReLU' already applied) to ONE pixel (y, x) of its window (argmax am1), so
-// dW1[o][kh][kw][ci] += g · x[y+kh-2][x+kw-2][ci] and db1[o] += g — a quarter of the dense
-// contraction, and neither dY1 nor shifted input copies exist.  Thread = (filter o = tid % 32,
-// cells pw = tid / 32 and tid / 32 + 8 of the unit); the 8 warps' sums are combined in fixed order.
-constexpr int C1P_NACC = 76;  // 25 taps x 3 channels + bias per thread
-__global__ void __launch_bounds__(256) k_c1dw_pooled4(const float* __restrict__ dp1m, const uint8_t* __restrict__ am1,
-                                                      const float* __restrict__ xpack, const int32_t* __restrict__ sidx,
-                                                      const int32_t* __restrict__ bpre, int A, int B, int G, int64_t U,
-                                                      float* __restrict__ part) {
-  pdl_wait();
-  extern __shared__ float sm[];
-  float* xr = sm;               // [6 rows][36 cols][4]: input rows 2ph-2 .. 2ph+3, columns -2 .. 33
-  float* red = sm + 6 * 36 * 4; // [8 warps][32 o][76]
-  const int c = blockIdx.x, o = threadIdx.x & 31, wq = threadIdx.x >> 5;
-  const int64_t u0 = (int64_t)c * U / G, u1 = (int64_t)(c + 1) * U / G;
-  if (u0 >= u1) return;
-  float acc[C1P_NACC];
-#pragma unroll
-  for (int j = 0; j < C1P_NACC; ++j) acc[j] = 0.f;
-  // client of the first unit
-  int a = 0;
-  {
-    const int64_t s0 = u0 / 16;
-    int lo = 0, hi = A - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (bpre[mid] <= s0) lo = mid;
-      else hi = mid - 1;
-    }
-    a = lo;
-  }
-  auto flush = [&](int aa) {
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < C1P_NACC; ++j) red[(wq * 32 + o) * C1P_NACC + j] = acc[j];
-    __syncthreads();
-    float* out = part + (int64_t)(aa + c) * 32 * 101;
-    for (int e = threadIdx.x; e < 32 * 101; e += blockDim.x) {
-      const int m = e / 101, n = e - m * 101;
-      float v = 0.f;
-      if (n == 100 || (n & 3) != 3) {
-        const int j = n == 100 ? 75 : (n >> 2) * 3 + (n & 3);
-        for (int w = 0; w < 8; ++w) v += red[(w * 32 + m) * C1P_NACC + j];
-      }
-      out[e] = v;
-    }
-#pragma unroll
-    for (int j = 0; j < C1P_NACC; ++j) acc[j] = 0.f;
-  };
-  for (int64_t u = u0; u < u1; ++u) {
-    const int64_t sg = u / 16;  // concatenated sample of the wave
-    while (sg >= bpre[a + 1]) {  // next client segment: flush the finished one
-      flush(a);
-      ++a;
-    }
-    const int ph = (int)(u % 16);
-    const int64_t slot = (int64_t)a * B + (sg - bpre[a]);
-    const float* xs = xpack + (int64_t)sidx[slot] * 32 * 32 * 4;
-    __syncthreads();  // previous unit's rows no longer read
-    for (int e = threadIdx.x; e < 6 * 36; e += blockDim.x) {
-      const int rr = e / 36, cc = e - rr * 36, y = 2 * ph - 2 + rr, x = cc - 2;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (y >= 0 && y < 32 && x >= 0 && x < 32) v = *reinterpret_cast<const float4*>(xs + (y * 32 + x) * 4);
-      *reinterpret_cast<float4*>(xr + e * 4) = v;
-    }
-    __syncthreads();
-    const int64_t cell0 = (slot * 16 + ph) * 16;  // first pooled cell of this row
-    float g[2];
-    int am[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int pw = wq + 8 * k;
-      g[k] = __ldg(dp1m + (cell0 + pw) * 32 + o);
-      am[k] = __ldg(am1 + (cell0 + pw) * 32 + o);
-    }
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      if (g[k] == 0.f) continue;
-      const int pw = wq + 8 * k;
-      const int dy = am[k] >> 1, x = 2 * pw + (am[k] & 1);  // window row 2ph + dy, column x
-      const float* xp = xr + (dy * 36 + x) * 4;            // padded row dy + kh, column x + kw
-#pragma unroll
-      for (int kh = 0; kh < 5; ++kh)
-#pragma unroll
-        for (int kw = 0; kw < 5; ++kw) {
-          const float4 v = *reinterpret_cast<const float4*>(xp + (kh * 36 + kw) * 4);
-          const int t = (kh * 5 + kw) * 3;
-          acc[t] = fmaf(g[k], v.x, acc[t]);
-          acc[t + 1] = fmaf(g[k], v.y, acc[t + 1]);
-          acc[t + 2] = fmaf(g[k], v.z, acc[t + 2]);
-        }
-      acc[75] += g[k];
-    }
-  }
-  flush(a);
-}
-
 // Σ of the split-K partials, then fused SGD on the conv weights and bias.
 // Partials: [A*nch] chunks of rpc samples (bpre == nullptr), or the balanced split-K layout
 // (bpre != nullptr): client a's partials are z = a + c for the CTAs c0..c1 covering its k-blocks
@@ -878,25 +776,12 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     ++n;
     pf.end(K_CONV2_DW, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
     pf.begin(st);
-    // conv1 dW from the pooled gradient (SIMT, a quarter of the dense work, no shifted copies):
-    // units = pooled rows, G CTAs with at least 8 units each
-    const int64_t U1 = (int64_t)d.H1 * wa.sum_bs;
-    g1 = (int)std::max<int64_t>(1, std::min<int64_t>(4 * (int64_t)wa.sms, U1 / 8));
-    if ((int64_t)A + g1 > b.part1_tc_cap) return -1;
-    {
-      const size_t sm = sizeof(float) * (6 * 36 * 4 + 8 * 32 * C1P_NACC);
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(k_c1dw_pooled4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        attr = true;
-      }
-      launch_pdl(wa.pdl, k_c1dw_pooled4, dim3(g1), 256, sm, st, b.dp1, b.am1, xpack, wa.sidx, wa.bpre, A, B, g1, U1,
-                 b.part1);
-    }
+    if (conv1_dw_tc(L, wa, b.xplanar, b.xrows, b.dp1, b.am1, b.slots, b.part1, b.part1_tc_cap, &g1, st) < 0)
+      return -1;
     ++n;
-    pf.end(K_CONV1_DW, f_c1, 4.0 * S * hw0 * d.cpad + 5.0 * S * hw1 * d.C1, st);
+    pf.end(K_CONV1_DW, f_c1, 4.0 * S * hw0 * d.cin + 5.0 * S * hw1 * d.C1, st);
     const int N2 = 25 * d.C1 + 1, N1 = 25 * d.cpad + 1;
-    DwRed r1{b.part1, d.C1, N1, L.o_c1w, L.o_c1b, b.c1wt, g1, U1, d.H1, (d.C1 * N1 + 255) / 256};
+    DwRed r1{b.part1, d.C1, N1, L.o_c1w, L.o_c1b, b.c1wt, g1, (int64_t)d.H0 * wa.sum_bs, d.H0, (d.C1 * N1 + 255) / 256};
     const int kps2 = conv2_dw_kps(L);
     DwRed r2{b.part2, d.C2, N2, L.o_c2w, L.o_c2b, nullptr, g2, (int64_t)kps2 * wa.sum_bs, kps2, (d.C2 * N2 + 255) / 256};
     pf.begin(st);

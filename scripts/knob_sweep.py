@@ -17,7 +17,7 @@ if os.environ.get("_KNOB_CHILD"):
         else:
             sizes = synth.client_sizes(wl)
             _, x, y = synth.population(wl, sizes)
-        ctx = fl.fl_round_init(fl.Config(model="cnn", batch_size=32, lr=wl.lr), sizes, torch.from_numpy(x).cuda(),
+        ctx = fl.fl_round_init(fl.Config(model="cnn", batch_size=32, local_epochs=wl.E, lr=wl.lr), sizes, torch.from_numpy(x).cuda(),
                                torch.from_numpy(y).cuda(), synth.init_params("cnn"))
         ids = np.arange(len(sizes))
         for i in range(3):
