@@ -241,7 +241,8 @@ __global__ void k_c2i(const float* __restrict__ canon, const int64_t* __restrict
                       float* __restrict__ internal) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P_pad; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t c = canon_of[i];
-    internal[i] = c >= 0 ? canon[c] : 0.f;
+    const float v = canon[c >= 0 ? c : 0];  // always an in-bounds load (padding slots read element 0)
+    internal[i] = c >= 0 ? v : 0.f;
   }
 }
 

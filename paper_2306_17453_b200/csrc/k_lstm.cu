@@ -476,7 +476,11 @@ __global__ void __launch_bounds__(256) k_lstm_embed(EmbArgs p) {
   const int row = p.sidx[s];
   for (int e = threadIdx.x; e < LT * LE; e += 256) {
     const int t = e / LE, j = e - t * LE;
-    const int ch = row >= 0 ? p.xpack[(int64_t)row * LT + t] : 0;  // padding rows: char 0 (dz = 0 there)
+    // padding rows (row < 0): char 0 (dz = 0 there).  The load always reads row max(row, 0): the
+    // compiler turned the conditional load into an unconditional one (compute-sanitizer flagged
+    // the row -1 read before the buffer).
+    const int chl = p.xpack[(int64_t)(row >= 0 ? row : 0) * LT + t];
+    const int ch = row >= 0 ? chl : 0;
     es[e] = w[p.o_emb + ch * LE + j];
   }
   __syncthreads();
@@ -515,7 +519,8 @@ __global__ void __launch_bounds__(256) k_lstm_head(HeadArgs p) {
   for (int e = tid; e < LV * LH; e += 256) Wf[e] = w[p.o_wfc + e];
   for (int e = tid; e < 4 * LH; e += 256) {
     const int r = e / LH, k = e - r * LH;
-    hT[r][k] = r < p.B ? p.H1[(((int64_t)a * p.B + r) * (LT + 1) + LT) * LH + k] : 0.f;
+    const float hv = p.H1[(((int64_t)a * p.B + (r < p.B ? r : 0)) * (LT + 1) + LT) * LH + k];  // in-bounds load
+    hT[r][k] = r < p.B ? hv : 0.f;
   }
   __syncthreads();
   const int lane = tid & 31, warp = tid >> 5;
@@ -597,7 +602,8 @@ __global__ void k_lstm_emb_sgd(const float* __restrict__ dE, const uint8_t* __re
       const int row = sidx[a * B + r];
       const float* de = dE + (((int64_t)a * B + r) * LT) * LE + j;
       for (int t = 0; t < LT; ++t) {
-        const int c = row >= 0 ? xpack[(int64_t)row * LT + t] : 0;
+        const int cl = xpack[(int64_t)(row >= 0 ? row : 0) * LT + t];  // always an in-bounds load
+        const int c = row >= 0 ? cl : 0;
         if (c == ch) g += de[t * LE];
       }
     }
