@@ -103,8 +103,8 @@ CnnBufs cnn_group_view(const CnnBufs& b, const CnnDims& d, int B, int64_t base_c
   CnnBufs v = b;
   const int64_t s0 = base_client * B;
   const int64_t hw0 = (int64_t)d.H0 * d.W0, hw1 = (int64_t)d.H1 * d.W1, hw2 = (int64_t)d.H2 * d.W2;
-  v.a1 = b.a1 + s0 * hw0 * d.C1;
-  v.dY1 = b.dY1 + s0 * hw0 * d.C1;
+  v.a1 = b.a1 ? b.a1 + s0 * hw0 * d.C1 : nullptr;  // full-resolution planes: SIMT path only
+  v.dY1 = b.dY1 ? b.dY1 + s0 * hw0 * d.C1 : nullptr;
   v.p1 = b.p1 + s0 * hw1 * d.C1;
   v.am1 = b.am1 + s0 * hw1 * d.C1;
   v.dp1 = b.dp1 + s0 * hw1 * d.C1;
@@ -869,8 +869,14 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       for (void* p : old)
         if (p) cudaFree(p);
       const int64_t hw0 = (int64_t)d.H0 * d.W0, hw1 = (int64_t)d.H1 * d.W1, hw2 = (int64_t)d.H2 * d.W2;
-      CK(cudaMalloc(&b.a1, sizeof(float) * S * hw0 * d.C1));
-      CK(cudaMalloc(&b.dY1, sizeof(float) * S * hw0 * d.C1));
+      // the full-resolution conv1 planes (pre-pool activation, its gradient) exist only on the
+      // FP32 SIMT path: the tensor-core / fused paths pool in conv1's epilogue and take conv1's
+      // dW from the pooled gradient (4.2 GB each at C3 on one GPU)
+      b.a1 = b.dY1 = nullptr;
+      if (c->cfg.math != 0) {
+        CK(cudaMalloc(&b.a1, sizeof(float) * S * hw0 * d.C1));
+        CK(cudaMalloc(&b.dY1, sizeof(float) * S * hw0 * d.C1));
+      }
       CK(cudaMalloc(&b.p1, sizeof(float) * S * hw1 * d.C1));
       CK(cudaMalloc(&b.am1, S * hw1 * d.C1));
       CK(cudaMalloc(&b.dp1, sizeof(float) * S * hw1 * d.C1));
@@ -887,7 +893,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       CK(cudaMemsetAsync(b.dh, 0, sizeof(float) * S * d.HID, c->st));
       CK(cudaMemsetAsync(b.p1, 0, sizeof(float) * S * hw1 * d.C1, c->st));
       CK(cudaMemsetAsync(b.dY2, 0, sizeof(float) * S * hw1 * d.C2, c->st));
-      CK(cudaMemsetAsync(b.dY1, 0, sizeof(float) * S * hw0 * d.C1, c->st));
+      if (b.dY1) CK(cudaMemsetAsync(b.dY1, 0, sizeof(float) * S * hw0 * d.C1, c->st));
       c->cb_slots_cap = S;
       b.slots = S;
     }
