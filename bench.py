@@ -230,39 +230,40 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def cpu_baseline(wl, sizes, x, y, theta, budget_samples, threads=0, seed=1):
+def cpu_baseline(wl, sizes, x, y, theta, max_client=64, threads=0, seed=1):
     """The oracle, as it stands, on a bounded random sample of the workload's clients.
 
-    The sample holds at least 2 clients per host thread (so every thread has work; the oracle
-    runs one OpenMP task per client) and ~budget_samples samples, issued largest-first.
-    client-updates/s = (sample samples/s) / (mean client samples per round); `cores` = the
-    threads that actually had a client.  A second, single-thread timing of the first client
-    is reported as `single_thread`."""
+    The fp64 oracle trains ~8 sample-steps per second per host thread on the CIFAR CNN, so one
+    average C3 client (~480 sample-steps) alone is about a minute of one core.  To keep a step at
+    ~10 s of wall time on all cores the sample is `threads` random clients of the cohort among
+    those with n <= max_client samples (one OpenMP task per client, largest first), and
+    client-updates/s = (sample-steps/s) / (mean sample-steps of a client of the whole workload):
+    the oracle's cost per sample-step does not depend on the client's size.  `cores` = the
+    threads that had a client.  A second, single-thread timing of one client is reported as
+    `single_thread`."""
     import oracle
     threads = threads or cpu_threads()
     rng = np.random.default_rng(seed)
-    order = rng.permutation(len(sizes))
-    pick, tot = [], 0
-    for c in order:
-        if tot >= budget_samples and len(pick) >= 2 * threads:
-            break
-        pick.append(int(c))
-        tot += int(sizes[c])
-    pick = sorted(pick, key=lambda c: -int(sizes[c]))
+    order = [int(c) for c in rng.permutation(len(sizes)) if sizes[c] <= max_client]
+    if not order:
+        order = [int(np.argmin(sizes))]
+    pick = sorted(order[:threads], key=lambda c: -int(sizes[c]))
+    tot = int(sizes[pick].sum())
     pop_off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
     mean_client = float(np.mean(sizes)) * wl.E
     t0 = time.perf_counter()
     _, used = oracle.train_clients(wl.model, theta, x, y, pop_off, np.array(pick), wl.B, wl.E, wl.lr, threads=threads)
     dt = time.perf_counter() - t0
     value = tot * wl.E / dt / mean_client
-    small = min(pick, key=lambda c: int(sizes[c]))
+    small = pick[-1]
     t1 = time.perf_counter()
     oracle.train_clients(wl.model, theta, x, y, pop_off, np.array([small]), wl.B, wl.E, wl.lr, threads=1)
     dt1 = time.perf_counter() - t1
-    return {"value": value, "unit": UNIT, "cores": int(min(used, len(pick))), "kind": "oracle",
-            "sample": f"{len(pick)} random clients of the cohort ({tot} samples x E={wl.E}), largest first, trained "
-                      f"by the fp64 oracle on {min(used, len(pick))} host threads in {dt:.1f} s; client-updates/s = "
-                      f"samples/s / mean client samples per round ({mean_client:.1f})",
+    cores = int(min(used, len(pick)))
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{len(pick)} random clients of the cohort with n <= {max_client} ({tot} samples x E={wl.E}), "
+                      f"largest first, trained by the fp64 oracle on {cores} host threads in {dt:.1f} s; "
+                      f"client-updates/s = sample-steps/s / mean sample-steps of a workload client ({mean_client:.1f})",
             "seconds": dt, "host_threads": int(threads),
             "single_thread": {"value": int(sizes[small]) * wl.E / dt1 / mean_client, "unit": UNIT, "cores": 1,
                               "sample": f"1 client ({int(sizes[small])} samples x E={wl.E}) in {dt1:.2f} s"}}
@@ -318,7 +319,7 @@ def run_reference(args, world, rank):
     theta = synth.init_params(wl.model)
     vals = []
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(wl, sizes, x, y, theta, budget_samples=args.ref_samples, seed=1 + i)
+        cb = cpu_baseline(wl, sizes, x, y, theta, max_client=args.ref_max_client, seed=1 + i)
         if i >= args.warmup:
             vals.append(cb)
     v = statistics.median(c["value"] for c in vals)
@@ -383,8 +384,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the configs[1] (C2) measurement at N = 1")
-    ap.add_argument("--cpu-samples", type=int, default=400)
-    ap.add_argument("--ref-samples", type=int, default=200)
+    ap.add_argument("--cpu-max-client", type=int, default=64,
+                    help="cpu_baseline samples clients with at most this many samples (~10 s per step)")
+    ap.add_argument("--ref-max-client", type=int, default=48,
+                    help="--impl reference: the same, per step (K + W steps must end within minutes)")
     ap.add_argument("--agg", default="nccl", choices=["nccl", "peer", "unaggregated"],
                     help="cross-rank aggregation (include/fl.h agg_mode): NCCL allreduce of partials, one "
                          "peer-memory kernel, or the unaggregated ablation (all client models to rank 0)")
@@ -484,7 +487,7 @@ def main():
         del x2d, y2d
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(wl, sizes, x, y, theta, args.cpu_samples)
+        cpu = cpu_baseline(wl, sizes, x, y, theta, args.cpu_max_client)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
