@@ -495,9 +495,14 @@ def main():
                 "step_ms": {"median": statistics.median(per_step), "p10": pct(per_step, 10),
                             "p90": pct(per_step, 90), "max_over_ranks": True},
                 # speech and LSTM run FP32 SIMT kernels; CNN GEMMs TF32
-                "dtype": "f32" if (args.math == 1 or wl.model in ("lstm", "speech", "logreg")) else "tf32",
-                "precision_note": "tensor-core GEMM operands tf32, fp32 accumulate; fp32 master weights, SGD, "
-                                  "softmax-CE; fp64 FedAvg accumulation",
+                # logreg and math = 1 run FP32 CUDA-core kernels; the CNNs' and the LSTM's GEMMs run
+                # on tcgen05 with TF32 operands (the LSTM recurrences stay FP32, R15)
+                "dtype": "f32" if (args.math == 1 or wl.model == "logreg") else "tf32",
+                "precision_note": ("FP32 CUDA-core kernels; fp64 FedAvg accumulation" if (args.math == 1 or
+                                   wl.model == "logreg") else
+                                   "tensor-core GEMM operands tf32, fp32 accumulate; fp32 master weights, SGD, "
+                                   "softmax-CE" + ("; LSTM recurrences fp32" if wl.model == "lstm" else "") +
+                                   "; fp64 FedAvg accumulation"),
                 "data": "synthetic (seeded, SURVEY §8d laws), device-resident",
                 "config": run_config(wl, desc, cohort, sizes, world, args.agg),
                 "round_stats": {k: st[k] for k in ["round_ms", "round_ms_max", "place_ms", "stage_ms", "train_ms",
