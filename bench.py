@@ -404,12 +404,16 @@ def main():
     wl, desc, scaling = workload(world, args.config)
     sizes, x, y, cohort = pop_for(wl)
     theta = synth.init_params(wl.model)
-    uid = None
-    if world > 1 and args.agg == "nccl":
+    def new_uid():
+        """A fresh NCCL unique id from rank 0 (one per communicator: an id is not reused)."""
+        if world == 1 or args.agg != "nccl":
+            return None
         import torch.distributed as dist
         obj = [fl.fl_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
+        return obj[0]
+
+    uid = new_uid()
     cfg = fl.Config(model=wl.model, batch_size=wl.B, local_epochs=wl.E, lr=wl.lr, shuffle=wl.shuffle, seed=wl.seed,
                     rank=rank, world_size=world, device=local, nccl_unique_id=uid, math=args.math,
                     agg_mode=args.agg)
@@ -445,6 +449,7 @@ def main():
     # e2e: the public API with HOST buffers; H2D of this rank's cohort rows and D2H of θ_new per step
     e2e = None
     if not args.no_e2e:
+        cfg.nccl_unique_id = new_uid()
         ctx2 = fl.fl_round_init(cfg, sizes, x, y, theta, on_device=False)
         if args.agg != "nccl":
             peer_connect(ctx2, world, len(cohort))
