@@ -484,9 +484,38 @@ struct DwRed {
   int64_t U;
   int kbps, nblk;
 };
-__global__ void __launch_bounds__(256) k_dw_reduce2_sgd(DwRed r1, DwRed r2, const int32_t* __restrict__ bpre, WSrc w,
-                                                        float* dst, int64_t P_pad, float lr) {
+// fc2 (classifier) SGD folded into the wave's final reduction launch: W2[q][n] -= η Σ_r dz[r][q] h[r][n],
+// b2[q] -= η Σ_r dz[r][q] (the same fmaf chain in r as k_head_sgd).  Nothing reads W2 between the
+// head's forward and the end of the wave, so the update can wait until here.
+struct HeadSgd {
+  const float* h;       // [slots][HID] fc1 activations of the wave
+  const float* dz;      // [slots][NCLS] softmax-CE gradient of the logits
+  const int32_t* bs;
+  int B, HID, NCLS;
+  int64_t o_w, o_b;
+  int nblk;
+};
+__global__ void __launch_bounds__(256) k_dw_reduce2_sgd(DwRed r1, DwRed r2, HeadSgd hd, const int32_t* __restrict__ bpre,
+                                                        WSrc w, float* dst, int64_t P_pad, float lr) {
   pdl_wait();
+  if ((int)blockIdx.x >= r1.nblk + r2.nblk) {  // fc2 SGD
+    const int a = blockIdx.y, b = hd.bs[a];
+    const int e = ((int)blockIdx.x - r1.nblk - r2.nblk) * blockDim.x + threadIdx.x;
+    const float* dzz = hd.dz + (int64_t)a * hd.B * hd.NCLS;
+    const float* hz = hd.h + (int64_t)a * hd.B * hd.HID;
+    if (e < hd.NCLS * hd.HID) {
+      const int q = e / hd.HID, n = e - q * hd.HID;
+      float g = 0.f;
+      for (int r = 0; r < b; ++r) g = fmaf(__ldg(dzz + r * hd.NCLS + q), __ldg(hz + (int64_t)r * hd.HID + n), g);
+      dst[(int64_t)a * P_pad + hd.o_w + e] = *w.at(a, hd.o_w + e) - lr * g;
+    } else if (e < hd.NCLS * hd.HID + hd.NCLS) {
+      const int q = e - hd.NCLS * hd.HID;
+      float g = 0.f;
+      for (int r = 0; r < b; ++r) g += __ldg(dzz + r * hd.NCLS + q);
+      dst[(int64_t)a * P_pad + hd.o_b + q] = *w.at(a, hd.o_b + q) - lr * g;
+    }
+    return;
+  }
   const bool second = (int)blockIdx.x >= r1.nblk;
   const DwRed& r = second ? r2 : r1;
   const int bx = second ? (int)blockIdx.x - r1.nblk : (int)blockIdx.x;
@@ -734,8 +763,11 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   pf.begin(st);
   launch_pdl(wa.pdl, k_head_fwd, dim3(A, (B + HR - 1) / HR), 256, hsm, st, b.h, ypack, wa.sidx, wa.bs, B, d.HID, d.NCLS, w, L.o_f2w,
                                                           L.o_f2b, b.dz, b.dh), ++n;
-  launch_pdl(wa.pdl, k_head_sgd, dim3(A, (d.HID + 63) / 64), 256, sizeof(float) * B * (d.NCLS + 64), st, b.h, b.dz, wa.bs, B, d.HID, d.NCLS, w, L.o_f2w, L.o_f2b,
-                                                          slots, L.P_pad, wa.lr), ++n;
+  // the CIFAR tensor-core path does the fc2 SGD in the wave's final reduction (k_dw_reduce2_sgd)
+  const bool fold_head_sgd = wa.use_tc && conv_tc_supported(L) && conv1_tc_supported(L);
+  if (!fold_head_sgd)
+    launch_pdl(wa.pdl, k_head_sgd, dim3(A, (d.HID + 63) / 64), 256, sizeof(float) * B * (d.NCLS + 64), st, b.h, b.dz,
+               wa.bs, B, d.HID, d.NCLS, w, L.o_f2w, L.o_f2b, slots, L.P_pad, wa.lr), ++n;
   pf.end(K_HEAD, 3.0 * f_f2, 8.0 * A * d.NCLS * d.HID + 8.0 * S * d.HID, st);
   // ---- backward (each layer's dX reads W before its dW epilogue overwrites it)
   pf.begin(st);
@@ -784,9 +816,10 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     DwRed r1{b.part1, d.C1, N1, L.o_c1w, L.o_c1b, b.c1wt, g1, (int64_t)d.H0 * wa.sum_bs, d.H0, (d.C1 * N1 + 255) / 256};
     const int kps2 = conv2_dw_kps(L);
     DwRed r2{b.part2, d.C2, N2, L.o_c2w, L.o_c2b, nullptr, g2, (int64_t)kps2 * wa.sum_bs, kps2, (d.C2 * N2 + 255) / 256};
+    HeadSgd hd{b.h, b.dz, wa.bs, B, d.HID, d.NCLS, L.o_f2w, L.o_f2b, (d.NCLS * d.HID + d.NCLS + 255) / 256};
     pf.begin(st);
-    launch_pdl(wa.pdl, k_dw_reduce2_sgd, dim3(r1.nblk + r2.nblk, A), 256, 0, st, r1, r2, wa.bpre, w, slots, L.P_pad,
-               wa.lr), ++n;
+    launch_pdl(wa.pdl, k_dw_reduce2_sgd, dim3(r1.nblk + r2.nblk + hd.nblk, A), 256, 0, st, r1, r2, hd, wa.bpre, w, slots,
+               L.P_pad, wa.lr), ++n;
     pf.end(K_CONV2_DWR, 0, 8.0 * A * (d.C2 * 25 * d.C1 + d.C1 * 25 * d.cin), st);
     return n;
   }
