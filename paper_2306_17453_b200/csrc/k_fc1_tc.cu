@@ -252,13 +252,6 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           for (int j = 0; j < 4; ++j)
             tc::tma_load_3d(sw + j * 16384, &mapWsrc, full + st, 128 * kt + 32 * j, 128 * c, a * p.wmul);
           tc::tma_load_3d(sw + BW_W, &mapDht, full + st, 0, a * p.B, 4 * c);
-          // two chunks ahead into L2 (this tile's c + 2, or the next tile's): with only two smem
-          // stages the HBM requests in flight per SM would otherwise be one 64 KB chunk
-          const int tn = c + 2 < nch ? t : t + gridDim.x, cn = c + 2 < nch ? c + 2 : c + 2 - nch;
-          if (tn < T) {
-            const int an = tn / KT, ktn = tn % KT;
-            for (int j = 0; j < 4; ++j) tc::tma_prefetch_3d(&mapWsrc, 128 * ktn + 32 * j, 128 * cn, an * p.wmul);
-          }
         }
       }
     }
