@@ -123,7 +123,6 @@ CnnBufs cnn_group_view(const CnnBufs& b, const CnnDims& d, int B, int64_t base_c
   v.part2_tc_cap = per_group_z;
   v.part1_tc_cap = per_group_z;
   v.fc1_part = b.fc1_part + (int64_t)g * b.fc1_part_floats;
-  v.c1wt = b.c1wt ? b.c1wt + base_client * C1WT_FLOATS : nullptr;
   return v;
 }
 
@@ -443,7 +442,7 @@ void fl_round_destroy(fl_ctx* c) {
   void* ptrs[] = {c->d_theta, c->d_canon_of, c->d_canon, c->d_slots, c->d_S, c->d_xpack, c->d_ypack, c->d_stage,
                   c->d_ystage, c->d_src_row, c->d_n, c->d_steps, c->d_slot_off, c->ws.d_sidx, c->ws.d_bs, c->ws.d_bpre,
                   c->cb.a1, c->cb.p1, c->cb.a2, c->cb.p2, c->cb.h, c->cb.dh, c->cb.am1, c->cb.am2, c->cb.dp2,
-                  c->cb.dY2, c->cb.dp1, c->cb.dY1, c->cb.part1, c->cb.part2, c->cb.xplanar, c->cb.fc1_part, c->cb.c1wt, c->cb.c1wt_g,
+                  c->cb.dY2, c->cb.dp1, c->cb.dY1, c->cb.part1, c->cb.part2, c->cb.xg, c->cb.fc1_part,
                   c->cb.dz, c->lb.xp, c->lb.G0, c->lb.G1, c->lb.dpre, c->lb.C0, c->lb.C1, c->lb.H0, c->lb.H1,
                   c->lb.dX, c->lb.E, c->lb.dE, c->lb.dhT};
   for (void* p : ptrs)
@@ -833,7 +832,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   // shifted planar copies of the input exist only for the tensor-core conv1 dW
   const bool want_planar = L.model == FL_MODEL_CNN_CIFAR && c->cfg.math == 0 && conv1_tc_supported(L);
   if (want_planar)
-    CK(grow_dev(c->cb.xplanar, c->cb.xplanar_cap, (c->xpack_cap / L.D_pack) * 16 * L.d.H0 * (L.d.W0 + 4)));
+    CK(grow_dev(c->cb.xg, c->cb.xg_cap, (c->xpack_cap / L.D_pack) * conv1_xg_floats()));
   CK(grow_dev(c->d_ypack, c->ypack_cap, R));
   CK(grow_dev(c->d_src_row, c->src_cap, R));
   CK(grow_dev(c->d_n, c->n_cap, K));
@@ -912,14 +911,6 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       c->cb_part_cap = pg * NG;
     }
     c->part_group_z = pg;
-    if (K > b.c1wt_cap) {  // pad taps must read as zero: cleared once per allocation
-      if (b.c1wt) cudaFree(b.c1wt);
-      b.c1wt = nullptr;
-      CK(cudaMalloc(&b.c1wt, sizeof(float) * K * C1WT_FLOATS));
-      b.c1wt_cap = K;
-      CK(cudaMemsetAsync(b.c1wt, 0, sizeof(float) * K * C1WT_FLOATS, c->st));
-    }
-    if (!b.c1wt_g) CK(cudaMalloc(&b.c1wt_g, sizeof(float) * C1WT_FLOATS));
   }
   c->place_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() -
                  c->tab_wait_ms;
@@ -977,7 +968,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       if (nq > 0) {
         if (cnn)
           launches += pack_cnn(L, c->d_stage + q0 * L.D_in, nullptr, nq, c->d_xpack + q0 * L.D_pack,
-                               want_planar ? c->cb.xplanar + q0 * 16 * L.d.H0 * (L.d.W0 + 4) : nullptr, ps);
+                               want_planar ? c->cb.xg + q0 * conv1_xg_floats() : nullptr, ps);
         else
           launches += gather_rows_f32(c->d_stage + q0 * L.D_in, nullptr, nq, L.D_pack, c->d_xpack + q0 * L.D_pack,
                                       ps);
@@ -1005,11 +996,10 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
     // one chunk: everything waits for it; several: each group waits for its own rows (wave loop)
     if (NQ == 1) CK(cudaStreamWaitEvent(st, c->ev_chunk[0], 0));
   } else {
-    if (cnn) launches += pack_cnn(L, xsrc, srow, R, c->d_xpack, want_planar ? c->cb.xplanar : nullptr, st);
+    if (cnn) launches += pack_cnn(L, xsrc, srow, R, c->d_xpack, want_planar ? c->cb.xg : nullptr, st);
     else launches += gather_rows_f32(xsrc, srow, R, L.D_pack, c->d_xpack, st);
     launches += gather_i32(ysrc, srow, R, c->d_ypack, st);
   }
-  if (cnn && c->cfg.math == 0 && conv1_tc_supported(L)) launches += c1wt_pack(c->d_theta + L.o_c1w, c->cb.c1wt_g, st);
   c->prof.end(K_PACK, 0, (double)R * (4.0 * (L.D_in + L.D_pack) + 8.0), st);
   CKL();
   CK(cudaEventRecord(c->ev_staged, st));

@@ -109,13 +109,10 @@ struct CnnBufs {
   int64_t part2_tc_cap = 0;                   // conv2 dW tensor-core partials capacity (chunks)
   int64_t part1_tc_cap = 0;                   // conv1 dW tensor-core partials capacity (chunks)
   int64_t xrows = 0;                          // rows of the packed input (TMA extent)
-  float* xplanar = nullptr;                   // 4 shifted planar copies [xrows][4 s][4 c][H0][W0+4]
+  float* xg = nullptr;                        // conv1 window layout [xrows][conv1_xg_floats()]
   float* fc1_part = nullptr;                  // fc1 forward split-K partials
   int64_t fc1_part_floats = 0;
-  int64_t xplanar_cap = 0;
-  float* c1wt = nullptr;    // [client slot][C1WT_FLOATS] tap-major conv1 weights (written by the SGD)
-  float* c1wt_g = nullptr;  // [C1WT_FLOATS] the same for θ_g (first wave)
-  int64_t c1wt_cap = 0;
+  int64_t xg_cap = 0;
 };
 
 // The buffers of one client group: every per-slot pointer advanced to the group's first
@@ -205,13 +202,14 @@ int conv2_dw_reduce_tc(const Layout& L, const WaveArgs& wa, const float* wsrc, i
 int64_t conv2_dw_tc_part_z(int64_t max_clients);
 int64_t conv2_dw_tc_z_floats();
 bool conv1_tc_supported(const Layout& L);
-// conv1 forward B operand: per-client tap-major weights [kw][kh = 0..5][32 o][4 c] (pad tap zero)
-constexpr int C1WT_FLOATS = 30 * 32 * 4;
-int c1wt_pack(const float* c1w, float* out, cudaStream_t st);
-int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, const float* wt, const float* xpack,
+// conv1 on tensor cores reads the input in the window layout xg (k_conv1_tc.cu):
+// [row][36 padded rows][8 windows][8 px][4 c], conv1_xg_floats() floats per packed row.
+int64_t conv1_xg_floats();
+int pack_xg(const float* xpack, int64_t rows, float* xg, cudaStream_t st);
+int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wstride, const float* xg,
                  int64_t xrows, float* p1, uint8_t* am1, cudaStream_t st);
 // conv1 dW partials; dY1 is expanded on chip from dp1m and pool1's argmax am1
-int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xplanar, int64_t xrows, const float* dp1m,
+int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xg, int64_t xrows, const float* dp1m,
                 const uint8_t* am1, int64_t slots, float* part, int64_t part_cap, int* g_out, cudaStream_t st);
 bool fc1_tc_supported(const Layout& L, int B);
 int fc1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wclients, const float* p2,
@@ -229,7 +227,7 @@ int logreg_train(const Layout& L, const WaveSched& ws, int n_local, int B, float
                  const int32_t* ypack, const float* theta_g, float* slots, const int32_t* steps_dev,
                  const int64_t* wave_slot_off_dev, cudaStream_t st);
 int pack_cnn(const Layout& L, const float* x_src, const int64_t* src_row, int64_t rows, float* xpack,
-             float* xplanar, cudaStream_t st);
+             float* xg, cudaStream_t st);
 int gather_rows_f32(const float* src, const int64_t* src_row, int64_t rows, int64_t dim, float* dst,
                     cudaStream_t st);
 int gather_i32(const int32_t* src, const int64_t* src_row, int64_t rows, int32_t* dst, cudaStream_t st);

@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(512) k_c1dw_pooled(const float* __restrict__ d
 // [kbps·bpre[a], kbps·bpre[a+1]) of U, split evenly over G CTAs.
 __global__ void k_dw_reduce_sgd(const float* __restrict__ part, int nch, int rpc, const int32_t* __restrict__ bs,
                                 int O, int N, WSrc w, int64_t o_w, int64_t o_b, float* dst, int64_t P_pad, float lr,
-                                float* __restrict__ wt, const int32_t* __restrict__ bpre, int G, int64_t U, int kbps) {
+                                const int32_t* __restrict__ bpre, int G, int64_t U, int kbps) {
   pdl_wait();  // (PDL) previous kernel's writes visible; the implicit trigger is at exit
   const int a = blockIdx.y;
   const int tot = O * N;
@@ -465,10 +465,6 @@ __global__ void k_dw_reduce_sgd(const float* __restrict__ part, int nch, int rpc
     const int64_t off = n < N - 1 ? o_w + (int64_t)m * (N - 1) + n : o_b + m;
     const float nv = *w.at(a, off) - lr * g;
     dst[(int64_t)a * P_pad + off] = nv;
-    if (wt && n < N - 1) {  // conv1 (cpad = 4): also the forward's tap-major copy
-      const int tap = n >> 2, kh = tap / 5, kw = tap - kh * 5;
-      wt[(int64_t)a * C1WT_FLOATS + ((kw * 6 + kh) * 32 + m) * 4 + (n & 3)] = nv;
-    }
   }
 }
 
@@ -479,7 +475,6 @@ struct DwRed {
   const float* part;
   int O, N;
   int64_t o_w, o_b;
-  float* wt;
   int G;
   int64_t U;
   int kbps, nblk;
@@ -529,10 +524,6 @@ __global__ void __launch_bounds__(256) k_dw_reduce2_sgd(DwRed r1, DwRed r2, Head
     const int64_t off = n < r.N - 1 ? r.o_w + (int64_t)m * (r.N - 1) + n : r.o_b + m;
     const float nv = *w.at(a, off) - lr * g;
     dst[(int64_t)a * P_pad + off] = nv;
-    if (r.wt && n < r.N - 1) {
-      const int tap = n >> 2, kh = tap / 5, kw = tap - kh * 5;
-      r.wt[(int64_t)a * C1WT_FLOATS + ((kw * 6 + kh) * 32 + m) * 4 + (n & 3)] = nv;
-    }
   }
 }
 
@@ -696,7 +687,7 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   const bool tc1 = wa.use_tc && conv1_tc_supported(L);
   pf.begin(st);
   if (tc1) {  // bias + ReLU + pool fused into the epilogue
-    if (conv1_fwd_tc(L, wa, w.base, wa.first ? b.c1wt_g : b.c1wt, xpack, b.xrows, b.p1, b.am1, st) < 0) return -1;
+    if (conv1_fwd_tc(L, wa, w.base, w.stride, b.xg, b.xrows, b.p1, b.am1, st) < 0) return -1;
     ++n;
     pf.end(K_CONV1_FWD, f_c1, 4.0 * S * hw0 * d.cin + 5.0 * S * hw1 * d.C1, st);
   } else if (wa.use_tc && d.cin == 1 && d.C1 == 32) {  // speech: conv1 + bias + ReLU + pool in one pass
@@ -808,14 +799,14 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     ++n;
     pf.end(K_CONV2_DW, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
     pf.begin(st);
-    if (conv1_dw_tc(L, wa, b.xplanar, b.xrows, b.dp1, b.am1, b.slots, b.part1, b.part1_tc_cap, &g1, st) < 0)
+    if (conv1_dw_tc(L, wa, b.xg, b.xrows, b.dp1, b.am1, b.slots, b.part1, b.part1_tc_cap, &g1, st) < 0)
       return -1;
     ++n;
     pf.end(K_CONV1_DW, f_c1, 4.0 * S * hw0 * d.cin + 5.0 * S * hw1 * d.C1, st);
     const int N2 = 25 * d.C1 + 1, N1 = 25 * d.cpad + 1;
-    DwRed r1{b.part1, d.C1, N1, L.o_c1w, L.o_c1b, b.c1wt, g1, (int64_t)d.H0 * wa.sum_bs, d.H0, (d.C1 * N1 + 255) / 256};
+    DwRed r1{b.part1, d.C1, N1, L.o_c1w, L.o_c1b, g1, 2 * wa.sum_bs, 2, (d.C1 * N1 + 255) / 256};  // half-sample tiles
     const int kps2 = conv2_dw_kps(L);
-    DwRed r2{b.part2, d.C2, N2, L.o_c2w, L.o_c2b, nullptr, g2, (int64_t)kps2 * wa.sum_bs, kps2, (d.C2 * N2 + 255) / 256};
+    DwRed r2{b.part2, d.C2, N2, L.o_c2w, L.o_c2b, g2, (int64_t)kps2 * wa.sum_bs, kps2, (d.C2 * N2 + 255) / 256};
     HeadSgd hd{b.h, b.dz, wa.bs, B, d.HID, d.NCLS, L.o_f2w, L.o_f2b, (d.NCLS * d.HID + d.NCLS + 255) / 256};
     pf.begin(st);
     launch_pdl(wa.pdl, k_dw_reduce2_sgd, dim3(r1.nblk + r2.nblk + hd.nblk, A), 256, 0, st, r1, r2, hd, wa.bpre, w, slots,
@@ -840,7 +831,7 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     pf.end(K_CONV2_DW, f_c2, 4.0 * S * hw1 * (d.C1 + d.C2), st);
     pf.begin(st);
     launch_pdl(wa.pdl, k_dw_reduce_sgd, dim3(16, A), 256, 0, st, b.part2, b.nch, rpc, wa.bs, d.C2, 25 * d.C1 + 1, w, L.o_c2w,
-                                                 L.o_c2b, slots, L.P_pad, wa.lr, nullptr, nullptr, 0, 0, 0), ++n;
+                                                 L.o_c2b, slots, L.P_pad, wa.lr, nullptr, 0, 0, 0), ++n;
     pf.end(K_CONV2_DWR, 0, 8.0 * A * d.C2 * 25 * d.C1, st);
   }
   int nch1 = b.nch, rpc1 = rpc, g1 = 0;
@@ -861,7 +852,7 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
     launch_pdl(wa.pdl, k_c1dw_pooled, dim3(b.nch, A), 512, sm, st, b.dp1, b.am1, xpack, wa.sidx, wa.bs, B, d.H0,
                d.W0, b.nch, rpc, b.part1), ++n;
   } else if (tc1) {
-    if (conv1_dw_tc(L, wa, b.xplanar, b.xrows, b.dp1, b.am1, b.slots, b.part1, b.part1_tc_cap, &g1, st) < 0)
+    if (conv1_dw_tc(L, wa, b.xg, b.xrows, b.dp1, b.am1, b.slots, b.part1, b.part1_tc_cap, &g1, st) < 0)
       return -1;
     ++n;
   } else {
@@ -873,8 +864,8 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   pf.begin(st);
   launch_pdl(wa.pdl, k_dw_reduce_sgd, dim3((d.C1 * (25 * d.cpad + 1) + 127) / 128, A), 128, 0, st, 
       b.part1, nch1, rpc1, wa.bs, d.C1, 25 * d.cpad + 1, w, L.o_c1w,
-                                              L.o_c1b, slots, L.P_pad, wa.lr, tc1 ? b.c1wt : nullptr,
-      tc1 ? wa.bpre : nullptr, g1, (int64_t)d.H0 * wa.sum_bs, d.H0), ++n;
+                                              L.o_c1b, slots, L.P_pad, wa.lr,
+      tc1 ? wa.bpre : nullptr, g1, 2 * wa.sum_bs, 2), ++n;  // conv1 tensor-core dW: half-sample tiles
   pf.end(K_CONV1_DWR, 0, 8.0 * A * d.C1 * 25 * d.cin, st);
   return n;
 }

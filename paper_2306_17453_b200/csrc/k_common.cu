@@ -166,44 +166,14 @@ __global__ void k_pack_cnn(const float* __restrict__ x, const int64_t* __restric
   }
 }
 
-// Four horizontally pre-shifted planar copies of the packed input for the conv1 weight
-// gradient's TMA loads (a TMA box may not start at a non-16-byte-aligned innermost
-// coordinate, so shifts by 1..3 pixels are baked in):
-//   xs[r][s][c][h][w'] = x[r][h][w' + s - 2][c] (0 outside), s in [0,4), w' in [0, W+4).
-__global__ void k_pack_shifted_planar(const float* __restrict__ xpack, int64_t rows, int H, int W,
-                                      float* __restrict__ xs) {
-  const int WP = W + 4;
-  const int64_t per = (int64_t)H * WP;  // one thread per (row r, h, w'): 16 outputs (s, c)
-  const int64_t tot = rows * per;
-  const int64_t plane = (int64_t)H * WP;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / per;
-    const int rem = (int)(e - r * per);
-    const int wp = rem % WP, h = rem / WP;
-    const float4* src = reinterpret_cast<const float4*>(xpack) + (r * H + h) * W;
-    float* out = xs + r * 16 * plane + (int64_t)h * WP + wp;
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int w = wp + s - 2;
-      const float4 v = (w >= 0 && w < W) ? src[w] : make_float4(0.f, 0.f, 0.f, 0.f);
-      out[(4 * s + 0) * plane] = v.x;
-      out[(4 * s + 1) * plane] = v.y;
-      out[(4 * s + 2) * plane] = v.z;
-      out[(4 * s + 3) * plane] = v.w;
-    }
-  }
-}
-
 int pack_cnn(const Layout& L, const float* x_src, const int64_t* src_row, int64_t rows, float* xpack,
-             float* xplanar, cudaStream_t st) {
+             float* xg, cudaStream_t st) {
   if (rows <= 0) return 0;
   int HW = L.d.H0 * L.d.W0;
   k_pack_cnn<<<grid_for(rows * HW, 256, 1 << 20), 256, 0, st>>>(x_src, src_row, rows, L.d.cin, HW, xpack, nullptr,
                                                                   L.d.cpad);
-  if (!xplanar) return 1;
-  k_pack_shifted_planar<<<grid_for(rows * L.d.H0 * (L.d.W0 + 4), 256, 1 << 20), 256, 0, st>>>(
-      xpack, rows, L.d.H0, L.d.W0, xplanar);
-  return 2;
+  if (!xg) return 1;
+  return 1 + pack_xg(xpack, rows, xg, st);  // conv1 tensor-core window layout
 }
 
 __global__ void k_gather_rows(const float* __restrict__ src, const int64_t* __restrict__ src_row, int64_t rows,
