@@ -207,7 +207,7 @@ bool conv1_tc_supported(const Layout& L);
 int64_t conv1_xg_floats();
 int pack_xg(const float* xpack, int64_t rows, float* xg, cudaStream_t st);
 int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wstride, const float* xg,
-                 int64_t xrows, float* p1, uint8_t* am1, cudaStream_t st);
+                 int64_t xrows, int64_t slots, float* p1, uint8_t* am1, cudaStream_t st);
 // conv1 dW partials; dY1 is expanded on chip from dp1m and pool1's argmax am1
 int conv1_dw_tc(const Layout& L, const WaveArgs& wa, const float* xg, int64_t xrows, const float* dp1m,
                 const uint8_t* am1, int64_t slots, float* part, int64_t part_cap, int* g_out, cudaStream_t st);

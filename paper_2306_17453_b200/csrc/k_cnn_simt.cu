@@ -687,7 +687,7 @@ int cnn_wave_simt(const Layout& L, const WaveArgs& wa, const float* xpack, const
   const bool tc1 = wa.use_tc && conv1_tc_supported(L);
   pf.begin(st);
   if (tc1) {  // bias + ReLU + pool fused into the epilogue
-    if (conv1_fwd_tc(L, wa, w.base, w.stride, b.xg, b.xrows, b.p1, b.am1, st) < 0) return -1;
+    if (conv1_fwd_tc(L, wa, w.base, w.stride, b.xg, b.xrows, b.slots, b.p1, b.am1, st) < 0) return -1;
     ++n;
     pf.end(K_CONV1_FWD, f_c1, 4.0 * S * hw0 * d.cin + 5.0 * S * hw1 * d.C1, st);
   } else if (wa.use_tc && d.cin == 1 && d.C1 == 32) {  // speech: conv1 + bias + ReLU + pool in one pass

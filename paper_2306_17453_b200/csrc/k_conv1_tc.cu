@@ -219,21 +219,20 @@ __global__ void __launch_bounds__(F_THREADS, 1)
         uint8_t* arow = p.am1 + (((int64_t)s * 16 + py) * 16) * C1 + o;
         // The pool window of windows-column j spans pixels 4j + s, 4j + (s ^ 1) (lanes s, s^1) in
         // rows 2py, 2py + 1.  The lane pair splits the 8 windows: the even lane pools j = k, the
-        // odd lane j = k + 4, each receiving the partner's two values of its window.
+        // odd lane j = k + 4, each receiving the partner's two values of its window.  The bias is
+        // common to the window, so it is added to the maximum only.
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const float mt = (odd ? v[k + 4] : v[k]) + bo, mb = (odd ? v[12 + k] : v[8 + k]) + bo;
-          const float st = (odd ? v[k] : v[k + 4]) + bo, sb = (odd ? v[8 + k] : v[12 + k]) + bo;
+          const float mt = odd ? v[k + 4] : v[k], mb = odd ? v[12 + k] : v[8 + k];
+          const float st = odd ? v[k] : v[k + 4], sb = odd ? v[8 + k] : v[12 + k];
           const float pt = __shfl_xor_sync(0xffffffffu, st, 1), pb = __shfl_xor_sync(0xffffffffu, sb, 1);
           // row-major window order: (top, even px), (top, odd px), (bottom, even), (bottom, odd)
           const float a0 = odd ? pt : mt, a1 = odd ? mt : pt, a2 = odd ? pb : mb, a3 = odd ? mb : pb;
-          float mx = a0;
-          uint32_t bi = 0;
-          if (a1 > mx) { mx = a1; bi = 1; }
-          if (a2 > mx) { mx = a2; bi = 2; }
-          if (a3 > mx) { mx = a3; bi = 3; }
+          const float mx = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+          const uint32_t bi = a0 == mx ? 0u : (a1 == mx ? 1u : (a2 == mx ? 2u : 3u));
+          const float r = mx + bo;
           const int px = 2 * (k + (odd ? 4 : 0)) + (s4 >> 1);
-          prow[px * C1] = mx > 0.f ? mx : 0.f;
+          prow[px * C1] = r > 0.f ? r : 0.f;
           arow[px * C1] = (uint8_t)bi;
         }
       }
@@ -464,7 +463,7 @@ int pack_xg(const float* xpack, int64_t rows, float* xg, cudaStream_t st) {
 
 // conv1 forward + bias + ReLU + 2x2 pool (+ argmax) on tensor cores: xg -> p1, am1.
 int conv1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t wstride, const float* xg,
-                 int64_t xrows, float* p1, uint8_t* am1, cudaStream_t st) {
+                 int64_t xrows, int64_t slots, float* p1, uint8_t* am1, cudaStream_t st) {
   CUtensorMap mx;
   if (!encode_xg(&mx, xg, xrows, 1)) return -1;
   static bool attr = false;
