@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         tc::mbar_init(gfull + i, 1);
         tc::mbar_init(gempty + i, BW_EPI);
         tc::mbar_init(p2full + i, 1);
-        tc::mbar_init(p2empty + i, 1);
+        tc::mbar_init(p2empty + i, BW_EPI);  // released by the dX epilogue (it reads p2 from the panel)
         tc::mbar_init(dxfull + i, 1);
         tc::mbar_init(dxempty + i, BW_EPI);
       }
@@ -285,7 +285,6 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                          tc::sdesc(up2 + k * 1024, NB * 128, 512, tc::kSW128_32B), IDESC_DW, k != 0);
           tc::mma_commit(gfull + buf);
         }
-        tc::mma_commit(p2empty + pb);
         tc::mma_commit(dxfull + pb);
       }
     }
@@ -302,27 +301,26 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       if (bs == 0) continue;
       const int pb = ti & 1, pph = (ti >> 1) & 1;
       ++ti;
-      // pool2 state of this thread's dX row and batch half: independent of the MMAs, loaded up
-      // front and only inspected in the dX epilogue, so the loads stay in flight during the chunks
+      // pool2 argmax of this thread's dX row and batch half: loaded during the panel's last chunk
+      // (few loads in flight while the SGD epilogue runs); p2 itself is read from the panel in smem
       const int k = kt * 128 + row, r0 = 16 * hf;
-      float p2v[16];
-      uint32_t amw[4];
-#pragma unroll
-      for (int r = 0; r < 16; ++r) p2v[r] = r0 + r < bs ? __ldg(p.p2 + ((int64_t)a * p.B + r0 + r) * p.F + k) : 0.f;
-#pragma unroll
-      for (int r4 = 0; r4 < 4; ++r4) {
-        uint32_t w = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int r = r0 + 4 * r4 + u;
-          const uint32_t b8 = r < bs ? __ldg(p.am2 + ((int64_t)a * p.B + r) * p.F + k) : 0u;
-          w |= b8 << (8 * u);
-        }
-        amw[r4] = w;
-      }
+      uint32_t amw[4] = {0u, 0u, 0u, 0u};
       for (int c = 0; c < nch; ++c, ++it) {
         const int st = it % BW_NST, buf = it & 1, gph = (it >> 1) & 1;
         uint8_t* sw = smem + st * BW_STAGE;
+        if (c == nch - 1) {
+#pragma unroll
+          for (int r4 = 0; r4 < 4; ++r4) {
+            uint32_t w = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int r = r0 + 4 * r4 + u;
+              const uint32_t b8 = r < bs ? __ldg(p.am2 + ((int64_t)a * p.B + r) * p.F + k) : 0u;
+              w |= b8 << (8 * u);
+            }
+            amw[r4] = w;
+          }
+        }
         tc::mbar_wait(gfull + buf, gph);
         tc::tc_fence_after();
         if (kt == 0 && hf == 0) {  // bias: b1[n] -= η Σ_r dh[r][n], from the stage's dh chunk (ATOM_32B)
@@ -373,6 +371,18 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       tc::tmem_ld16(tdx, v);
       tc::tc_fence_before();
       tc::mbar_arrive(dxempty + pb);
+      // p2[r][k] from the panel (chunk k/32, row r, SWIZZLE_128B_ATOM_32B), then release it
+      float p2v[16];
+      {
+        const uint8_t* pan = smem + BW_P2 + pb * BW_P2B + (row >> 5) * 4096 + (row & 7) * 4;
+        const int g = (row & 31) >> 3;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const int rr = r0 + r;
+          p2v[r] = *reinterpret_cast<const float*>(pan + rr * 128 + ((g ^ (rr & 3)) << 5));
+        }
+      }
+      tc::mbar_arrive(p2empty + pb);
       const int cc = k % p.C2, pw = (k / p.C2) % p.W2, ph = k / (p.C2 * p.W2);
       const int W1 = p.W1, H1 = p.H1;  // a trailing odd row / column gets no gradient (floor pooling)
 #pragma unroll
