@@ -304,22 +304,13 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       // pool2 argmax of this thread's dX row and batch half: loaded during the panel's last chunk
       // (few loads in flight while the SGD epilogue runs); p2 itself is read from the panel in smem
       const int k = kt * 128 + row, r0 = 16 * hf;
-      uint32_t amw[4] = {0u, 0u, 0u, 0u};
+      uint32_t amb[16];  // pool2 argmax bytes of rows r0.. r0+15 (consumed only in the dX epilogue)
       for (int c = 0; c < nch; ++c, ++it) {
         const int st = it % BW_NST, buf = it & 1, gph = (it >> 1) & 1;
         uint8_t* sw = smem + st * BW_STAGE;
         if (c == nch - 1) {
 #pragma unroll
-          for (int r4 = 0; r4 < 4; ++r4) {
-            uint32_t w = 0;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int r = r0 + 4 * r4 + u;
-              const uint32_t b8 = r < bs ? __ldg(p.am2 + ((int64_t)a * p.B + r) * p.F + k) : 0u;
-              w |= b8 << (8 * u);
-            }
-            amw[r4] = w;
-          }
+          for (int r = 0; r < 16; ++r) amb[r] = r0 + r < bs ? __ldg(p.am2 + ((int64_t)a * p.B + r0 + r) * p.F + k) : 0u;
         }
         tc::mbar_wait(gfull + buf, gph);
         tc::tc_fence_after();
@@ -334,17 +325,25 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           uint8_t* ob = smem + BW_OUT + (oi & 1) * 16384;
           float v[16];
           const uint32_t tg = tbase + ((uint32_t)(qd * 32) << 16) + buf * 128 + 32 * j + 16 * hf;
-          tc::tmem_ld16(tg, v);  // issued before the barrier: overlaps the wait for the store buffer
+          // the old W1 values (32-byte granule g of the row sits at g ^ (row % 4), ATOM_32B) and the
+          // gradient are read before the barrier: both loads overlap the wait for the store buffer
+          const uint8_t* rowp = sw + j * 16384 + row * 128;
+          float4 wv[2][2];
+#pragma unroll
+          for (int g2 = 0; g2 < 2; ++g2)
+#pragma unroll
+            for (int hq = 0; hq < 2; ++hq)
+              wv[g2][hq] = reinterpret_cast<const float4*>(rowp + (((2 * hf + g2) ^ (row & 3)) << 5))[hq];
+          tc::tmem_ld16(tg, v);
           if (storer) tc::bulk_wait_read<1>();  // the store issued from this buffer two sub-chunks ago has read it
           asm volatile("bar.sync 1, %0;" ::"n"(BW_EPI) : "memory");
-          const uint8_t* rowp = sw + j * 16384 + row * 128;
           uint8_t* orow = ob + row * 128;
 #pragma unroll
-          for (int g2 = 0; g2 < 2; ++g2) {  // 32-byte granule g of the row sits at g ^ (row % 4) (ATOM_32B)
+          for (int g2 = 0; g2 < 2; ++g2) {
             const int off = ((2 * hf + g2) ^ (row & 3)) << 5;
 #pragma unroll
             for (int hq = 0; hq < 2; ++hq) {
-              float4 w = reinterpret_cast<const float4*>(rowp + off)[hq];
+              float4 w = wv[g2][hq];
               w.x -= p.lr * v[8 * g2 + 4 * hq];
               w.y -= p.lr * v[8 * g2 + 4 * hq + 1];
               w.z -= p.lr * v[8 * g2 + 4 * hq + 2];
@@ -390,7 +389,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         if (r0 + r >= bs) break;
         const int64_t s = (int64_t)a * p.B + r0 + r;
         const float g = p2v[r] > 0.f ? v[r] : 0.f;
-        const int am = (amw[r >> 2] >> (8 * (r & 3))) & 0xff;
+        const int am = (int)amb[r];
         float* d = p.dY2 + ((s * H1 + 2 * ph) * W1 + 2 * pw) * p.C2 + cc;
         d[0] = am == 0 ? g : 0.f;
         d[p.C2] = am == 1 ? g : 0.f;
