@@ -29,7 +29,8 @@ namespace {
 constexpr int NB = 32;   // batch slots per client in the MMA N (or K) dimension
 
 // ------------------------------------------------------------------ forward
-constexpr int FW_A = 128 * 128, FW_B = NB * 128, FW_STAGE = FW_A + FW_B, FW_NST = 6;
+// a stage holds FW_KB consecutive 32-wide k-blocks (512-byte runs of every W1 row per TMA box)
+constexpr int FW_KB = 4, FW_A = FW_KB * 128 * 128, FW_B = FW_KB * NB * 128, FW_STAGE = FW_A + FW_B, FW_NST = 2;
 constexpr int FW_BAR = FW_NST * FW_STAGE, FW_SMEM = FW_BAR + 128 + 1024;
 
 struct FwArgs {
@@ -43,11 +44,12 @@ struct FwArgs {
 
 __global__ void __launch_bounds__(192, 1)
     k_fc1_fwd_tc(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, FwArgs p) {
+  static_assert(FW_NST * FW_STAGE + 128 + 1024 <= 227 * 1024, "shared memory");
   constexpr uint32_t IDESC = tc::idesc_tf32(128, NB, 0, 0);
   const int a = blockIdx.y, mt = blockIdx.x / p.ksplit, ks = blockIdx.x % p.ksplit;
   const int bs = p.bs[a];
   if (bs == 0) return;
-  const int kb0 = ks * p.kpb, kb1 = min(p.F / 32, kb0 + p.kpb), nkb = kb1 - kb0;
+  const int kb0 = ks * p.kpb, kb1 = min(p.F / 32, kb0 + p.kpb), nkb = (kb1 - kb0) / FW_KB;  // stages
   // PDL: wait for the previous kernel before taking TMEM (a parked CTA holding columns
   // would stall other streams' kernels) or touching anything it writes.
   pdl_wait();
@@ -81,12 +83,12 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     if (tc::elect_one()) {
       for (int i = 0; i < nkb; ++i) {
-        const int st = i % FW_NST, ph = (i / FW_NST) & 1, kb = kb0 + i;
+        const int st = i % FW_NST, ph = (i / FW_NST) & 1, kb = kb0 + i * FW_KB;
         tc::mbar_wait(empty + st, ph ^ 1);
         uint8_t* sa = smem + st * FW_STAGE;
         tc::mbar_expect_tx(full + st, FW_STAGE);
-        tc::tma_load_3d(sa, &mapW, full + st, 32 * kb, 128 * mt, a * p.wmul);
-        tc::tma_load_3d(sa + FW_A, &mapX, full + st, 32 * kb, a * p.B, 0);
+        tc::tma_load_4d(sa, &mapW, full + st, 0, 128 * mt, kb, a * p.wmul);  // [kb][128 n][32 k]
+        tc::tma_load_3d(sa + FW_A, &mapX, full + st, 0, a * p.B, kb);         // [kb][32 r][32 k]
       }
     }
   } else if (warp == 1) {
@@ -97,9 +99,9 @@ __global__ void __launch_bounds__(192, 1)
         tc::tc_fence_after();
         const uint32_t sa = tc::smem_u32(smem + st * FW_STAGE), sb = sa + FW_A;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          tc::mma_tf32(tbase, tc::sdesc(sa + k * 32, 0, 1024, tc::kSW128), tc::sdesc(sb + k * 32, 0, 1024, tc::kSW128),
-                       IDESC, (i | k) != 0);
+        for (int k = 0; k < 4 * FW_KB; ++k)
+          tc::mma_tf32(tbase, tc::sdesc(sa + (k >> 2) * 16384 + (k & 3) * 32, 0, 1024, tc::kSW128),
+                       tc::sdesc(sb + (k >> 2) * 4096 + (k & 3) * 32, 0, 1024, tc::kSW128), IDESC, (i | k) != 0);
         tc::mma_commit(empty + st);
       }
       tc::mma_commit(tfull);
@@ -428,19 +430,20 @@ int fc1_fwd_tc(const Layout& L, const WaveArgs& wa, const float* wbase, int64_t 
                int64_t slots, float* h, float* part, int64_t part_floats, cudaStream_t st, int* launches) {
   const CnnDims& d = L.d;
   CUtensorMap mw, mx;
-  uint64_t dw[3] = {(uint64_t)d.F, (uint64_t)d.HID, (uint64_t)wclients};
-  uint64_t sw[2] = {(uint64_t)d.F * 4, (uint64_t)L.P_pad * 4};
-  uint32_t bw[3] = {32, 128, 1};
-  uint64_t dx[3] = {(uint64_t)d.F, (uint64_t)slots, 1};
-  uint64_t sx[2] = {(uint64_t)d.F * 4, (uint64_t)d.F * 4 * slots};
-  uint32_t bx[3] = {32, NB, 1};
-  if (!tmap_encode(&mw, wbase + L.o_f1w, 3, dw, sw, bw, 1) || !tmap_encode(&mx, p2, 3, dx, sx, bx, 1)) return -1;
+  // W1 viewed as [client][k-block][n][32 k] and p2 as [k-block][slot][32 k]: one box = FW_KB k-blocks
+  uint64_t dw[4] = {32, (uint64_t)d.HID, (uint64_t)d.F / 32, (uint64_t)wclients};
+  uint64_t sw[3] = {(uint64_t)d.F * 4, 128, (uint64_t)L.P_pad * 4};
+  uint32_t bw[4] = {32, 128, FW_KB, 1};
+  uint64_t dx[3] = {32, (uint64_t)slots, (uint64_t)d.F / 32};
+  uint64_t sx[2] = {(uint64_t)d.F * 4, 128};
+  uint32_t bx[3] = {32, NB, FW_KB};
+  if (!tmap_encode(&mw, wbase + L.o_f1w, 4, dw, sw, bw, 1) || !tmap_encode(&mx, p2, 3, dx, sx, bx, 1)) return -1;
   const int mtiles = d.HID / 128, nkb = d.F / 32;
   static const int ctas = std::max(1, env_knob("FL_FC1F_CTAS", 2 * 148));
   int ksplit = (ctas + wa.A * mtiles - 1) / (wa.A * mtiles);
   ksplit = ksplit < 1 ? 1 : (ksplit > 16 ? 16 : ksplit);
   while (ksplit > 1 && (int64_t)wa.A * ksplit * NB * d.HID > part_floats) --ksplit;
-  const int kpb = (nkb + ksplit - 1) / ksplit;
+  const int kpb = (nkb + ksplit * FW_KB - 1) / (ksplit * FW_KB) * FW_KB;  // whole stages per split
   ksplit = (nkb + kpb - 1) / kpb;
   static bool attr = false;
   set_smem(k_fc1_fwd_tc, FW_SMEM, attr);
