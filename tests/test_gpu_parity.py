@@ -4,6 +4,9 @@ Bars (BASELINE.json north_star): placement / segment offsets bit-exact;
 aggregation alone within 1e-6 relative (reading A20: |g − o| ≤ 1e-6·s_p with
 s_p = Σ_k (n_k/N)|θ_k,p|); parameters within 1e-3 max-abs after a full round.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -20,7 +23,10 @@ import paper_2306_17453_b200 as fl  # noqa: E402
 
 TOL_ROUND = 1e-3
 TOL_AGG = 1e-6
-TOL_DRIFT = 1e-2  # per-client envelope for 126-step trajectories (reading R14)
+# 126-step trajectories (reading R14): each path's drift from fp64 is bounded by twice
+# the drift the fp64 oracle itself shows when θ_g is perturbed once at that path's precision
+# (tests/golden/c3_drift_envelope.json, written by scripts/drift_envelope.py from oracle/ only)
+DRIFT_FACTOR = 2.0
 
 
 def make_ctx(wl, sizes, x, y, theta, on_device=True, **kw):
@@ -261,9 +267,10 @@ def test_C3_full_size_decomposed():
       (i)  the aggregation of the GPU's own θ_k at full size within 1e-6 (reading R9);
       (ii) θ_k of 12 random clients with <= 16 SGD steps within 1e-3 of the fp64 oracle;
       (iii) the 4 largest clients (126 steps) on the TF32 path AND on the FP32 SIMT path
-           (math = 1) within the drift envelope 1e-2 (reading R14): over 126 steps the
-           dynamics amplify any fp32 rounding — the FP32 path itself departs from fp64 by
-           ~4e-3 — so a per-client 1e-3 bar is unattainable there, while θ_new, which the
+           (math = 1) within twice the oracle's own drift envelope (reading R14): over 126
+           steps the dynamics amplify any rounding — two EXACT fp64 trajectories whose θ_g
+           differ by one fp32 roundoff (2^-24 relative) end 3.8e-3 apart, by one TF32 rounding
+           1.1e-2 apart — so a per-client 1e-3 bar is unattainable there, while θ_new, which the
            north star bounds, is 6.8e-5 from the full fp64 oracle over all 1,000 clients
            (scripts/c3_full_oracle.py -> profiles/r01/c3_parity.json).
     Placement across 8 GPUs changes none of this: per-client training is placement-independent
@@ -303,7 +310,10 @@ def test_C3_full_size_decomposed():
     print("C3: agg", ea, "small", ["%.1e" % e for e in e_small], "big tf32", ["%.1e" % e for e in e_big],
           "big fp32", ["%.1e" % e for e in e_simt])
     assert max(e_small) <= TOL_ROUND, e_small
-    assert max(e_big) <= TOL_DRIFT and max(e_simt) <= TOL_DRIFT, (e_big, e_simt)
+    env = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c3_drift_envelope.json")))
+    assert env["clients"] == [int(c) for c in big], (env["clients"], big)
+    assert max(e_big) <= DRIFT_FACTOR * max(env["drift_tf32"]), (e_big, env["drift_tf32"])
+    assert max(e_simt) <= DRIFT_FACTOR * max(env["drift_fp32"]), (e_simt, env["drift_fp32"])
 
 
 # char-LSTM (a6): ragged clients (1 to 3 steps of B = 4), full round vs the fp64 oracle
