@@ -168,3 +168,20 @@ def test_round_identical_clients_equal_single_client():
     single = oracle.local_sgd("logreg", theta, x1, y1, 5, 1, 0.1)
     assert N == 40
     assert np.allclose(out, single, rtol=0, atol=1e-15)
+
+
+def test_c3_drift_envelope_golden_matches_workload():
+    """tests/golden/c3_drift_envelope.json (written by scripts/drift_envelope.py from oracle/
+    only) must describe the 4 largest clients of the C3 cohort the GPU test checks, and its
+    envelopes must be ordered as the precisions are (one fp32 roundoff < one TF32 rounding)."""
+    import json
+    import os
+
+    import synth
+
+    env = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c3_drift_envelope.json")))
+    wl = synth.preset("C3")
+    sizes = synth.client_sizes(wl)[np.sort(synth.cohort(wl))]
+    big = np.argsort(-sizes, kind="stable")[:4]
+    assert env["clients"] == [int(c) for c in big] and env["sizes"] == [int(sizes[c]) for c in big]
+    assert 0 < max(env["drift_fp32"]) < max(env["drift_tf32"]) < max(env["update_maxabs"])
