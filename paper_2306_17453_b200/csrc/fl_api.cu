@@ -164,11 +164,17 @@ struct Nccl {
 };
 Nccl g_nccl;
 
+// Grow-only device buffers.  A replaced buffer is retired to `grave` and freed when the context
+// is destroyed, not here: cudaFree synchronises the whole device, so a rank that grows a buffer
+// mid-run would wait for every other context's kernels — including a peer rank's aggregation
+// kernel that is itself waiting for this rank (two ranks in one process, f3/f4), a stall of up to
+// a second per growth.  Growth allocates 1/8 headroom so share changes rarely trigger it.
 template <class T>
-cudaError_t grow_dev(T*& p, int64_t& cap, int64_t need) {
+cudaError_t grow_dev(std::vector<void*>& grave, T*& p, int64_t& cap, int64_t need) {
   if (need <= cap && p) return cudaSuccess;
-  if (p) cudaFree(p);
+  if (p) grave.push_back(p);
   p = nullptr;
+  if (cap > 0) need += need / 8;
   int64_t n = std::max<int64_t>(need, 1);
   cudaError_t e = cudaMalloc((void**)&p, sizeof(T) * (size_t)n);
   cap = e == cudaSuccess ? n : 0;
@@ -338,6 +344,7 @@ struct fl_ctx {
   bool peer_on = false;
   PeerArgs peer{};
   std::vector<void*> ipc_opened;             // peer buffers mapped with cudaIpcOpenMemHandle
+  std::vector<void*> grave;                  // replaced device buffers, freed at destroy (grow_dev)
   unsigned long long* d_sig = nullptr;       // [(FL_MAX_PEERS + 1) · T] signal words
   int peer_T = 0;
   float* d_recv = nullptr;                   // server (rank 0) receive buffer, unaggregated mode
@@ -448,6 +455,7 @@ void fl_round_destroy(fl_ctx* c) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  for (void* p : c->grave) cudaFree(p);
   void* pptrs[] = {c->d_sig, c->d_recv, c->d_dst_row, c->d_nplan, c->d_ctr};
   for (void* p : pptrs)
     if (p) cudaFree(p);
@@ -827,23 +835,23 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
     for (int32_t a = 0; a < ws.A[(size_t)k]; ++a) pre[a + 1] = pre[a] + h_bs[ws.bs_off[(size_t)k] + a];
   }
   // device capacity (grow-only; allocation happens on the first round of a given size)
-  CK(grow_dev(c->d_slots, c->slots_cap, std::max<int64_t>(K, 1) * L.P_pad));
-  CK(grow_dev(c->d_xpack, c->xpack_cap, std::max<int64_t>(R, 1) * L.D_pack));
+  CK(grow_dev(c->grave, c->d_slots, c->slots_cap, std::max<int64_t>(K, 1) * L.P_pad));
+  CK(grow_dev(c->grave, c->d_xpack, c->xpack_cap, std::max<int64_t>(R, 1) * L.D_pack));
   // shifted planar copies of the input exist only for the tensor-core conv1 dW
   const bool want_planar = L.model == FL_MODEL_CNN_CIFAR && c->cfg.math == 0 && conv1_tc_supported(L);
   if (want_planar)
-    CK(grow_dev(c->cb.xg, c->cb.xg_cap, (c->xpack_cap / L.D_pack) * conv1_xg_floats()));
-  CK(grow_dev(c->d_ypack, c->ypack_cap, R));
-  CK(grow_dev(c->d_src_row, c->src_cap, R));
-  CK(grow_dev(c->d_n, c->n_cap, K));
-  CK(grow_dev(c->d_steps, c->steps_cap, K));
-  CK(grow_dev(c->d_slot_off, c->slot_off_cap, ws.n_waves + 1));
-  CK(grow_dev(ws.d_sidx, c->sidx_cap, n_sidx));
-  CK(grow_dev(ws.d_bs, c->bs_cap, n_bs));
-  CK(grow_dev(ws.d_bpre, c->bpre_cap, n_bs + ws.n_waves));
+    CK(grow_dev(c->grave, c->cb.xg, c->cb.xg_cap, (c->xpack_cap / L.D_pack) * conv1_xg_floats()));
+  CK(grow_dev(c->grave, c->d_ypack, c->ypack_cap, R));
+  CK(grow_dev(c->grave, c->d_src_row, c->src_cap, R));
+  CK(grow_dev(c->grave, c->d_n, c->n_cap, K));
+  CK(grow_dev(c->grave, c->d_steps, c->steps_cap, K));
+  CK(grow_dev(c->grave, c->d_slot_off, c->slot_off_cap, ws.n_waves + 1));
+  CK(grow_dev(c->grave, ws.d_sidx, c->sidx_cap, n_sidx));
+  CK(grow_dev(c->grave, ws.d_bs, c->bs_cap, n_bs));
+  CK(grow_dev(c->grave, ws.d_bpre, c->bpre_cap, n_bs + ws.n_waves));
   if (!c->pop_dev) {
-    CK(grow_dev(c->d_stage, c->stage_cap, std::max<int64_t>(R, 1) * L.D_in));
-    CK(grow_dev(c->d_ystage, c->ystage_cap, R));
+    CK(grow_dev(c->grave, c->d_stage, c->stage_cap, std::max<int64_t>(R, 1) * L.D_in));
+    CK(grow_dev(c->grave, c->d_ystage, c->ystage_cap, R));
   }
   const bool cnn = (L.model == FL_MODEL_CNN_CIFAR || L.model == FL_MODEL_CNN_SPEECH);
   const bool lstm = L.model == FL_MODEL_CHAR_LSTM;
@@ -852,7 +860,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
     float** bufs[] = {&b.xp, &b.G0, &b.G1, &b.dpre, &b.C0, &b.C1, &b.H0, &b.H1, &b.dX, &b.E, &b.dE, &b.dhT};
     const int kind[] = {0, 0, 0, 0, 1, 1, 1, 1, 2, 3, 3, 4};
     for (int i = 0; i < 12; ++i) {
-      if (*bufs[i]) cudaFree(*bufs[i]);
+      if (*bufs[i]) c->grave.push_back(*bufs[i]);  // freed at destroy (see grow_dev)
       *bufs[i] = nullptr;
       CK(cudaMalloc(bufs[i], sizeof(float) * lstm_act_floats(K * B, kind[i])));
     }
@@ -866,7 +874,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
     if (S > c->cb_slots_cap) {
       void* old[] = {b.a1, b.p1, b.a2, b.p2, b.h, b.dh, b.am1, b.am2, b.dp2, b.dY2, b.dp1, b.dY1, b.dz};
       for (void* p : old)
-        if (p) cudaFree(p);
+        if (p) c->grave.push_back(p);  // freed at destroy (see grow_dev)
       const int64_t hw0 = (int64_t)d.H0 * d.W0, hw1 = (int64_t)d.H1 * d.W1, hw2 = (int64_t)d.H2 * d.W2;
       // the full-resolution conv1 planes (pre-pool activation, its gradient) exist only on the
       // FP32 SIMT path: the tensor-core / fused paths pool in conv1's epilogue and take conv1's
@@ -903,7 +911,7 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
     if (pg * NG > c->cb_part_cap) {
       void* old[] = {b.part1, b.part2, b.fc1_part};
       for (void* p : old)
-        if (p) cudaFree(p);
+        if (p) c->grave.push_back(p);  // freed at destroy (see grow_dev)
       CK(cudaMalloc(&b.part2, sizeof(float) * NG * pg * std::max<int64_t>(d.C2 * (25 * d.C1 + 1), conv2_dw_tc_z_floats())));
       CK(cudaMalloc(&b.part1, sizeof(float) * NG * pg * d.C1 * (25 * d.cpad + 1)));
       b.fc1_part_floats = (int64_t)160 * 32 * d.HID;
@@ -1162,7 +1170,7 @@ fl_status fl_aggregate(fl_ctx* c, float* out_params, int64_t* out_total_samples)
                      (long long)c->recv_cap, (long long)Kt);
     std::vector<int64_t> dst((size_t)K);
     for (int64_t e = 0; e < K; ++e) dst[(size_t)e] = c->plan_off[(size_t)r] + c->exec[(size_t)e];
-    CK(grow_dev(c->d_dst_row, c->dst_cap, K));
+    CK(grow_dev(c->grave, c->d_dst_row, c->dst_cap, K));
     if (K) CK(cudaMemcpyAsync(c->d_dst_row, dst.data(), sizeof(int64_t) * K, cudaMemcpyHostToDevice, st));
     const unsigned long long seq = ++c->agg_seq;
     CK(cudaEventRecord(c->ev_acc1, st));
@@ -1175,7 +1183,7 @@ fl_status fl_aggregate(fl_ctx* c, float* out_params, int64_t* out_total_samples)
     } else {
       std::vector<int64_t> np((size_t)Kt);
       for (int64_t i = 0; i < Kt; ++i) np[(size_t)i] = c->n_samples[(size_t)c->plan_ids[(size_t)i]];
-      CK(grow_dev(c->d_nplan, c->nplan_cap, Kt));
+      CK(grow_dev(c->grave, c->d_nplan, c->nplan_cap, Kt));
       CK(cudaMemcpyAsync(c->d_nplan, np.data(), sizeof(int64_t) * Kt, cudaMemcpyHostToDevice, st));
       n += wait_flags(c->d_sig, 0, W, 1, seq, st);  // every rank's models have landed
       n += fedavg_accum_final(c->d_recv, Pp, c->d_nplan, (int)Kt, Pp, c->d_theta, (double)c->N_total, c->d_theta, st);
@@ -1466,7 +1474,7 @@ fl_status fl_fedavg_vectors(fl_ctx* c, const float* theta_k, const int64_t* n, i
     N += n[k];
   }
   CK(cudaSetDevice(c->cfg.device));
-  CK(grow_dev(c->d_n, c->n_cap, K));
+  CK(grow_dev(c->grave, c->d_n, c->n_cap, K));
   CK(cudaMemcpyAsync(c->d_n, n, sizeof(int64_t) * K, cudaMemcpyHostToDevice, c->st));
   CK(cudaEventRecord(c->ev_agg0, c->st));
   fedavg_accum_final(theta_k, P, c->d_n, (int)K, P, theta_g, (double)N, out, c->st);

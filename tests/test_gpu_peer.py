@@ -175,11 +175,25 @@ def test_heterogeneous_ranks_lb_beats_bu(tmp_path):
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = tmp_path / "hetero.json"
     env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", CUDA_MODULE_LOADING="EAGER")
-    subprocess.run([sys.executable, os.path.join(root, "scripts", "hetero_emulation.py"), "--clients", "1000",
-                    "--rounds", "6", "--out", str(out)], check=True, env=env, timeout=600)
-    res = json.load(open(out))
+
+    def slow_rank_ms_per_step(res):
+        return [r["train_ms"][1] / max(r["steps"][1], 1) for p in ("bu", "lb") for r in res[p]["rounds"]]
+
+    # Emulation validity: the partitions' speeds must stay put.  Two ranks in one process share
+    # HBM, L2 and the hardware work queues; in some runs (seen with the round-1 kernels too) the
+    # 44-SM rank's streams get serialised behind the other rank's for the whole experiment, its
+    # time per SGD step inflating 2-5x for the same work, which no placement rule can fix.  Such
+    # a run is detected from the slow rank's ms per step (> 1.6x its minimum) and re-run once.
+    for attempt in range(2):
+        out = tmp_path / f"hetero{attempt}.json"
+        subprocess.run([sys.executable, os.path.join(root, "scripts", "hetero_emulation.py"), "--clients", "1000",
+                        "--rounds", "6", "--out", str(out)], check=True, env=env, timeout=600)
+        res = json.load(open(out))
+        mps = slow_rank_ms_per_step(res)
+        print(f"attempt {attempt}: slow-rank ms/step {min(mps):.4f}..{max(mps):.4f}")
+        if max(mps) <= 1.6 * min(mps):
+            break
     bu, lb = res["bu"], res["lb"]
     assert bu["sm_count"][0] > 1.5 * bu["sm_count"][1]
     print(f"timedelta BU {bu['timedelta_ms_mean_after_r0']:.2f} ms, LB {lb['timedelta_ms_mean_after_r0']:.2f} ms")
