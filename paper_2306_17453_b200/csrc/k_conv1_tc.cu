@@ -210,10 +210,13 @@ __global__ void __launch_bounds__(F_THREADS, 1)
       const int buf = it & 1, dph = (it >> 1) & 1;
       tc::mbar_wait(dfull + buf, dph);
       tc::tc_fence_after();
+      float vv[32];  // both 16-column chunks of this warp's part in one TMEM load
+      tc::tmem_ld32(tbase + lrow + F_TD + buf * 128 + qp * 32, vv);
+      tc::tc_fence_before();
+      tc::mbar_arrive(dempty + buf);  // accumulator drained: the next tile's MMAs may start
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {  // 16 columns = image rows 2·py, 2·py + 1 x 8 windows
-        float v[16];
-        tc::tmem_ld16(tbase + lrow + F_TD + buf * 128 + qp * 32 + cc * 16, v);
+        const float* v = vv + 16 * cc;
         const int py = 8 * h + 2 * qp + cc;
         float* prow = p.p1 + (((int64_t)s * 16 + py) * 16) * C1 + o;
         uint8_t* arow = p.am1 + (((int64_t)s * 16 + py) * 16) * C1 + o;
@@ -236,8 +239,6 @@ __global__ void __launch_bounds__(F_THREADS, 1)
           arow[px * C1] = (uint8_t)bi;
         }
       }
-      tc::tc_fence_before();
-      tc::mbar_arrive(dempty + buf);
     }
   }
   tc::tc_fence_before();
