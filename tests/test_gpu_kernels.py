@@ -6,6 +6,8 @@ inputs (read back with fl_debug_read), so upstream differences cannot mask or fa
 an error.  TF32 operands keep 10 mantissa bits: outputs match to ~1e-3 relative in
 norm; pooling argmax may flip only where two window values are that close.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -38,7 +40,18 @@ def one_wave(sizes, math=0):
     _, x, y = synth.population(wl, sizes)
     theta = synth.init_params("cnn")
     cfg = fl.Config(model="cnn", batch_size=B, lr=wl.lr, math=math)
-    ctx = fl.fl_round_init(cfg, sizes, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), theta)
+    # one client group, no solo streams: client a's wave-0 activations sit at slots [a·B, a·B + B)
+    # of the debug buffers (the scheduler otherwise spreads clients over per-group buffers)
+    saved = {k: os.environ.get(k) for k in ("FL_GROUPS", "FL_SOLO")}
+    os.environ.update(FL_GROUPS="1", FL_SOLO="0")
+    try:
+        ctx = fl.fl_round_init(cfg, sizes, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), theta)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     ctx.fl_place(np.arange(len(sizes)))
     ctx.fl_train_clients(0)  # single-step clients: the buffers hold wave 0
     return ctx, theta
@@ -54,6 +67,10 @@ def rel(a, b):
 
 
 SIZES = [np.array([32]), np.array([32, 5, 17])]
+# conv1's kernels split a wave's half-sample tiles evenly over the CTAs, so with more tiles than
+# SMs one CTA's range crosses client boundaries (rebuilding the shifted taps in TMEM, closing a dW
+# segment mid-range): 40 clients, ragged ones in between
+SIZES_MANY = [np.array([32] * 12 + [7] + [32] * 12 + [19, 3] + [32] * 12 + [30])]
 
 
 @pytest.mark.parametrize("sizes", SIZES)
@@ -129,18 +146,28 @@ def client_x(sizes):
     return [torch.from_numpy(x[off[a]:off[a + 1]]).double().reshape(-1, 3, 32, 32) for a in range(len(sizes))]
 
 
-@pytest.mark.parametrize("sizes", SIZES)
+@pytest.mark.parametrize("sizes", SIZES + SIZES_MANY)
 def test_conv1_forward_tc(sizes):
     ctx, theta = one_wave(sizes)
     S = len(sizes) * B
     p1 = ctx.fl_debug_read("p1", (S, 16, 16, 32))
+    am1 = ctx.fl_debug_read("am1", (S, 16, 16, 32), np.uint8)
     P = params(theta)
     for a, xa in enumerate(client_x(sizes)):
-        ref = F.max_pool2d(F.relu(F.conv2d(xa, P["conv1.w"], P["conv1.b"], padding=2)), 2)
+        pre = F.conv2d(xa, P["conv1.w"], P["conv1.b"], padding=2)  # [n][32][32][32] fp64
+        ref = F.max_pool2d(F.relu(pre), 2)
         assert rel(p1[a * B:a * B + len(xa)], ref.permute(0, 2, 3, 1).numpy()) < TOL, a
+        # pool1's argmax (row-major window index) must select a maximum of its window, up to
+        # TF32 rounding of near-ties
+        win = pre.numpy().reshape(len(xa), 32, 16, 2, 16, 2).transpose(0, 2, 4, 1, 3, 5).reshape(len(xa), 16, 16, 32, 4)
+        am = am1[a * B:a * B + len(xa)].astype(np.int64)
+        assert am.max() <= 3
+        picked = np.take_along_axis(win, am[..., None], axis=-1)[..., 0]
+        gap = win.max(-1) - picked
+        assert gap.max() <= 1e-3 * np.abs(win).max(), (a, float(gap.max()))
 
 
-@pytest.mark.parametrize("sizes", SIZES)
+@pytest.mark.parametrize("sizes", SIZES + SIZES_MANY)
 def test_conv1_dw_tc(sizes):
     ctx, theta = one_wave(sizes)
     S = len(sizes) * B
