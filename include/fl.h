@@ -208,6 +208,17 @@ fl_status fl_train_clients(fl_ctx* ctx, int32_t round_index);
  * (canonical layout, synchronous copy); out_total_samples: nullable. */
 fl_status fl_aggregate(fl_ctx* ctx, float* out_params, int64_t* out_total_samples);
 
+/* fl_aggregate with the copy of θ_new only ENQUEUED on the ctx stream: the call returns
+ * without waiting, so the host can place and issue the next round while this one runs on
+ * the device (rounds are stream-ordered: the next round reads this θ_new on the device).
+ * out_params: nullable; else page-locked host float32[P] (cudaHostAlloc / cudaHostRegister /
+ * torch pin_memory), FL_ERR_INVALID for pageable memory.  Its contents are valid after
+ * fl_synchronize (or any later synchronising call) and must not be reused before. */
+fl_status fl_aggregate_async(fl_ctx* ctx, float* out_params, int64_t* out_total_samples);
+
+/* Block until all work issued on the ctx (rounds, copies) has completed. */
+fl_status fl_synchronize(fl_ctx* ctx);
+
 /* fl_place + fl_train_clients + fl_aggregate, timed; stats nullable.  Asynchronous
  * with respect to the host except for the stats event reads (it synchronises the
  * ctx stream when stats != NULL).  With a communicator, stats != NULL makes the call

@@ -30,7 +30,7 @@ PEER_BLOB_BYTES = 512
 
 # Symbols include/fl.h declares (checked by tests/test_abi.py).
 EXPORTS = ["fl_abi_version", "fl_n_params", "fl_place_plan", "fl_pack_plan", "fl_nccl_unique_id", "fl_round_init",
-           "fl_place", "fl_train_clients", "fl_aggregate", "fl_round", "fl_fedavg_vectors", "fl_get_local_plan",
+           "fl_place", "fl_train_clients", "fl_aggregate", "fl_aggregate_async", "fl_synchronize", "fl_round", "fl_fedavg_vectors", "fl_get_local_plan",
            "fl_get_client_params", "fl_get_global_params", "fl_set_global_params", "fl_get_stats",
            "fl_set_profiling", "fl_get_kernel_stats", "fl_get_stream", "fl_last_error", "fl_round_destroy", "fl_debug_read",
            "fl_lb_fit", "fl_set_timing_records", "fl_get_client_times", "fl_peer_export", "fl_peer_connect"]
@@ -97,6 +97,8 @@ def lib():
             "fl_place": (C.c_int, [vp, vp, i64, i32, vp, vp, vp]),
             "fl_train_clients": (C.c_int, [vp, i32]),
             "fl_aggregate": (C.c_int, [vp, vp, vp]),
+            "fl_aggregate_async": (C.c_int, [vp, vp, vp]),
+            "fl_synchronize": (C.c_int, [vp]),
             "fl_round": (C.c_int, [vp, vp, i64, i32, vp, i32, vp]),
             "fl_fedavg_vectors": (C.c_int, [vp, vp, vp, i64, i64, vp, vp]),
             "fl_get_local_plan": (C.c_int, [vp, vp, vp, vp, vp]),
@@ -282,6 +284,19 @@ class Ctx:
         tot = C.c_int64(0)
         self._check(lib().fl_aggregate(self._h, _ptr(out), C.byref(tot)), "fl_aggregate")
         return out, int(tot.value)
+
+    def fl_aggregate_async(self, out=None):
+        """fl_aggregate without waiting: θ_new lands in `out` (page-locked float32[P], e.g.
+        torch.empty(P, pin_memory=True)) once fl_synchronize returns."""
+        tot = C.c_int64(0)
+        p = None if out is None else C.c_void_p(out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data)
+        if out is not None and (str(out.dtype) not in ("float32", "torch.float32") or len(out) != self.P):
+            raise FLError(FL_ERR_INVALID, "fl_aggregate_async: float32[P] output required")
+        self._check(lib().fl_aggregate_async(self._h, p, C.byref(tot)), "fl_aggregate_async")
+        return int(tot.value)
+
+    def fl_synchronize(self):
+        self._check(lib().fl_synchronize(self._h), "fl_synchronize")
 
     def fl_round(self, cohort, policy="bu", lb_coef=None, round_index=0, stats=True):
         cohort = _i64(cohort)

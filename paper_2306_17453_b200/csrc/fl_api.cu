@@ -275,10 +275,16 @@ struct fl_ctx {
   int64_t xpack_cap = 0;
   int32_t* d_ypack = nullptr;
   int64_t ypack_cap = 0;
-  float* d_stage = nullptr;
-  int64_t stage_cap = 0;
+  // host-population staging, double-buffered across rounds: round r copies into buffer r % 2
+  // while round r−1 may still run (only its packs wait for round r−1, ev_start)
+  float* d_stage = nullptr;   // this round's buffer (one of d_stage2)
   int32_t* d_ystage = nullptr;
-  int64_t ystage_cap = 0;
+  float* d_stage2[2] = {nullptr, nullptr};
+  int64_t stage_cap2[2] = {0, 0};
+  int32_t* d_ystage2[2] = {nullptr, nullptr};
+  int64_t ystage_cap2[2] = {0, 0};
+  cudaEvent_t ev_sfree[2] = {nullptr, nullptr};  // recorded after the last pack reading buffer b
+  int stage_par = 0;
   int64_t* d_src_row = nullptr;
   int64_t src_cap = 0;
   int64_t* d_n = nullptr;
@@ -446,8 +452,8 @@ void fl_round_destroy(fl_ctx* c) {
   cudaSetDevice(c->cfg.device);
   if (c->st) cudaStreamSynchronize(c->st);
   if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
-  void* ptrs[] = {c->d_theta, c->d_canon_of, c->d_canon, c->d_slots, c->d_S, c->d_xpack, c->d_ypack, c->d_stage,
-                  c->d_ystage, c->d_src_row, c->d_n, c->d_steps, c->d_slot_off, c->ws.d_sidx, c->ws.d_bs, c->ws.d_bpre,
+  void* ptrs[] = {c->d_theta, c->d_canon_of, c->d_canon, c->d_slots, c->d_S, c->d_xpack, c->d_ypack, c->d_stage2[0],
+                  c->d_ystage2[0], c->d_stage2[1], c->d_ystage2[1], c->d_src_row, c->d_n, c->d_steps, c->d_slot_off, c->ws.d_sidx, c->ws.d_bs, c->ws.d_bpre,
                   c->cb.a1, c->cb.p1, c->cb.a2, c->cb.p2, c->cb.h, c->cb.dh, c->cb.am1, c->cb.am2, c->cb.dp2,
                   c->cb.dY2, c->cb.dp1, c->cb.dY1, c->cb.part1, c->cb.part2, c->cb.xg, c->cb.fc1_part,
                   c->cb.dz, c->lb.xp, c->lb.G0, c->lb.G1, c->lb.dpre, c->lb.C0, c->lb.C1, c->lb.H0, c->lb.H1,
@@ -464,7 +470,8 @@ void fl_round_destroy(fl_ctx* c) {
   if (c->h_rstat) cudaFreeHost(c->h_rstat);
   if (c->d_rstat) cudaFree(c->d_rstat);
   cudaEvent_t evs[] = {c->ev_entry, c->ev_start, c->ev_staged, c->ev_trained, c->ev_agg0,
-                       c->ev_acc1, c->ev_ar0, c->ev_ar1, c->ev_end, c->ev_tab[0], c->ev_tab[1]};
+                       c->ev_acc1, c->ev_ar0, c->ev_ar1, c->ev_end, c->ev_tab[0], c->ev_tab[1],
+                       c->ev_sfree[0], c->ev_sfree[1]};
   for (cudaEvent_t e : evs)
     if (e) cudaEventDestroy(e);
   if (c->host_registered) cudaHostUnregister((void*)c->x);
@@ -561,6 +568,7 @@ fl_status fl_round_init(const fl_config* cfg, const fl_population* pop, const fl
   cudaEvent_t* evs[] = {&c->ev_entry, &c->ev_start, &c->ev_staged, &c->ev_trained, &c->ev_agg0,
                         &c->ev_acc1, &c->ev_ar0, &c->ev_ar1, &c->ev_end, &c->ev_tab[0], &c->ev_tab[1]};
   for (cudaEvent_t* e : evs) CK(cudaEventCreate(e));
+  for (cudaEvent_t& e : c->ev_sfree) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (const char* ng = getenv("FL_GROUPS")) c->ngroups = std::max(1, atoi(ng));
   if (const char* ns = getenv("FL_SOLO")) c->nsolo = std::max(0, atoi(ns));
   if (const char* ss = getenv("FL_SOLO_SMS")) c->solo_sms = std::max(8, std::min(c->n_sms, atoi(ss)));
@@ -850,8 +858,11 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   CK(grow_dev(c->grave, ws.d_bs, c->bs_cap, n_bs));
   CK(grow_dev(c->grave, ws.d_bpre, c->bpre_cap, n_bs + ws.n_waves));
   if (!c->pop_dev) {
-    CK(grow_dev(c->grave, c->d_stage, c->stage_cap, std::max<int64_t>(R, 1) * L.D_in));
-    CK(grow_dev(c->grave, c->d_ystage, c->ystage_cap, R));
+    const int b = c->stage_par;
+    CK(grow_dev(c->grave, c->d_stage2[b], c->stage_cap2[b], std::max<int64_t>(R, 1) * L.D_in));
+    CK(grow_dev(c->grave, c->d_ystage2[b], c->ystage_cap2[b], R));
+    c->d_stage = c->d_stage2[b];
+    c->d_ystage = c->d_ystage2[b];
   }
   const bool cnn = (L.model == FL_MODEL_CNN_CIFAR || L.model == FL_MODEL_CNN_SPEECH);
   const bool lstm = L.model == FL_MODEL_CHAR_LSTM;
@@ -995,7 +1006,12 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
       c->ev_copy.push_back(f);
     }
     cs_stage = c->prof.on ? st : c->cst;  // a profiled round stays serialised on st
-    if (cs_stage != st) CK(cudaStreamWaitEvent(cs_stage, c->ev_start, 0));
+    if (cs_stage != st) {
+      // the copies only need this staging buffer back (packed two rounds ago); the packs write
+      // xpack / xg / ypack, which the previous round reads until st reaches ev_start
+      CK(cudaStreamWaitEvent(cs_stage, c->ev_sfree[c->stage_par], 0));
+      CK(cudaStreamWaitEvent(c->pst, c->ev_start, 0));
+    }
     // chunks 0 and 1 now; chunk q >= 2 is issued from the wave loop when step chunk_t0[q-1]
     // is issued, so the first waves are not queued behind every copy of the round
     for (; q_issued < std::min<int64_t>(NQ, 2); ++q_issued)
@@ -1123,6 +1139,10 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   }
   c->rec_valid = c->rec_on;
   CK(cudaEventRecord(c->ev_trained, st));
+  if (!c->pop_dev && R > 0) {  // every chunk of this round was packed on pst: its buffer is free after that
+    CK(cudaEventRecord(c->ev_sfree[c->stage_par], c->prof.on ? st : c->pst));
+    c->stage_par ^= 1;
+  }
   c->kernels = launches + tl;
   c->train_launches = tl;
   c->h2d = h2d;
@@ -1130,7 +1150,32 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   return FL_OK;
 }
 
+static fl_status aggregate(fl_ctx* c, float* out_params, int64_t* out_total_samples, bool sync);
+
 fl_status fl_aggregate(fl_ctx* c, float* out_params, int64_t* out_total_samples) {
+  return aggregate(c, out_params, out_total_samples, true);
+}
+
+fl_status fl_aggregate_async(fl_ctx* c, float* out_params, int64_t* out_total_samples) {
+  if (!c) return FL_ERR_INVALID;
+  if (out_params) {  // an async D2H into pageable memory would silently synchronise the host
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, out_params) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+      cudaGetLastError();
+      return set_err(c, FL_ERR_INVALID, "fl_aggregate_async: out_params must be page-locked host memory");
+    }
+  }
+  return aggregate(c, out_params, out_total_samples, false);
+}
+
+fl_status fl_synchronize(fl_ctx* c) {
+  if (!c) return FL_ERR_INVALID;
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaStreamSynchronize(c->st));
+  return FL_OK;
+}
+
+static fl_status aggregate(fl_ctx* c, float* out_params, int64_t* out_total_samples, bool sync) {
   if (!c) return FL_ERR_INVALID;
   if (c->failed || !c->trained) return set_err(c, FL_ERR_STATE, c->failed ? "ctx failed" : "train before aggregate");
   if (c->N_total <= 0) return set_err(c, FL_ERR_EMPTY, "total sample count is 0");
@@ -1226,7 +1271,7 @@ fl_status fl_aggregate(fl_ctx* c, float* out_params, int64_t* out_total_samples)
     internal_to_canon(c->d_theta, c->d_canon_of, Pp, c->d_canon, st);
     CKL();
     CK(cudaMemcpyAsync(out_params, c->d_canon, sizeof(float) * c->L.P, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    if (sync) CK(cudaStreamSynchronize(st));
   }
   return FL_OK;
 }

@@ -357,3 +357,39 @@ def test_lstm_round_two_epochs_shuffled_host_population(math):
     for i in range(len(sizes)):
         assert np.max(np.abs(tk_gpu[i] - tk[i])) <= TOL_LSTM[math], (i, _lstm_block_errors(tk_gpu[i], tk[i]))
     assert np.max(np.abs(out - ref)) <= TOL_LSTM[math]
+
+
+def test_async_aggregate_pipelined_rounds_match_sync():
+    """fl_aggregate_async (θ_new copied into pinned memory without a host wait, the next round
+    placed and issued while the device still runs this one) gives bit-identical θ_new to the
+    synchronous fl_aggregate over several rounds with changing cohorts; host population (the
+    staging copies of round r+1 must not overtake round r's use of the staging buffer)."""
+    wl = synth.preset("C2", n_pop=24, n_cohort=24)
+    sizes = synth.client_sizes(wl)
+    _, x, y = synth.population(wl, sizes)
+    theta = synth.init_params("cnn")
+    rng = np.random.default_rng(11)
+    cohorts = [np.sort(rng.choice(len(sizes), size=k, replace=False)) for k in (20, 9, 24, 13)]
+    ref = []
+    c1, _ = make_ctx(wl, sizes, x, y, theta, on_device=False)
+    for r, c in enumerate(cohorts):
+        c1.fl_place(c)
+        c1.fl_train_clients(r)
+        ref.append(c1.fl_aggregate(want_params=True)[0])
+    c1.close()
+    c2, _ = make_ctx(wl, sizes, x, y, theta, on_device=False)
+    outs = [torch.empty(c2.P, dtype=torch.float32, pin_memory=True) for _ in cohorts]
+    with pytest.raises(fl.FLError):  # pageable output memory is refused
+        c2.fl_place(cohorts[0])
+        c2.fl_train_clients(0)
+        c2.fl_aggregate_async(np.empty(c2.P, np.float32))
+    c2.close()
+    c2, _ = make_ctx(wl, sizes, x, y, theta, on_device=False)
+    for r, c in enumerate(cohorts):
+        c2.fl_place(c)
+        c2.fl_train_clients(r)
+        assert c2.fl_aggregate_async(outs[r]) == sizes[c].sum()
+    c2.fl_synchronize()
+    for r in range(len(cohorts)):
+        assert np.array_equal(outs[r].numpy(), ref[r]), r
+    c2.close()
