@@ -685,8 +685,15 @@ fl_status fl_train_clients(fl_ctx* c, int32_t round_index) {
   // a group of their own on a high-priority stream; the rest of the longest-first order is
   // dealt round-robin into NR groups. Each group is contiguous in execution order and itself
   // longest-first, so its active set in every wave is a prefix.
+  // Solo groups pay off only when the longest client is a sizeable share of the round's work
+  // (its lone-client step latency then sets the round time, e.g. C2: 63 of 819 batches); for a
+  // throughput-bound cohort (C3: 63 of 7,951) their reserved SMs and extra streams cost more
+  // than they save (measured C3 212.3 -> 207.8 ms without them, C2 13.8 -> 15.3 ms).
   const bool cnn_model = (L.model == FL_MODEL_CNN_CIFAR || L.model == FL_MODEL_CNN_SPEECH);
-  const int NS = cnn_model ? (int)std::min<int64_t>(c->nsolo, std::max<int64_t>(0, K - 1)) : 0;
+  int64_t nb_sum = 0;
+  for (int64_t i = 0; i < K; ++i) nb_sum += nb(i);
+  const bool solo_pays = K > 0 && nb(c->exec[0]) * 32 >= nb_sum;
+  const int NS = (cnn_model && solo_pays) ? (int)std::min<int64_t>(c->nsolo, std::max<int64_t>(0, K - 1)) : 0;
   const int NR = cnn_model ? (int)std::max<int64_t>(1, std::min<int64_t>(c->ngroups, K - NS)) : 1;
   const int NG = NS + NR;
   std::vector<int64_t> gsize((size_t)NG, 0);
